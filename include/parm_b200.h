@@ -1,0 +1,111 @@
+/*
+ * parm_b200.h — C ABI of the B200-native Parm MoE-layer hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), is stream-ordered, never synchronises the host and never
+ * allocates: the caller (the PyTorch host layer, or any FFI binding) owns all
+ * memory, including workspaces sized by the *_workspace() queries.  Status is
+ * an int (0 = ok, 1 = bad argument, 2 = launch failure); the message of the
+ * last failure on the calling thread is returned by parm_last_error().
+ *
+ * The reference (/root/reference, `moesched`) is pure Python/NumPy, so it has
+ * no native FFI of its own; each function below cites the reference Python
+ * interface whose work it replaces.  INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef PARM_B200_H
+#define PARM_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARM_ABI_VERSION 1
+
+/* Addressing of a slot tensor split over expert-parallel blocks, expert-
+ * sharding partials (summed in p order) and MP slot shards:
+ *   row(e, s, p) = ptr + (e / e_local) * stride_ep + (e % e_local) * stride_i
+ *                + p * stride_p + (s / slot_div) * stride_shi
+ *                + (s % slot_div) * stride_slo            (element strides)  */
+typedef struct parm_slot_view {
+    const void* ptr; /* bf16 */
+    int e_local;
+    int n_p;
+    int slot_div;
+    int pad_;
+    long long stride_ep;
+    long long stride_i;
+    long long stride_p;
+    long long stride_shi;
+    long long stride_slo;
+} parm_slot_view;
+
+int parm_abi_version(void);
+const char* parm_last_error(void);
+
+/* Gate, forward: logits (f64 accumulation of bf16 inputs), softmax, stable
+ * top-k.  Replaces moesched.dataplane.gate (dataplane.py:86-103).
+ * x: (n, M) bf16 row stride ldx; wg: (M, E) bf16.
+ * Outputs: expert_idx (n, k) int32 in selection order, combine_w (n, k) f32
+ * (= softmax score of the pick), probs (n, E) f32 (nullable). */
+int parm_gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, int k, int* expert_idx,
+                  float* combine_w, float* probs, void* stream);
+
+/* Gate, slot pass: token-major capacity fill (dataplane.py:104-116).
+ * slot_idx (n, k) int32 (-1 = dropped); slot_src (E, cap) int32 = t*k+j of
+ * the pick occupying (e, slot) or -1; fill (E) = filled slots per expert. */
+int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
+                    void* stream);
+
+/* Dispatch build by gather: out[e][s'] = x[t] (times scale[t*k+j] when scale
+ * is non-null) for the pick in slot s = slot_lo + s', zeros when unfilled or
+ * s >= cap.  Writes straight into an AlltoAll send layout.  Replaces the
+ * GateOutput.dispatch fill (dataplane.py:101,112) and S2's slot split + pad
+ * (dataplane.py:373-378); with scale it is the adjoint of the combine. */
+int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
+                       int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
+                       long long out_stride_s, void* stream);
+
+/* Combine: out[t] = sum_j combine_w[t,j] * sum_p Y_p[e_j, s_j] (dropped
+ * picks contribute 0).  Fuses fused_combine's local ESP sum
+ * (collectives.py:296-310) with _combine (dataplane.py:131-143). */
+int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
+                     int n, int k, int M, void* out, long long ldo, void* stream);
+
+/* Combine backward: dlogits (n, E) f32 through the softmax scores of the kept
+ * picks.  No reference counterpart (the reference has no backward). */
+int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
+                     const int* slot_idx, const float* probs, int n, int k, int E, int M, float* dlogits,
+                     void* stream);
+
+/* Dispatch backward: dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
+ * (dlogits nullable).  Adjoint of the dump + dispatch fill. */
+int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
+                      const void* wg, int n, int k, int E, int M, void* dx, long long ldx, void* stream);
+
+/* S2: out (E, slots, M) = sum_p Y_p[e, s], the ESP sum of fused_combine
+ * (collectives.py:302-310) materialised before the MP AllGather. */
+int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, void* stream);
+
+/* Gate weight gradient dWg (M, E) f32 = x^T dlogits (deterministic two-pass).
+ * accumulate != 0 adds into dwg. */
+size_t parm_gate_wgrad_workspace(int n, int M, int E);
+int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, void* workspace,
+                    size_t workspace_bytes, float* dwg, int accumulate, void* stream);
+
+/* Grouped tcgen05 GEMM D_g = A_g * B_g^T over `groups` experts, bf16 in,
+ * f32 accumulate.  major_*: 0 = K-major ([g][mn][k]), 1 = MN-major
+ * ([g][k][mn]).  epi: 0 bf16, 1 relu->bf16, 2 mask by aux>0 -> bf16,
+ * 3 f32, 4 f32 accumulate.  Requires M%128 == 0, N%64 == 0, K%64 == 0.
+ * Replaces expert_shard_forward (dataplane.py:122-128) and its adjoints. */
+int parm_grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A,
+                      long long lda, long long gsa, const void* B, long long ldb, long long gsb, void* D,
+                      long long ldd, long long gsd, const void* aux, long long ld_aux, long long gs_aux,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARM_B200_H */

@@ -1,0 +1,101 @@
+"""ctypes binding of the C ABI in ``include/parm_b200.h`` (``libparm_b200.so``).
+
+This is the only way the host layer reaches the GPU kernels.  There is no
+fallback: if the library is missing or cannot load, every op raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libparm_b200.so"
+
+_c_int = ctypes.c_int
+_c_ll = ctypes.c_longlong
+_vp = ctypes.c_void_p
+_size = ctypes.c_size_t
+
+
+class SlotViewC(ctypes.Structure):
+    _fields_ = [
+        ("ptr", _vp),
+        ("e_local", _c_int),
+        ("n_p", _c_int),
+        ("slot_div", _c_int),
+        ("pad_", _c_int),
+        ("stride_ep", _c_ll),
+        ("stride_i", _c_ll),
+        ("stride_p", _c_ll),
+        ("stride_shi", _c_ll),
+        ("stride_slo", _c_ll),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/parm_b200.h exactly.
+SIGNATURES = {
+    "parm_abi_version": (_c_int, []),
+    "parm_last_error": (ctypes.c_char_p, []),
+    "parm_gate_fwd": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "parm_gate_slots": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "parm_dispatch_rows": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
+                                    _c_ll, _c_ll, _vp]),
+    "parm_combine_fwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_ll,
+                                  _vp]),
+    "parm_combine_bwd": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
+                                  _c_int, _vp, _vp]),
+    "parm_dispatch_bwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
+                                   _vp, _c_ll, _vp]),
+    "parm_esp_sum": (_c_int, [ctypes.POINTER(SlotViewC), _c_int, _c_int, _c_int, _vp, _vp]),
+    "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
+    "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
+    "parm_grouped_gemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_ll, _vp,
+                                   _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp]),
+}
+
+ABI_VERSION = 1
+
+
+class ParmError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+
+class ParmArgError(ParmError, ValueError):
+    """Status 1: argument validation failed inside the library."""
+
+
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library; raise loudly when it is absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise ImportError(
+            f"{p} is missing: build it with `python -m paper_2407_00599_b200.build` (or __graft_entry__.build()); "
+            "there is no CPU fallback for the Parm MoE kernels")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.parm_abi_version() != ABI_VERSION:
+        raise ImportError(f"{p}: ABI version {lib.parm_abi_version()} != {ABI_VERSION}")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.parm_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ParmArgError(msg)
+        raise ParmError(f"{name} failed ({rc}): {msg}")

@@ -1,0 +1,124 @@
+// extern "C" boundary: plain pointers/sizes in, int status out (include/parm_b200.h).
+#include <cstdarg>
+#include <cstring>
+
+#include "../../include/parm_b200.h"
+#include "common.cuh"
+
+namespace parm {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+const char* last_error() { return g_err; }
+
+int gate_fwd(const void*, long long, const void*, int, int, int, int, int*, float*, float*, cudaStream_t);
+int gate_slots(const int*, int, int, int, int, int*, int*, int*, cudaStream_t);
+size_t gate_wgrad_workspace(int, int, int);
+int gate_wgrad(const void*, long long, const float*, int, int, int, float*, size_t, float*, int, cudaStream_t);
+int dispatch_rows(const void*, long long, const int*, const float*, int, int, int, int, int, int, void*, long long,
+                  long long, cudaStream_t);
+int combine_fwd(const SlotView&, const int*, const int*, const float*, int, int, int, void*, long long, cudaStream_t);
+int combine_bwd(const void*, long long, const SlotView&, const int*, const int*, const float*, int, int, int, int,
+                float*, cudaStream_t);
+int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int, void*,
+                 long long, cudaStream_t);
+int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
+int grouped_gemm(int, int, int, int, int, int, int, const void*, long long, long long, const void*, long long,
+                 long long, void*, long long, long long, const void*, long long, long long, cudaStream_t);
+
+static SlotView to_view(const parm_slot_view* v) {
+    SlotView s;
+    static_assert(sizeof(SlotView) == sizeof(parm_slot_view), "slot view ABI mismatch");
+    std::memcpy(&s, v, sizeof(s));
+    return s;
+}
+
+}  // namespace parm
+
+using parm::to_view;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int parm_abi_version(void) { return PARM_ABI_VERSION; }
+
+const char* parm_last_error(void) { return parm::last_error(); }
+
+int parm_gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, int k, int* expert_idx,
+                  float* combine_w, float* probs, void* stream) {
+    return parm::gate_fwd(x, ldx, wg, n, M, E, k, expert_idx, combine_w, probs, S(stream));
+}
+
+int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
+                    void* stream) {
+    return parm::gate_slots(expert_idx, n, k, E, cap, slot_idx, slot_src, fill, S(stream));
+}
+
+int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
+                       int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
+                       long long out_stride_s, void* stream) {
+    return parm::dispatch_rows(x, ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, out, out_stride_e,
+                               out_stride_s, S(stream));
+}
+
+int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
+                     int n, int k, int M, void* out, long long ldo, void* stream) {
+    if (!y) {
+        parm::set_error("combine_fwd: null slot view");
+        return 1;
+    }
+    return parm::combine_fwd(to_view(y), expert_idx, slot_idx, combine_w, n, k, M, out, ldo, S(stream));
+}
+
+int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
+                     const int* slot_idx, const float* probs, int n, int k, int E, int M, float* dlogits,
+                     void* stream) {
+    if (!y) {
+        parm::set_error("combine_bwd: null slot view");
+        return 1;
+    }
+    return parm::combine_bwd(dout, ld_dout, to_view(y), expert_idx, slot_idx, probs, n, k, E, M, dlogits, S(stream));
+}
+
+int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
+                      const void* wg, int n, int k, int E, int M, void* dx, long long ldx, void* stream) {
+    if (!dr) {
+        parm::set_error("dispatch_bwd: null slot view");
+        return 1;
+    }
+    return parm::dispatch_bwd(to_view(dr), expert_idx, slot_idx, dlogits, wg, n, k, E, M, dx, ldx, S(stream));
+}
+
+int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, void* stream) {
+    if (!y) {
+        parm::set_error("esp_sum: null slot view");
+        return 1;
+    }
+    return parm::esp_sum(to_view(y), E, slots, M, out, S(stream));
+}
+
+size_t parm_gate_wgrad_workspace(int n, int M, int E) { return parm::gate_wgrad_workspace(n, M, E); }
+
+int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, void* workspace,
+                    size_t workspace_bytes, float* dwg, int accumulate, void* stream) {
+    return parm::gate_wgrad(x, ldx, dlogits, n, M, E, reinterpret_cast<float*>(workspace), workspace_bytes, dwg,
+                            accumulate, S(stream));
+}
+
+int parm_grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A,
+                      long long lda, long long gsa, const void* B, long long ldb, long long gsb, void* D,
+                      long long ldd, long long gsd, const void* aux, long long ld_aux, long long gs_aux,
+                      void* stream) {
+    return parm::grouped_gemm(major_a, major_b, epi, M, N, K, groups, A, lda, gsa, B, ldb, gsb, D, ldd, gsd, aux,
+                              ld_aux, gs_aux, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// Shared device/host helpers for the Parm B200 MoE-layer kernels (sm_100a only).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "paper_2407_00599_b200 kernels are written for sm_100a only"
+#endif
+
+namespace parm {
+
+using bf16 = __nv_bfloat16;
+
+// Host-side error channel behind parm_last_error(); thread-local so rank
+// threads never see each other's messages.
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define PARM_CHECK_ARG(cond, ...)                 \
+    do {                                          \
+        if (!(cond)) {                            \
+            ::parm::set_error(__VA_ARGS__);       \
+            return 1;                             \
+        }                                         \
+    } while (0)
+
+#define PARM_CHECK_LAUNCH(what)                                                   \
+    do {                                                                          \
+        cudaError_t e__ = cudaGetLastError();                                     \
+        if (e__ != cudaSuccess) {                                                 \
+            ::parm::set_error("%s: launch failed: %s", what, cudaGetErrorString(e__)); \
+            return 2;                                                             \
+        }                                                                         \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+__device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
+
+// 16-byte vector of 8 bf16 values.
+struct alignas(16) Vec8 {
+    __nv_bfloat162 h[4];
+};
+
+__device__ __forceinline__ Vec8 ld_vec8(const bf16* p) {
+    Vec8 v;
+    *reinterpret_cast<int4*>(&v) = __ldg(reinterpret_cast<const int4*>(p));
+    return v;
+}
+
+__device__ __forceinline__ void st_vec8(bf16* p, const Vec8& v) {
+    *reinterpret_cast<int4*>(p) = *reinterpret_cast<const int4*>(&v);
+}
+
+__device__ __forceinline__ void vec8_to_f32(const Vec8& v, float* f) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 t = __bfloat1622float2(v.h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+__device__ __forceinline__ Vec8 f32_to_vec8(const float* f) {
+    Vec8 v;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v.h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+// Addressing of a slot tensor that may be split across expert-parallel
+// blocks, expert-sharding partial sources and MP slot shards.  Row of
+// (expert e, slot s, partial p) lives at
+//   ptr + (e / e_local) * stride_ep + (e % e_local) * stride_i + p * stride_p
+//       + (s / slot_div) * stride_shi + (s % slot_div) * stride_slo
+// (strides in elements).  Covers every receive layout the three schedules
+// produce; n_p partials are summed in p order.
+struct SlotView {
+    const bf16* ptr;
+    int e_local;
+    int n_p;
+    int slot_div;
+    int pad_;
+    long long stride_ep;
+    long long stride_i;
+    long long stride_p;
+    long long stride_shi;
+    long long stride_slo;
+};
+
+__device__ __forceinline__ long long slot_offset(const SlotView& v, int e, int s, int p) {
+    int ep = e / v.e_local;
+    int i = e - ep * v.e_local;
+    int shi = s / v.slot_div;
+    int slo = s - shi * v.slot_div;
+    return (long long)ep * v.stride_ep + (long long)i * v.stride_i + (long long)p * v.stride_p +
+           (long long)shi * v.stride_shi + (long long)slo * v.stride_slo;
+}
+
+}  // namespace parm

@@ -1,0 +1,168 @@
+"""Thin typed wrappers: torch device tensors -> C-ABI calls on the current stream.
+
+Each wrapper validates dtypes/devices/contiguity on the host (cheap) and hands
+raw pointers to ``libparm_b200.so``.  Nothing here computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+KMAJOR, MNMAJOR = 0, 1
+EPI_BF16, EPI_RELU, EPI_DRELU, EPI_F32, EPI_F32_ACC = 0, 1, 2, 3, 4
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+@dataclass
+class SlotView:
+    """Python side of ``parm_slot_view`` (see include/parm_b200.h)."""
+
+    base: torch.Tensor           # bf16 storage the strides index into
+    e_local: int
+    n_p: int = 1
+    slot_div: int = 1 << 30
+    stride_ep: int = 0
+    stride_i: int = 0
+    stride_p: int = 0
+    stride_shi: int = 0
+    stride_slo: int = 0
+    offset: int = 0              # element offset added to base
+
+    def c(self) -> _lib.SlotViewC:
+        _need(self.base, torch.bfloat16, "slot view base")
+        return _lib.SlotViewC(self.base.data_ptr() + 2 * self.offset, self.e_local, self.n_p, self.slot_div, 0,
+                              self.stride_ep, self.stride_i, self.stride_p, self.stride_shi, self.stride_slo)
+
+
+def plain_view(t: torch.Tensor, e_local: int | None = None) -> SlotView:
+    """(E, S, M) contiguous slot tensor, one partial."""
+    E, S, M = t.shape
+    el = E if e_local is None else e_local
+    return SlotView(t, e_local=el, stride_ep=el * S * M, stride_i=S * M, stride_slo=M)
+
+
+def gate_fwd(x: torch.Tensor, wg: torch.Tensor, k: int, expert_idx: torch.Tensor, combine_w: torch.Tensor,
+             probs: torch.Tensor | None) -> None:
+    _need(x, torch.bfloat16, "tokens")
+    _need(wg, torch.bfloat16, "gate weights")
+    n, M = x.shape
+    E = wg.shape[1]
+    if x.stride(1) != 1 or not wg.is_contiguous():
+        raise ValueError("tokens rows and gate weights must be contiguous")
+    _lib.call("parm_gate_fwd", x.data_ptr(), x.stride(0), wg.data_ptr(), n, M, E, k, expert_idx.data_ptr(),
+              combine_w.data_ptr(), _ptr(probs), _stream())
+
+
+def gate_slots(expert_idx: torch.Tensor, E: int, cap: int, slot_idx: torch.Tensor, slot_src: torch.Tensor,
+               fill: torch.Tensor) -> None:
+    n, k = expert_idx.shape
+    _lib.call("parm_gate_slots", expert_idx.data_ptr(), n, k, E, cap, slot_idx.data_ptr(), slot_src.data_ptr(),
+              fill.data_ptr(), _stream())
+
+
+def dispatch_rows(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, out: torch.Tensor,
+                  scale: torch.Tensor | None = None) -> None:
+    """out: (E, S_out, M) view (any strides with unit inner stride)."""
+    _need(x, torch.bfloat16, "rows source")
+    _need(out, torch.bfloat16, "dispatch out")
+    E, S, M = out.shape
+    if out.stride(2) != 1 or x.stride(1) != 1:
+        raise ValueError("dispatch rows need unit inner stride")
+    _lib.call("parm_dispatch_rows", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
+              slot_lo, S, M, out.data_ptr(), out.stride(0), out.stride(1), _stream())
+
+
+def combine_fwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,
+                out: torch.Tensor) -> None:
+    n, M = out.shape
+    k = expert_idx.shape[1]
+    v = view.c()
+    _lib.call("parm_combine_fwd", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(),
+              combine_w.data_ptr(), n, k, M, out.data_ptr(), out.stride(0), _stream())
+
+
+def combine_bwd(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor,
+                probs: torch.Tensor, dlogits: torch.Tensor) -> None:
+    n, M = dout.shape
+    k = expert_idx.shape[1]
+    E = probs.shape[1]
+    v = view.c()
+    _lib.call("parm_combine_bwd", dout.data_ptr(), dout.stride(0), ctypes.byref(v), expert_idx.data_ptr(),
+              slot_idx.data_ptr(), probs.data_ptr(), n, k, E, M, dlogits.data_ptr(), _stream())
+
+
+def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, dlogits: torch.Tensor | None,
+                 wg: torch.Tensor | None, E: int, dx: torch.Tensor) -> None:
+    n, M = dx.shape
+    k = expert_idx.shape[1]
+    v = view.c()
+    _lib.call("parm_dispatch_bwd", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(), _ptr(dlogits),
+              _ptr(wg), n, k, E, M, dx.data_ptr(), dx.stride(0), _stream())
+
+
+def esp_sum(view: SlotView, out: torch.Tensor) -> None:
+    E, S, M = out.shape
+    v = view.c()
+    _lib.call("parm_esp_sum", ctypes.byref(v), E, S, M, out.data_ptr(), _stream())
+
+
+def gate_wgrad_workspace(n: int, M: int, E: int) -> int:
+    return int(_lib.load().parm_gate_wgrad_workspace(n, M, E))
+
+
+def gate_wgrad(x: torch.Tensor, dlogits: torch.Tensor, dwg: torch.Tensor, workspace: torch.Tensor,
+               accumulate: bool = False) -> None:
+    n, M = x.shape
+    E = dlogits.shape[1]
+    _lib.call("parm_gate_wgrad", x.data_ptr(), x.stride(0), dlogits.data_ptr(), n, M, E, workspace.data_ptr(),
+              workspace.numel() * workspace.element_size(), dwg.data_ptr(), int(accumulate), _stream())
+
+
+def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d: torch.Tensor, epi: int,
+                 aux: torch.Tensor | None = None) -> None:
+    """D_g = A_g B_g^T for 3-D (G, rows, cols) operands.
+
+    K-major A is (G, M, K); MN-major A is (G, K, M).  Same for B with N.
+    D is (G, M, N) bf16 or f32 according to ``epi``.
+    """
+    _need(a, torch.bfloat16, "A")
+    _need(b, torch.bfloat16, "B")
+    G = a.shape[0]
+    if major_a == KMAJOR:
+        M, K = a.shape[1], a.shape[2]
+    else:
+        K, M = a.shape[1], a.shape[2]
+    N = b.shape[1] if major_b == KMAJOR else b.shape[2]
+    Kb = b.shape[2] if major_b == KMAJOR else b.shape[1]
+    if Kb != K or b.shape[0] != G or tuple(d.shape) != (G, M, N):
+        raise ValueError(f"grouped_gemm shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
+    for t, nm in ((a, "A"), (b, "B"), (d, "D")):
+        if t.stride(2) != 1:
+            raise ValueError(f"{nm} needs a unit inner stride")
+    want = torch.float32 if epi in (EPI_F32, EPI_F32_ACC) else torch.bfloat16
+    _need(d, want, "D")
+    if aux is not None:
+        _need(aux, torch.bfloat16, "aux")
+    _lib.call("parm_grouped_gemm", major_a, major_b, epi, M, N, K, G, a.data_ptr(), a.stride(1), a.stride(0),
+              b.data_ptr(), b.stride(1), b.stride(0), d.data_ptr(), d.stride(1), d.stride(0), _ptr(aux),
+              aux.stride(1) if aux is not None else 0, aux.stride(0) if aux is not None else 0, _stream())
