@@ -97,12 +97,12 @@ int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, i
 /* Grouped tcgen05 GEMM D_g = A_g * B_g^T over `groups` experts, bf16 in,
  * f32 accumulate.  major_*: 0 = K-major ([g][mn][k]), 1 = MN-major
  * ([g][k][mn]).  epi: 0 bf16, 1 relu->bf16, 2 mask by aux>0 -> bf16,
- * 3 f32, 4 f32 accumulate.  Requires M%128 == 0, N%64 == 0, K%64 == 0.
+ * 3 f32, 4 f32 accumulate; the product is scaled by alpha.  Requires M%128 == 0, N%64 == 0, K%64 == 0.
  * Replaces expert_shard_forward (dataplane.py:122-128) and its adjoints. */
 int parm_grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A,
                       long long lda, long long gsa, const void* B, long long ldb, long long gsb, void* D,
                       long long ldd, long long gsd, const void* aux, long long ld_aux, long long gs_aux,
-                      void* stream);
+                      float alpha, void* stream);
 
 #ifdef __cplusplus
 }

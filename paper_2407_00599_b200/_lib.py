@@ -52,7 +52,7 @@ SIGNATURES = {
     "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
     "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
     "parm_grouped_gemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_ll, _vp,
-                                   _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp]),
+                                   _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp, _c_ll, _c_ll, ctypes.c_float, _vp]),
 }
 
 ABI_VERSION = 1

@@ -50,6 +50,7 @@ struct Params {
     long long ldd, gsd;         // D row stride / group stride (elements)
     const bf16* aux;            // relu mask source for kEpiDReluBF16 (same shape as D)
     long long ld_aux, gs_aux;
+    float alpha;                // D = alpha * A B^T (+ D for kEpiF32Acc)
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -310,8 +311,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float* dst = reinterpret_cast<float*>(p.D) + (long long)g * p.gsd + (long long)row * p.ldd + col;
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
-                        float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                               __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                        float4 o = make_float4(p.alpha * __uint_as_float(r[4 * v]),
+                                               p.alpha * __uint_as_float(r[4 * v + 1]),
+                                               p.alpha * __uint_as_float(r[4 * v + 2]),
+                                               p.alpha * __uint_as_float(r[4 * v + 3]));
                         if (EPI == kEpiF32Acc) {
                             float4 prev = reinterpret_cast<float4*>(dst)[v];
                             o.x += prev.x;
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     bf16* dst = reinterpret_cast<bf16*>(p.D) + (long long)g * p.gsd + (long long)row * p.ldd + col;
                     float f[32];
 #pragma unroll
-                    for (int v = 0; v < 32; ++v) f[v] = __uint_as_float(r[v]);
+                    for (int v = 0; v < 32; ++v) f[v] = p.alpha * __uint_as_float(r[v]);
                     if (EPI == kEpiReluBF16) {
 #pragma unroll
                         for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
@@ -418,7 +421,7 @@ static int dispatch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, con
 // Public entry (wrapped by the C ABI in capi.cu).
 int grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A, long long lda,
                  long long gsa, const void* B, long long ldb, long long gsb, void* D, long long ldd, long long gsd,
-                 const void* aux, long long ld_aux, long long gs_aux, cudaStream_t stream) {
+                 const void* aux, long long ld_aux, long long gs_aux, float alpha, cudaStream_t stream) {
     using namespace gemm;
     PARM_CHECK_ARG(M > 0 && N > 0 && K > 0 && groups > 0, "gemm: empty problem M=%d N=%d K=%d G=%d", M, N, K, groups);
     PARM_CHECK_ARG(M % BM == 0, "gemm: M=%d must be a multiple of %d", M, BM);
@@ -454,6 +457,7 @@ int grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int gro
     p.aux = reinterpret_cast<const bf16*>(aux);
     p.ld_aux = ld_aux;
     p.gs_aux = gs_aux;
+    p.alpha = alpha;
     const int combo = major_a * 2 + major_b;
     switch (combo) {
         case 0:  // K,K : forward GEMMs

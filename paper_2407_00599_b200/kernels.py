@@ -139,7 +139,7 @@ def gate_wgrad(x: torch.Tensor, dlogits: torch.Tensor, dwg: torch.Tensor, worksp
 
 
 def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d: torch.Tensor, epi: int,
-                 aux: torch.Tensor | None = None) -> None:
+                 aux: torch.Tensor | None = None, alpha: float = 1.0) -> None:
     """D_g = A_g B_g^T for 3-D (G, rows, cols) operands.
 
     K-major A is (G, M, K); MN-major A is (G, K, M).  Same for B with N.
@@ -165,4 +165,5 @@ def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d
         _need(aux, torch.bfloat16, "aux")
     _lib.call("parm_grouped_gemm", major_a, major_b, epi, M, N, K, G, a.data_ptr(), a.stride(1), a.stride(0),
               b.data_ptr(), b.stride(1), b.stride(0), d.data_ptr(), d.stride(1), d.stride(0), _ptr(aux),
-              aux.stride(1) if aux is not None else 0, aux.stride(0) if aux is not None else 0, _stream())
+              aux.stride(1) if aux is not None else 0, aux.stride(0) if aux is not None else 0, float(alpha),
+              _stream())

@@ -1,0 +1,183 @@
+"""Generate golden fixtures by running the REAL reference (moesched) in the build container.
+
+    python tests/golden/make_golden.py      # needs /root/reference (read-only import)
+
+Outputs ``tests/golden/golden.npz`` + ``tests/golden/golden_meta.json``.  These pin
+``oracle/moe_oracle.py`` (and the host-side config/trace/cost logic) to the
+reference; the GPU box never needs /root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+
+from moesched import collectives as C  # noqa: E402
+from moesched import config as CF  # noqa: E402
+from moesched import costs as K  # noqa: E402
+from moesched import dataplane as D  # noqa: E402
+from moesched.cli import SweepGrid  # noqa: E402
+
+from oracle.moe_oracle import round_bf16  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+arrays: dict[str, np.ndarray] = {}
+meta: dict = {"gate": [], "forward": [], "schedules": [], "collectives": [], "costs": {}}
+
+
+def put(name: str, a) -> str:
+    arrays[name] = np.asarray(a)
+    return name
+
+
+def gate_case(name, tokens, weights, k, cap, offset=0):
+    g = D.gate(tokens, weights, k, cap, token_offset=offset)
+    meta["gate"].append({
+        "name": name, "k": k, "cap": cap, "offset": offset,
+        "tokens": put(f"gate/{name}/tokens", tokens), "weights": put(f"gate/{name}/weights", weights),
+        "expert_index": put(f"gate/{name}/expert_index", g.expert_index),
+        "slot_index": put(f"gate/{name}/slot_index", g.slot_index),
+        "combine_weights": put(f"gate/{name}/combine_weights", g.combine_weights),
+        "dropped": sorted([list(x) for x in g.dropped]),
+        "dispatch_sum": float(g.dispatch.sum()),
+    })
+
+
+# ---- gate known-answer cases (test_dataplane.py:27-72) and bf16 random cases
+gate_case("tie", np.ones((5, 3)), np.zeros((3, 2)), 1, 5)
+rng = np.random.default_rng(1)
+gate_case("overflow", rng.normal(size=(4, 3)), rng.normal(size=(3, 2)), 1, 1)
+rng = np.random.default_rng(0)
+gate_case("full_k2", rng.normal(size=(6, 3)), rng.normal(size=(3, 2)), 2, 6)
+for seed, (n, M, E, k, cap) in enumerate([(512, 256, 4, 2, 308), (512, 256, 4, 2, 100), (256, 64, 8, 2, 40),
+                                          (300, 128, 16, 4, 90), (1000, 64, 32, 2, 70)]):
+    r = np.random.default_rng(100 + seed)
+    x = round_bf16(r.normal(size=(n, M)))
+    w = round_bf16(r.normal(size=(M, E)))
+    gate_case(f"bf16_{seed}", x, w, k, cap, offset=7 * seed)
+
+# ---- reference_forward: the published golden vector + a bf16 block
+cfg = CF.MoEConfig(1, 8, 4, 4, 2, 1, 2.0)
+w = D.ExpertWeights.generate(cfg, seed=2024)
+tok = np.random.default_rng(99).normal(size=(8, 4))
+meta["forward"].append({"name": "golden_vector", "cfg": [1, 8, 4, 4, 2, 1, 2.0], "weight_seed": 2024,
+                        "tokens": put("fwd/golden/tokens", tok),
+                        "out": put("fwd/golden/out", D.reference_forward(cfg, w, tok))})
+cfg = CF.MoEConfig(2, 64, 64, 128, 4, 2, 1.2)
+w = D.ExpertWeights.generate(cfg, seed=3)
+wb = D.ExpertWeights(round_bf16(w.gate), round_bf16(w.w1), round_bf16(w.w2))
+tok = round_bf16(np.random.default_rng(4).normal(size=(128, 64)))
+meta["forward"].append({"name": "bf16_block", "cfg": [2, 64, 64, 128, 4, 2, 1.2], "weight_seed": 3,
+                        "tokens": put("fwd/bf16/tokens", tok), "gate": put("fwd/bf16/gate", wb.gate),
+                        "w1": put("fwd/bf16/w1", wb.w1), "w2": put("fwd/bf16/w2", wb.w2),
+                        "out": put("fwd/bf16/out", D.reference_forward(cfg, wb, tok))})
+
+
+# ---- run_schedule on small worlds (outputs, traces, drops, ffn_rows)
+def sched_case(name, cfg_t, layout_t, seed, esp_contiguous=True, bf16=False, store_outputs=True):
+    cfg = CF.MoEConfig(*cfg_t)
+    lay = CF.ParallelLayout(*layout_t, esp_contiguous=esp_contiguous)
+    cluster = CF.ClusterSpec(1, lay.world_size, 4e-10, 4e-9)
+    w = D.ExpertWeights.generate(cfg, seed=seed)
+    inputs = np.random.default_rng(seed + 1).normal(size=(lay.world_size // lay.mp_size, cfg.tokens_per_rank,
+                                                          cfg.embed_dim))
+    if bf16:
+        w = D.ExpertWeights(round_bf16(w.gate), round_bf16(w.w1), round_bf16(w.w2))
+        inputs = round_bf16(inputs)
+    entry = {"name": name, "cfg": list(cfg_t), "layout": list(layout_t), "esp_contiguous": esp_contiguous,
+             "seed": seed, "bf16": bf16, "capacity": CF.derive_capacity(cfg), "results": {}}
+    for s in D.SCHEDULES:
+        res = D.run_schedule(s, cfg, lay, cluster, w, inputs)
+        out = res.outputs
+        rec = {
+            "trace": [[r.collective, r.group, r.group_size, r.elements, r.wire_per_rank, r.phases, r.overlapped]
+                      for r in res.trace],
+            "dropped": sorted([list(x) for x in res.dropped]),
+            "ffn_rows": res.ffn_rows,
+            "oracle_error": D.oracle_errors(cfg, lay, w, inputs, res),
+            "row_sums": put(f"sched/{name}/{s}/row_sums", out.sum(axis=2)),
+        }
+        if store_outputs:
+            rec["outputs"] = put(f"sched/{name}/{s}/outputs", out)
+        entry["results"][s] = rec
+    meta["schedules"].append(entry)
+
+
+sched_case("fig2", (1, 8, 4, 4, 2, 1, 2.0), (2, 2, 2, 4), 4)
+sched_case("fig2_flipped", (1, 8, 4, 4, 2, 1, 2.0), (2, 2, 2, 4), 13, esp_contiguous=False)
+sched_case("overflow_mp1", (1, 4, 4, 4, 2, 1, 0.5), (1, 2, 2, 4), 11)
+sched_case("overflow_mp2", (1, 8, 4, 4, 2, 1, 0.5), (2, 2, 2, 4), 12)
+sched_case("p8_c2shape_small", (2, 16, 16, 32, 8, 2, 1.2), (2, 4, 2, 8), 21)
+sched_case("p8_mp4", (2, 16, 8, 16, 8, 2, 2.4), (4, 8, 1, 8), 22)
+sched_case("p4_ep4", (4, 8, 8, 8, 4, 2, 2.0), (1, 4, 1, 4), 23)
+sched_case("p2_esp2", (4, 8, 8, 16, 4, 2, 1.2), (2, 1, 2, 2), 24)
+# BASELINE config 1 (C1) on bf16-rounded data: routing-bearing row sums only (outputs are 4 MB)
+sched_case("c1_bf16", (4, 128, 256, 512, 4, 2, 1.2), (2, 2, 2, 4), 0, bf16=True, store_outputs=False)
+
+# ---- fused collectives on random worlds
+for ep, esp, mp in [(2, 2, 1), (4, 2, 2), (2, 4, 2), (8, 1, 4), (1, 4, 1)]:
+    P = ep * esp
+    for flip in (True, False):
+        lay = CF.ParallelLayout(mp, ep, esp, P, esp_contiguous=flip)
+        r = np.random.default_rng(P * 10 + ep + (0 if flip else 5))
+        n = P * ep * 3
+        world = C.WorldState([r.normal(size=n) for _ in range(P)])
+        nm = f"coll/ep{ep}_esp{esp}_mp{mp}_{'c' if flip else 'f'}"
+        meta["collectives"].append({
+            "name": nm, "layout": [mp, ep, esp, P], "esp_contiguous": flip,
+            "inputs": put(nm + "/inputs", np.stack(world.buffers)),
+            "fused_dispatch": put(nm + "/fused_dispatch", np.stack(C.fused_dispatch(world, lay).buffers)),
+            "fused_combine": put(nm + "/fused_combine", np.stack(C.fused_combine(world, lay).buffers)),
+            "saa": put(nm + "/saa", np.stack(C.saa(world, lay).buffers)),
+            "alltoall_ep": put(nm + "/alltoall_ep", np.stack(C.alltoall(world, lay, "ep").buffers)),
+            "allgather_esp": put(nm + "/allgather_esp", np.stack(C.allgather(world, lay, "esp").buffers)),
+            "reduce_scatter_esp": put(nm + "/reduce_scatter_esp",
+                                      np.stack(C.reduce_scatter(world, lay, "esp").buffers)),
+            "allreduce_mp": put(nm + "/allreduce_mp", np.stack(C.allreduce(world, lay, "mp").buffers)),
+        })
+
+# ---- cost model / selector
+prof = K.CostProfile()
+vals = {}
+r = np.random.default_rng(7)
+for key in K.ALL_KEYS:
+    a, b = float(r.uniform(1e-5, 1e-4)), float(r.uniform(1e-10, 1e-9))
+    prof.add(K.AlphaBeta(a, b, key[0], key[1]))
+    vals["/".join(key)] = [a, b]
+reports = []
+points, skipped = SweepGrid().run()
+for cid, cfg, lay in points[::37]:
+    rep = K.select_schedule(cfg, lay, prof)
+    lit = K.select_schedule(cfg, lay, prof, alg1_literal=True)
+    reports.append({"id": cid, "cfg": [cfg.samples_per_rank, cfg.seq_len, cfg.embed_dim, cfg.hidden_dim,
+                                       cfg.num_experts, cfg.top_k, cfg.capacity_factor],
+                    "layout": [lay.mp_size, lay.ep_size, lay.esp_size, lay.world_size],
+                    "t": [rep.t_baseline, rep.t_fused, rep.t_s1, rep.t_s2], "chosen": rep.chosen,
+                    "breakdown": rep.breakdown,
+                    "literal_t": [lit.t_s1, lit.t_s2], "literal_chosen": lit.chosen})
+fits = []
+for alpha, beta in ((6.64e-4, 5.38e-10), (1.09e-4, 7.14e-10)):
+    rr = np.random.default_rng(555)
+    xs = np.geomspace(2 ** 10, 2 ** 24, 24)
+    samples = [(float(x), float((alpha + beta * x) * (1 + 0.01 * rr.standard_normal()))) for x in xs for _ in range(8)]
+    ab = K.fit_alpha_beta(samples)
+    fits.append({"samples": samples, "alpha": ab.alpha, "beta": ab.beta, "r2": ab.r_squared,
+                 "clamped": ab.alpha_clamped})
+meta["costs"] = {"profile": vals, "reports": reports, "fits": fits, "grid_points": len(points),
+                 "grid_skipped": skipped,
+                 "grid_points_p8": sum(1 for p in points if p[2].world_size == 8),
+                 "capacity_kat": [CF.derive_capacity(CF.MoEConfig(4, 128, 256, 512, 4, 2, 1.2)),
+                                  CF.derive_capacity(CF.MoEConfig(8, 1024, 1024, 4096, 8, 2, 1.2)),
+                                  CF.derive_capacity(CF.MoEConfig(4, 128, 256, 512, 4, 2, 2.4)),
+                                  CF.derive_capacity(CF.MoEConfig(8, 1024, 1024, 4096, 8, 2, 2.4))]}
+
+np.savez_compressed(OUT / "golden.npz", **arrays)
+(OUT / "golden_meta.json").write_text(json.dumps(meta, indent=1, default=float))
+print("wrote", OUT / "golden.npz", sum(a.nbytes for a in arrays.values()) / 1e6, "MB raw")
