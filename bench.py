@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark: Parm MoE-layer forward+backward on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl parm|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = forward + backward of ONE MoE layer (gate -> dispatch -> expert FFN
+-> combine and its adjoint, weight gradients included) over one batch of
+synthetic tokens of the BASELINE config-2 per-rank shape (B=8 L=1024 M=1024
+H=4096 E=8 top-2 f=1.2), weak-scaled over the measurement plan's layouts
+(BASELINE.md §3): N=1 (MP,EP,ESP)=(1,1,1), N=2 (2,1,2), N=4 (2,2,2),
+N=8 (2,4,2).  The headline schedule is the one the Algorithm-1 selector picks
+with the calibrated NVLink profile (profiles/nvlink_profile.csv, else a
+nominal NVLink profile); baseline/S1/S2 are all timed and reported.
+
+value = distinct tokens processed by the whole job per second
+      = (P / N_MP) * B * L / t_step,  t_step = max over ranks (CUDA events).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE layer fwd+bwd ms & tokens/s at 1/2/4/8 B200; speedup vs baseline sched"
+C2 = dict(samples_per_rank=8, seq_len=1024, embed_dim=1024, hidden_dim=4096, num_experts=8, top_k=2,
+          capacity_factor=1.2)
+LAYOUTS = {1: (1, 1, 1), 2: (2, 1, 2), 4: (2, 2, 2), 8: (2, 4, 2)}   # (MP, EP, ESP)
+CPU_SAMPLE_TOKENS = 2048
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("parm", "reference"), default="parm")
+    ap.add_argument("--schedule", default="auto", help="auto (selector) | baseline | s1 | s2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="time only the headline schedule")
+    return ap.parse_args()
+
+
+def layout_for(n: int):
+    from paper_2407_00599_b200.config import ParallelLayout
+
+    if n not in LAYOUTS:
+        raise SystemExit(f"--gpus must be one of {sorted(LAYOUTS)}")
+    mp, ep, esp = LAYOUTS[n]
+    return ParallelLayout(mp, ep, esp, n)
+
+
+def tokens_per_step(cfg, layout) -> int:
+    return layout.world_size // layout.mp_size * cfg.tokens_per_rank
+
+
+# ---------------------------------------------------------------- reference (CPU) arm
+def oracle_step_rate(cfg, layout, sample_tokens: int, reps: int, warmup: int = 0):
+    """The reference algorithm (oracle port of moesched's data plane + restated
+    backward) on the host cores: fwd+bwd of (P/MP) blocks of ``sample_tokens``
+    tokens with the full M/H/E.  Returns (tokens/s, seconds per step, cores)."""
+    import numpy as np
+
+    from oracle import moe_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        cores = os.cpu_count() or 1
+    M, H, E, k, f = cfg.embed_dim, cfg.hidden_dim, cfg.num_experts, cfg.top_k, cfg.capacity_factor
+    w = O.Weights.generate(M, H, E, seed=0)
+    blocks = layout.world_size // layout.mp_size
+    rng = np.random.default_rng(0)
+    xs = [rng.normal(size=(sample_tokens, M)) for _ in range(blocks)]
+    ds = [rng.normal(size=(sample_tokens, M)) for _ in range(blocks)]
+    cap = O.derive_capacity(sample_tokens, E, k, f)
+
+    def step():
+        for x, d in zip(xs, ds):
+            _, c = O.block_forward(x, w, k, cap)
+            O.block_backward(c, w, d)
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        step()
+    dt = (time.perf_counter() - t0) / reps
+    return blocks * sample_tokens / dt, dt, cores
+
+
+def run_reference_arm(args, rank: int, world: int) -> None:
+    from paper_2407_00599_b200.config import MoEConfig
+
+    if rank != 0:
+        return
+    cfg = MoEConfig(**C2)
+    layout = layout_for(args.gpus)
+    rate, dt, cores = oracle_step_rate(cfg, layout, CPU_SAMPLE_TOKENS, max(1, args.steps), warmup=min(args.warmup, 1))
+    sample = (f"{layout.world_size // layout.mp_size} block(s) x {CPU_SAMPLE_TOKENS} tokens (of "
+              f"{cfg.tokens_per_rank}) per step, full M/H/E, f64 NumPy oracle fwd+bwd")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, layout, "oracle"),
+        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, layout, schedule) -> dict:
+    return {
+        "workload": "BASELINE config 2 per-rank shape: one MoE layer B=8 L=1024 M=1024 H=4096 E=8 top-2 f=1.2",
+        "layout": f"MP={layout.mp_size} EP={layout.ep_size} ESP={layout.esp_size} P={layout.world_size}",
+        "schedule": schedule,
+        "global_batch_tokens": tokens_per_step(cfg, layout),
+        "seq_len": cfg.seq_len,
+        "parallelism": f"mp{layout.mp_size}-ep{layout.ep_size}-esp{layout.esp_size}",
+        "l2": "per-step working set (weights + activations ~0.5 GB/rank) >> 126 MB L2; no explicit flush",
+    }
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.samples: list[list[str]] = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx.append(float(s[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, s[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- GPU arm
+def pick_schedule(cfg, layout, requested: str):
+    from paper_2407_00599_b200 import selector
+
+    if requested != "auto":
+        return requested, None
+    prof_path = ROOT / "profiles" / "nvlink_profile.csv"
+    if prof_path.exists():
+        prof = selector.load_profile(prof_path)
+        src = str(prof_path.relative_to(ROOT))
+    else:
+        prof = selector.CostProfile()
+        beta = 2.0 / 700e9           # bf16 element over ~700 GB/s NVLink (nominal)
+        for c, g in selector.ALL_KEYS:
+            prof.add(selector.AlphaBeta(2e-5, beta, c, g))
+        src = "nominal NVLink profile (alpha 20us, 700 GB/s)"
+    rep = selector.select_schedule(cfg, layout, prof)
+    return rep.chosen, {"profile": src, "t_s1_pred_ms": rep.t_s1 * 1e3, "t_s2_pred_ms": rep.t_s2 * 1e3,
+                        "t_baseline_pred_ms": rep.t_baseline * 1e3}
+
+
+def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev):
+    import torch
+
+    for _ in range(warmup):
+        layer.forward(schedule, xs)
+        layer.backward(ds)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        layer.forward(schedule, xs)
+        layer.backward(ds)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev):
+    """Public-API step with host buffers: H2D of the step's tokens and upstream
+    gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
+    and a D2H read of the step's routing metric (per-expert fill)."""
+    import torch
+
+    r = layer.ranks[0]
+    comp = torch.cuda.current_stream()
+    cps = torch.cuda.Stream()
+    dx = [torch.empty(host_x.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    dd = [torch.empty(host_d.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    metric = torch.empty(layer.d.E, dtype=torch.int32).pin_memory()
+    for f in free:
+        f.record(comp)
+
+    def prefetch(slot):
+        with torch.cuda.stream(cps):
+            cps.wait_event(free[slot])
+            dx[slot].copy_(host_x, non_blocking=True)
+            dd[slot].copy_(host_d, non_blocking=True)
+            ready[slot].record(cps)
+
+    def run(total):
+        prefetch(0)
+        for i in range(total):
+            s = i % 2
+            if i + 1 < total:
+                prefetch((i + 1) % 2)
+            comp.wait_event(ready[s])
+            layer.forward(schedule, {r: dx[s]})
+            layer.backward({r: dd[s]})
+            metric.copy_(layer.routing(r).fill, non_blocking=True)
+            free[s].record(comp)
+
+    run(warmup)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    cps.wait_event(e0)
+    run(steps)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist is not None:
+        dist.barrier()
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = 2 * host_x.numel() * 2
+    d2h = layer.d.E * 4
+    return ms, h2d, d2h
+
+
+def gemm_roofline(layer, schedule, xs, ds, steps, dist, dev):
+    """Average tcgen05 grouped-GEMM launch over `steps` steps, CUDA events on the launching stream."""
+    import torch
+
+    from paper_2407_00599_b200 import kernels as K
+
+    K.gemm_timer = K.GemmTimer()
+    try:
+        for _ in range(steps):
+            layer.forward(schedule, xs)
+            layer.backward(ds)
+        ms, launches, padded_flops = K.gemm_timer.total_ms()
+    finally:
+        K.gemm_timer = None
+    d = layer.d
+    r = layer.ranks[0]
+    b = layer.st[r].bufs[schedule if d.P > 1 else "_local"]
+    useful_rows = int((b["recv"].abs().amax(dim=-1) > 0).sum().item())   # real (kept) assignment rows
+    alg_flops_step = 6 * 2 * useful_rows * d.M * d.Hs                   # 6 GEMMs per step (fwd 2, bwd 4)
+    per_launch_alg = alg_flops_step / 6
+    avg_ms = ms / launches
+    return {"kernel": "grouped_gemm_kernel (tcgen05.mma kind::f16, TMA, TMEM)", "avg_launch_ms": avg_ms,
+            "alg_flops_per_launch": per_launch_alg, "padded_flops_per_launch": padded_flops / launches,
+            "launches": launches, "useful_rows": useful_rows, "gemm_ms_per_step": ms / steps}
+
+
+def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
+    import numpy as np
+    import torch
+
+    from paper_2407_00599_b200 import _lib
+    from paper_2407_00599_b200.config import MoEConfig
+    from paper_2407_00599_b200.runtime import MoELayer
+    from paper_2407_00599_b200.world import LocalWorld, NcclWorld
+
+    dist = None
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=dev)
+        dist = tdist
+    cfg = MoEConfig(**C2)
+    layout = layout_for(args.gpus)
+    if layout.world_size != world:
+        raise SystemExit(f"--gpus {args.gpus} needs {args.gpus} ranks (got {world})")
+    w = NcclWorld(layout, dev) if world > 1 else LocalWorld(layout, dev)
+    layer = MoELayer(cfg, layout, w)
+    layer.init_random(seed=0)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank // layout.mp_size)
+    x = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, generator=g, device=dev).to(torch.bfloat16)
+    dout = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, generator=g, device=dev).to(torch.bfloat16)
+    xs, ds = {rank: x}, {rank: dout}
+
+    schedule, sel = pick_schedule(cfg, layout, args.schedule)
+    others = [] if args.no_compare or layout.world_size == 1 else [s for s in ("baseline", "s1", "s2")
+                                                                     if s != schedule]
+    sched_ms = {}
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    n0 = _lib.launch_count
+    ms = time_steps(layer, schedule, xs, ds, args.steps, args.warmup, dist, dev)
+    launches = (_lib.launch_count - n0) * args.steps // (args.steps + args.warmup)
+    clk = clocks.stop() if clocks else None
+    sched_ms[schedule] = ms
+    for s in others:
+        sched_ms[s] = time_steps(layer, s, xs, ds, args.steps, args.warmup, dist, dev)
+    roof = gemm_roofline(layer, schedule, xs, ds, max(3, min(args.steps, 10)), dist, dev)
+    e2e = None
+    if not args.no_e2e:
+        hx = x.cpu().pin_memory()
+        hd = dout.cpu().pin_memory()
+        e_ms, h2d, d2h = time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev)
+        tps = tokens_per_step(cfg, layout)
+        e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream)"}
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("bf16_tflops_sustained")
+    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
+    if peak is None:
+        peak, peak_src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    achieved = roof["alg_flops_per_launch"] / (roof["avg_launch_ms"] / 1e3) / 1e12
+    traffic = None
+    tfile = ROOT / "profiles" / "gemm_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "kernel": roof["kernel"],
+                "avg_launch_ms": roof["avg_launch_ms"], "launches_sampled": roof["launches"],
+                "alg_flops_per_launch": roof["alg_flops_per_launch"],
+                "executed_tflops": roof["padded_flops_per_launch"] / (roof["avg_launch_ms"] / 1e3) / 1e12,
+                "gemm_share_of_step": roof["gemm_ms_per_step"] / ms,
+                "units": "alg FLOPs = 2 * kept assignment rows * M * (H/N_ESP) per GEMM; 6 GEMMs per step"}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, dt, cores = oracle_step_rate(cfg, layout, CPU_SAMPLE_TOKENS, 3)
+        cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"{CPU_SAMPLE_TOKENS} of {cfg.tokens_per_rank} tokens, full M/H/E, f64 NumPy oracle "
+                         f"fwd+bwd, 3 steps ({dt:.2f} s/step)"}
+    tps = tokens_per_step(cfg, layout)
+    line = {
+        "metric": METRIC, "value": tps / (ms / 1e3), "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) tokens, reference-scaled random weights)",
+        "config": config_block(cfg, layout, schedule),
+        "schedules_ms": sched_ms,
+        "speedup_vs_baseline_schedule": (sched_ms["baseline"] / ms) if "baseline" in sched_ms and
+                                        schedule != "baseline" else None,
+        "selector": sel,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_gpu_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

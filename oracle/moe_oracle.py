@@ -199,8 +199,8 @@ def block_forward(tokens: np.ndarray, w: Weights, k: int, capacity: int, token_o
     E = w.gate.shape[1]
     r = gate(tokens, w.gate, k, capacity, token_offset)
     d = dispatch_tensor(tokens, r, E)
-    h = np.maximum(np.einsum("esm,emh->esh", d, w.w1), 0.0)
-    y = np.einsum("esh,ehm->esm", h, w.w2)
+    h = np.maximum(np.matmul(d, w.w1), 0.0)          # batched BLAS per expert
+    y = np.matmul(h, w.w2)
     out = combine(r, y, tokens.shape[1])
     return out, BlockCache(tokens, r, d, h, y)
 
@@ -243,10 +243,10 @@ def block_backward(c: BlockCache, w: Weights, dout: np.ndarray) -> BlockGrads:
         e, s = r.expert_index[t, j], r.slot_index[t, j]
         dY[e, s] += r.combine_weights[t, j, None] * dout[t]
         dS[t, e] += np.einsum("tm,tm->t", dout[t], c.expert_out[e, s])
-    dH = np.einsum("esm,ehm->esh", dY, w.w2) * (c.hidden > 0)
-    dw2 = np.einsum("esh,esm->ehm", c.hidden, dY)
-    dw1 = np.einsum("esm,esh->emh", c.dispatch, dH)
-    dR = np.einsum("esh,emh->esm", dH, w.w1)
+    dH = np.matmul(dY, w.w2.transpose(0, 2, 1)) * (c.hidden > 0)
+    dw2 = np.matmul(c.hidden.transpose(0, 2, 1), dY)
+    dw1 = np.matmul(c.dispatch.transpose(0, 2, 1), dH)
+    dR = np.matmul(dH, w.w1.transpose(0, 2, 1))
     dx = np.zeros((n, M))
     for j in range(k):
         t = np.nonzero(r.slot_index[:, j] >= 0)[0]

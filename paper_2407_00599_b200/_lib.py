@@ -91,9 +91,16 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     return lib
 
 
+# Kernel launches each entry point issues on success (bench.py's gpu_launches).
+LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     lib = load()
     rc = getattr(lib, name)(*args)
+    launch_count += LAUNCHES_PER_CALL.get(name, 1)
     if rc != 0:
         msg = lib.parm_last_error().decode(errors="replace")
         if rc == 1:

@@ -138,6 +138,26 @@ def gate_wgrad(x: torch.Tensor, dlogits: torch.Tensor, dwg: torch.Tensor, worksp
               workspace.numel() * workspace.element_size(), dwg.data_ptr(), int(accumulate), _stream())
 
 
+class GemmTimer:
+    """Optional CUDA-event bracketing of every grouped GEMM launch (bench.py roofline).
+
+    Events are recorded on the launching (current) stream, so the measured
+    interval is the kernel's own duration in stream order.
+    """
+
+    def __init__(self) -> None:
+        self.pairs: list[tuple[torch.cuda.Event, torch.cuda.Event, int]] = []
+
+    def total_ms(self) -> tuple[float, int, int]:
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b, _ in self.pairs)
+        flops = sum(f for _, _, f in self.pairs)
+        return ms, len(self.pairs), flops
+
+
+gemm_timer: GemmTimer | None = None
+
+
 def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d: torch.Tensor, epi: int,
                  aux: torch.Tensor | None = None, alpha: float = 1.0) -> None:
     """D_g = A_g B_g^T for 3-D (G, rows, cols) operands.
@@ -145,6 +165,21 @@ def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d
     K-major A is (G, M, K); MN-major A is (G, K, M).  Same for B with N.
     D is (G, M, N) bf16 or f32 according to ``epi``.
     """
+    if gemm_timer is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha)
+        e1.record()
+        G, Mx = a.shape[0], (a.shape[1] if major_a == KMAJOR else a.shape[2])
+        Kx = a.shape[2] if major_a == KMAJOR else a.shape[1]
+        Nx = b.shape[1] if major_b == KMAJOR else b.shape[2]
+        gemm_timer.pairs.append((e0, e1, 2 * G * Mx * Nx * Kx))   # executed (padded) FLOPs
+        return
+    _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha)
+
+
+def _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha) -> None:
     _need(a, torch.bfloat16, "A")
     _need(b, torch.bfloat16, "B")
     G = a.shape[0]
