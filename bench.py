@@ -50,6 +50,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="time only the headline schedule")
+    ap.add_argument("--eager", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
 
 
@@ -206,20 +207,27 @@ def pick_schedule(cfg, layout, requested: str):
                         "t_baseline_pred_ms": rep.t_baseline * 1e3}
 
 
-def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev):
+def make_step(layer, schedule, xs, ds, use_graph: bool):
+    """One fwd+bwd step: a replayed CUDA graph (default) or eager launches."""
+    if use_graph:
+        g = layer.capture_step(schedule, xs, ds)
+        return g.replay
+    return lambda: (layer.forward(schedule, xs), layer.backward(ds))
+
+
+def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev, use_graph=True):
     import torch
 
+    step = make_step(layer, schedule, xs, ds, use_graph)
     for _ in range(warmup):
-        layer.forward(schedule, xs)
-        layer.backward(ds)
+        step()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
-        layer.forward(schedule, xs)
-        layer.backward(ds)
+        step()
     e1.record()
     torch.cuda.synchronize()
     if dist is not None:
@@ -232,7 +240,7 @@ def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev):
     return ms
 
 
-def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev):
+def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_graph=True):
     """Public-API step with host buffers: H2D of the step's tokens and upstream
     gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
     and a D2H read of the step's routing metric (per-expert fill)."""
@@ -248,6 +256,7 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev):
     metric = torch.empty(layer.d.E, dtype=torch.int32).pin_memory()
     for f in free:
         f.record(comp)
+    steps_fn = [make_step(layer, schedule, {r: dx[sl]}, {r: dd[sl]}, use_graph) for sl in range(2)]
 
     def prefetch(slot):
         with torch.cuda.stream(cps):
@@ -263,8 +272,7 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev):
             if i + 1 < total:
                 prefetch((i + 1) % 2)
             comp.wait_event(ready[s])
-            layer.forward(schedule, {r: dx[s]})
-            layer.backward({r: dd[s]})
+            steps_fn[s]()
             metric.copy_(layer.routing(r).fill, non_blocking=True)
             free[s].record(comp)
 
@@ -349,19 +357,22 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
                                                                      if s != schedule]
     sched_ms = {}
     clocks = ClockSampler(local_rank) if rank == 0 else None
+    use_graph = not args.eager
     n0 = _lib.launch_count
-    ms = time_steps(layer, schedule, xs, ds, args.steps, args.warmup, dist, dev)
-    launches = (_lib.launch_count - n0) * args.steps // (args.steps + args.warmup)
+    layer.forward(schedule, xs)
+    layer.backward(ds)
+    launches = (_lib.launch_count - n0) * args.steps          # our kernels per step x timed steps
+    ms = time_steps(layer, schedule, xs, ds, args.steps, args.warmup, dist, dev, use_graph)
     clk = clocks.stop() if clocks else None
     sched_ms[schedule] = ms
     for s in others:
-        sched_ms[s] = time_steps(layer, s, xs, ds, args.steps, args.warmup, dist, dev)
+        sched_ms[s] = time_steps(layer, s, xs, ds, args.steps, args.warmup, dist, dev, use_graph)
     roof = gemm_roofline(layer, schedule, xs, ds, max(3, min(args.steps, 10)), dist, dev)
     e2e = None
     if not args.no_e2e:
         hx = x.cpu().pin_memory()
         hd = dout.cpu().pin_memory()
-        e_ms, h2d, d2h = time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev)
+        e_ms, h2d, d2h = time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev, use_graph)
         tps = tokens_per_step(cfg, layout)
         e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
@@ -405,6 +416,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
                                         schedule != "baseline" else None,
         "selector": sel,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "launch_mode": "eager" if args.eager else "cuda_graph (one replay per step; NCCL calls captured)",
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 1
+#define PARM_ABI_VERSION 2
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -46,10 +46,10 @@ const char* parm_last_error(void);
 
 /* Gate, forward: logits (f64 accumulation of bf16 inputs), softmax, stable
  * top-k.  Replaces moesched.dataplane.gate (dataplane.py:86-103).
- * x: (n, M) bf16 row stride ldx; wg: (M, E) bf16.
+ * x: (n, M) bf16 row stride ldx; wg_t: gate weights TRANSPOSED, (E, M) bf16.
  * Outputs: expert_idx (n, k) int32 in selection order, combine_w (n, k) f32
  * (= softmax score of the pick), probs (n, E) f32 (nullable). */
-int parm_gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, int k, int* expert_idx,
+int parm_gate_fwd(const void* x, long long ldx, const void* wg_t, int n, int M, int E, int k, int* expert_idx,
                   float* combine_w, float* probs, void* stream);
 
 /* Gate, slot pass: token-major capacity fill (dataplane.py:104-116).
@@ -80,29 +80,62 @@ int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* 
                      void* stream);
 
 /* Dispatch backward: dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
- * (dlogits nullable).  Adjoint of the dump + dispatch fill. */
+ * (dlogits nullable; wg_t is (E, M)).  Adjoint of the dump + dispatch fill. */
 int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
-                      const void* wg, int n, int k, int E, int M, void* dx, long long ldx, void* stream);
+                      const void* wg_t, int n, int k, int E, int M, void* dx, long long ldx, void* stream);
 
 /* S2: out (E, slots, M) = sum_p Y_p[e, s], the ESP sum of fused_combine
  * (collectives.py:302-310) materialised before the MP AllGather. */
 int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, void* stream);
 
-/* Gate weight gradient dWg (M, E) f32 = x^T dlogits (deterministic two-pass).
+/* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic two-pass).
  * accumulate != 0 adds into dwg. */
 size_t parm_gate_wgrad_workspace(int n, int M, int E);
 int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, void* workspace,
-                    size_t workspace_bytes, float* dwg, int accumulate, void* stream);
+                    size_t workspace_bytes, float* dwg_t, int accumulate, void* stream);
 
-/* Grouped tcgen05 GEMM D_g = A_g * B_g^T over `groups` experts, bf16 in,
- * f32 accumulate.  major_*: 0 = K-major ([g][mn][k]), 1 = MN-major
- * ([g][k][mn]).  epi: 0 bf16, 1 relu->bf16, 2 mask by aux>0 -> bf16,
- * 3 f32, 4 f32 accumulate; the product is scaled by alpha.  Requires M%128 == 0, N%64 == 0, K%64 == 0.
+/* A bf16/f32 tensor addressed as [hi][lo][g][row][col]: element (hi, lo, g, r, c)
+ * at ptr + hi*hi_stride + lo*lo_stride + g*g_stride + r*ld + c (element strides).
+ * Plain 3-D [g][row][col] tensors set hi/lo strides to 0 (nhi = nlo = 1). */
+typedef struct parm_rows {
+    const void* ptr;
+    long long ld;
+    long long g_stride;
+    long long lo_stride;
+    long long hi_stride;
+} parm_rows;
+
+/* Grouped tcgen05/TMEM/TMA GEMM over the MoE layer's segmented expert rows
+ * (every row tensor is the AlltoAll receive layout [src_hi][src_lo][expert][r < seg_len][col]).
+ * kind 0 (ROW):  D[hi][lo][g][r][n] = alpha * sum_k A[hi][lo][g][r][k] * B[g][n][k]
+ *                b_major 0: B stored [g][n][k]; 1: B stored [g][k][n].  K, N % 64 == 0.
+ *                epi 0 bf16, 1 relu -> bf16, 2 keep where aux > 0 -> bf16 (aux shaped like D).
+ * kind 1 (WGT):  D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n]
+ *                M % 128 == 0, N % 64 == 0; epi 3 f32, 4 f32 accumulate.
+ * fill (nullable, int32 [hi][lo][g]): rows >= fill of a segment are skipped
+ * (capacity padding); they must be zero in A for ROW partial tiles.
  * Replaces expert_shard_forward (dataplane.py:122-128) and its adjoints. */
-int parm_grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A,
-                      long long lda, long long gsa, const void* B, long long ldb, long long gsb, void* D,
-                      long long ldd, long long gsd, const void* aux, long long ld_aux, long long gs_aux,
-                      float alpha, void* stream);
+typedef struct parm_gemm_desc {
+    int kind;
+    int epi;
+    int b_major;
+    int groups;
+    int nhi;
+    int nlo;
+    int seg_len;
+    int M;
+    int N;
+    int K;
+    float alpha;
+    int pad_;
+    parm_rows a;
+    parm_rows b;
+    parm_rows d;
+    parm_rows aux;
+    const int* fill;
+} parm_gemm_desc;
+
+int parm_gemm(const parm_gemm_desc* desc, void* stream);
 
 #ifdef __cplusplus
 }

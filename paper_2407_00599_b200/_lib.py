@@ -34,6 +34,17 @@ class SlotViewC(ctypes.Structure):
     ]
 
 
+class RowsC(ctypes.Structure):
+    _fields_ = [("ptr", _vp), ("ld", _c_ll), ("g_stride", _c_ll), ("lo_stride", _c_ll), ("hi_stride", _c_ll)]
+
+
+class GemmDescC(ctypes.Structure):
+    _fields_ = [("kind", _c_int), ("epi", _c_int), ("b_major", _c_int), ("groups", _c_int), ("nhi", _c_int),
+                ("nlo", _c_int), ("seg_len", _c_int), ("M", _c_int), ("N", _c_int), ("K", _c_int),
+                ("alpha", ctypes.c_float), ("pad_", _c_int), ("a", RowsC), ("b", RowsC), ("d", RowsC),
+                ("aux", RowsC), ("fill", _vp)]
+
+
 # name -> (restype, argtypes); mirrors include/parm_b200.h exactly.
 SIGNATURES = {
     "parm_abi_version": (_c_int, []),
@@ -51,11 +62,10 @@ SIGNATURES = {
     "parm_esp_sum": (_c_int, [ctypes.POINTER(SlotViewC), _c_int, _c_int, _c_int, _vp, _vp]),
     "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
     "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
-    "parm_grouped_gemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_ll, _vp,
-                                   _c_ll, _c_ll, _vp, _c_ll, _c_ll, _vp, _c_ll, _c_ll, ctypes.c_float, _vp]),
+    "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class ParmError(RuntimeError):

@@ -30,8 +30,7 @@ int combine_bwd(const void*, long long, const SlotView&, const int*, const int*,
 int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int, void*,
                  long long, cudaStream_t);
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
-int grouped_gemm(int, int, int, int, int, int, int, const void*, long long, long long, const void*, long long,
-                 long long, void*, long long, long long, const void*, long long, long long, float, cudaStream_t);
+int moe_gemm(const parm_gemm_desc&, cudaStream_t);
 
 static SlotView to_view(const parm_slot_view* v) {
     SlotView s;
@@ -113,12 +112,12 @@ int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, i
                             accumulate, S(stream));
 }
 
-int parm_grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A,
-                      long long lda, long long gsa, const void* B, long long ldb, long long gsb, void* D,
-                      long long ldd, long long gsd, const void* aux, long long ld_aux, long long gs_aux,
-                      float alpha, void* stream) {
-    return parm::grouped_gemm(major_a, major_b, epi, M, N, K, groups, A, lda, gsa, B, ldb, gsb, D, ldd, gsd, aux,
-                              ld_aux, gs_aux, alpha, S(stream));
+int parm_gemm(const parm_gemm_desc* desc, void* stream) {
+    if (!desc) {
+        parm::set_error("gemm: null descriptor");
+        return 1;
+    }
+    return parm::moe_gemm(*desc, S(stream));
 }
 
 }  // extern "C"

@@ -13,28 +13,49 @@
 // sees (every bf16 x bf16 product is exact in f64, so only the summation order
 // differs from the oracle's BLAS f64 dot); softmax and ranking run in f64.
 // The slot pass is an exact per-expert exclusive prefix count over tokens.
+//
+// Gate weights live on the device TRANSPOSED, wgT (E, M), so a lane's 8
+// consecutive columns of one expert are one 16-byte load.
 #include "common.cuh"
 
 namespace parm {
 
 constexpr int kGateThreads = 256;
 
-// One warp handles TPW tokens at once so each Wg load is reused TPW times.
-template <int EMAX, int TPW>
+// Warp-level reduce-scatter of 32 doubles: on return v[0] of lane L holds the
+// warp-wide sum of input index L.  31 double shuffles instead of 5 x 32.
+__device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = upper ? v[i] : v[i + o];
+            const double keep = upper ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+// One warp handles TPW = 32 / EMAX tokens; after the reduce-scatter lane
+// L = q * EMAX + e owns (token t0 + q, expert e): softmax max/sum over the
+// EMAX-lane group by shuffles, one exp and one divide per lane, stable rank
+// by comparing against the group's other lanes.
+template <int EMAX>
 __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __restrict__ x, long long ldx,
-                                                                 const bf16* __restrict__ wg, int n, int M, int E,
+                                                                 const bf16* __restrict__ wgT, int n, int M, int E,
                                                                  int k, int* __restrict__ expert_idx,
                                                                  float* __restrict__ combine_w,
                                                                  float* __restrict__ probs) {
+    constexpr int TPW = 32 / EMAX;
     const int lane = threadIdx.x & 31;
     const int warp_global = (blockIdx.x * kGateThreads + threadIdx.x) >> 5;
     const int num_warps = (gridDim.x * kGateThreads) >> 5;
     for (int t0 = warp_global * TPW; t0 < n; t0 += num_warps * TPW) {
-        double acc[TPW][EMAX];
+        double v[32];
 #pragma unroll
-        for (int q = 0; q < TPW; ++q)
-#pragma unroll
-            for (int e = 0; e < EMAX; ++e) acc[q][e] = 0.0;
+        for (int i = 0; i < 32; ++i) v[i] = 0.0;
         for (int c = lane * 8; c < M; c += 256) {
             float xv[TPW][8];
 #pragma unroll
@@ -47,134 +68,131 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const bf16* wrow = wg + (long long)(c + u) * E;
+            for (int e = 0; e < EMAX; ++e) {
+                if (e < E) {
+                    float wv[8];
+                    vec8_to_f32(ld_vec8(wgT + (long long)e * M + c), wv);
 #pragma unroll
-                for (int e = 0; e < EMAX; ++e) {
-                    if (e < E) {
-                        const double w = (double)bf2f(wrow[e]);
+                    for (int u = 0; u < 8; ++u) {
+                        const double w = (double)wv[u];
 #pragma unroll
-                        for (int q = 0; q < TPW; ++q) acc[q][e] = fma((double)xv[q][u], w, acc[q][e]);
+                        for (int q = 0; q < TPW; ++q) v[q * EMAX + e] = fma((double)xv[q][u], w, v[q * EMAX + e]);
                     }
                 }
             }
         }
-        // Butterfly all-reduce: every lane ends with every logit.
+        const double logit = reduce_scatter32(v, lane);
+        const int q = lane / EMAX;
+        const int e = lane - q * EMAX;
+        const int t = t0 + q;
+        const bool valid = (e < E);
+        double mx = valid ? logit : -INFINITY;
 #pragma unroll
-        for (int q = 0; q < TPW; ++q)
+        for (int o = 1; o < EMAX; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const double ex = valid ? exp(logit - mx) : 0.0;
+        double sum = ex;
 #pragma unroll
-            for (int e = 0; e < EMAX; ++e)
+        for (int o = 1; o < EMAX; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double score = ex / sum;
+        int rank = 0;
+        const int base = q * EMAX;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], off);
-
-#pragma unroll
-        for (int q = 0; q < TPW; ++q) {
-            const int t = t0 + q;
-            if (t >= n) break;
-            double mx = acc[q][0];
-#pragma unroll
-            for (int e = 1; e < EMAX; ++e)
-                if (e < E) mx = fmax(mx, acc[q][e]);
-            double ex[EMAX];
-            double sum = 0.0;
-#pragma unroll
-            for (int e = 0; e < EMAX; ++e) {
-                ex[e] = (e < E) ? exp(acc[q][e] - mx) : 0.0;
-                sum += ex[e];
+        for (int i = 0; i < EMAX; ++i) {
+            const double other = __shfl_sync(0xffffffffu, score, base + i);
+            rank += (i < E) && ((other > score) || (other == score && i < e));
+        }
+        if (valid && t < n) {
+            if (rank < k) {
+                expert_idx[(long long)t * k + rank] = e;
+                combine_w[(long long)t * k + rank] = (float)score;
             }
-            // Lane e owns expert e: compute its stable descending rank.
-            if (lane < E) {
-                double mine = 0.0;
-#pragma unroll
-                for (int e = 0; e < EMAX; ++e)
-                    if (e == lane) mine = ex[e] / sum;
-                int rank = 0;
-#pragma unroll
-                for (int e = 0; e < EMAX; ++e) {
-                    if (e < E) {
-                        const double other = ex[e] / sum;
-                        rank += (other > mine) || (other == mine && e < lane);
-                    }
-                }
-                if (rank < k) {
-                    expert_idx[(long long)t * k + rank] = lane;
-                    combine_w[(long long)t * k + rank] = (float)mine;
-                }
-                if (probs) probs[(long long)t * E + lane] = (float)mine;
-            }
+            if (probs) probs[(long long)t * E + e] = (float)score;
         }
     }
 }
 
 // Exclusive per-expert prefix count over tokens -> slots (single CTA, exact).
+// Two passes: warp w owns a contiguous token range; pass 1 counts its picks
+// per expert, a 32-entry scan per expert gives each warp its base, pass 2
+// assigns slots in token order with ballot prefixes.
 constexpr int kSlotThreads = 1024;
 constexpr int kMaxExperts = 64;
 
+template <int EMAX>
 __global__ void __launch_bounds__(kSlotThreads) gate_slots_kernel(const int* __restrict__ expert_idx, int n, int k,
                                                                    int E, int cap, int* __restrict__ slot_idx,
                                                                    int* __restrict__ slot_src,
                                                                    int* __restrict__ fill) {
-    __shared__ int warp_cnt[32][kMaxExperts];
-    __shared__ int running[kMaxExperts];
-    __shared__ int chunk_tot[kMaxExperts];
+    __shared__ int warp_cnt[32][EMAX];
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    for (long long i = tid; i < (long long)E * cap; i += kSlotThreads) slot_src[i] = -1;
-    if (tid < E) running[tid] = 0;
-    __syncthreads();
     const unsigned lt_mask = (1u << lane) - 1u;
-    for (int base = 0; base < n; base += kSlotThreads) {
-        const int t = base + tid;
+    const int per = ((n + 32 * 32 - 1) / (32 * 32)) * 32;   // tokens per warp, multiple of 32
+    const int t_begin = warp * per;
+    const int t_end = min(n, t_begin + per);
+
+    int cnt[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) cnt[e] = 0;
+    for (int base = t_begin; base < t_end; base += 32) {
+        const int t = base + lane;
+        unsigned pick = 0;  // bitmask of experts picked by token t (E <= EMAX <= 32 here)
+        if (t < t_end)
+            for (int j = 0; j < k; ++j) pick |= 1u << expert_idx[(long long)t * k + j];
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) cnt[e] += __popc(__ballot_sync(0xffffffffu, (pick >> e) & 1u));
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) warp_cnt[warp][e] = cnt[e];
+    for (long long i = tid; i < (long long)E * cap; i += kSlotThreads) slot_src[i] = -1;
+    __syncthreads();
+    if (tid < E) {
+        int acc = 0;
+        for (int w = 0; w < 32; ++w) {
+            const int c = warp_cnt[w][tid];
+            warp_cnt[w][tid] = acc;
+            acc += c;
+        }
+        fill[tid] = acc < cap ? acc : cap;
+    }
+    __syncthreads();
+    int run[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) run[e] = warp_cnt[warp][e];
+    for (int base = t_begin; base < t_end; base += 32) {
+        const int t = base + lane;
         int ex[8];
-        const int kk = k < 8 ? k : 8;
+        unsigned pick = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) ex[j] = (t < n && j < kk) ? expert_idx[(long long)t * k + j] : -1;
-        int pre[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pre[j] = 0;
-        for (int e = 0; e < E; ++e) {
-            bool flag = false;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) flag |= (ex[j] == e);
-            const unsigned b = __ballot_sync(0xffffffffu, flag);
-            const int p = __popc(b & lt_mask);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (ex[j] == e) pre[j] = p;
-            if (lane == 0) warp_cnt[warp][e] = __popc(b);
+        for (int j = 0; j < 8; ++j) {
+            ex[j] = (t < t_end && j < k) ? expert_idx[(long long)t * k + j] : -1;
+            if (ex[j] >= 0) pick |= 1u << ex[j];
         }
-        __syncthreads();
-        if (tid < E) {
-            int acc = 0;
-            for (int w = 0; w < 32; ++w) {
-                const int c = warp_cnt[w][tid];
-                warp_cnt[w][tid] = acc;
-                acc += c;
-            }
-            chunk_tot[tid] = acc;
-        }
-        __syncthreads();
-        if (t < n) {
-            for (int j = 0; j < kk; ++j) {
-                const int e = ex[j];
-                const int slot = running[e] + warp_cnt[warp][e] + pre[j];
-                if (slot < cap) {
-                    slot_idx[(long long)t * k + j] = slot;
-                    slot_src[(long long)e * cap + slot] = t * k + j;
-                } else {
-                    slot_idx[(long long)t * k + j] = -1;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            const unsigned b = __ballot_sync(0xffffffffu, (pick >> e) & 1u);
+            if ((pick >> e) & 1u) {
+                const int slot = run[e] + __popc(b & lt_mask);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (ex[j] == e) {
+                        if (slot < cap) {
+                            slot_idx[(long long)t * k + j] = slot;
+                            slot_src[(long long)e * cap + slot] = t * k + j;
+                        } else {
+                            slot_idx[(long long)t * k + j] = -1;
+                        }
+                    }
                 }
             }
+            run[e] += __popc(b);
         }
-        __syncthreads();
-        if (tid < E) running[tid] += chunk_tot[tid];
-        __syncthreads();
     }
-    if (tid < E) fill[tid] = running[tid] < cap ? running[tid] : cap;
 }
 
-// dWg partials: part[c][m][e] = sum_{t in chunk c} x[t][m] * dlogits[t][e].
+// dWg^T partials: part[c][e][m] = sum_{t in chunk c} dlogits[t][e] * x[t][m].
 template <int EMAX>
 __global__ void __launch_bounds__(256) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
                                                                   const float* __restrict__ dlogits, int n, int M,
@@ -204,7 +222,7 @@ __global__ void __launch_bounds__(256) gate_wgrad_partial_kernel(const bf16* __r
         }
     }
     if (m < M)
-        for (int e = 0; e < E; ++e) part[((long long)c * M + m) * E + e] = acc[e];
+        for (int e = 0; e < E; ++e) part[((long long)c * E + e) * M + m] = acc[e];
 }
 
 __global__ void sum_partials_kernel(const float* __restrict__ part, int chunks, long long len, float* __restrict__ out,
@@ -217,33 +235,36 @@ __global__ void sum_partials_kernel(const float* __restrict__ part, int chunks, 
 }
 
 // ------------------------------------------------------------------ host
-template <int EMAX, int TPW>
-static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wg, int n, int M, int E, int k, int* ei,
+template <int EMAX>
+static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wgT, int n, int M, int E, int k, int* ei,
                             float* cw, float* probs, cudaStream_t s) {
+    constexpr int TPW = 32 / EMAX;
     const int warps_needed = (n + TPW - 1) / TPW;
     int blocks = (warps_needed * 32 + kGateThreads - 1) / kGateThreads;
     const int max_blocks = kNumSMs * 8;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    gate_fwd_kernel<EMAX, TPW><<<blocks, kGateThreads, 0, s>>>(x, ldx, wg, n, M, E, k, ei, cw, probs);
+    gate_fwd_kernel<EMAX><<<blocks, kGateThreads, 0, s>>>(x, ldx, wgT, n, M, E, k, ei, cw, probs);
 }
 
-int gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, int k, int* expert_idx,
+int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E, int k, int* expert_idx,
              float* combine_w, float* probs, cudaStream_t s) {
     PARM_CHECK_ARG(k >= 1 && k <= E, "top_k (%d) exceeds number of experts (%d)", k, E);
     PARM_CHECK_ARG(E <= 32, "gate: at most 32 experts supported (got %d)", E);
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "gate: embed (%d) and row stride must be multiples of 8", M);
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
-    auto W = reinterpret_cast<const bf16*>(wg);
-    if (E <= 4)
-        launch_gate_fwd<4, 4>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
+    auto W = reinterpret_cast<const bf16*>(wgT);
+    if (E <= 2)
+        launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
+    else if (E <= 4)
+        launch_gate_fwd<4>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 8)
-        launch_gate_fwd<8, 4>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
+        launch_gate_fwd<8>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 16)
-        launch_gate_fwd<16, 2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
+        launch_gate_fwd<16>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else
-        launch_gate_fwd<32, 1>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
+        launch_gate_fwd<32>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     PARM_CHECK_LAUNCH("gate_fwd");
     return 0;
 }
@@ -251,9 +272,12 @@ int gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, 
 int gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
                cudaStream_t s) {
     PARM_CHECK_ARG(k >= 1 && k <= 8, "gate_slots: top_k must be in [1, 8] (got %d)", k);
-    PARM_CHECK_ARG(E >= 1 && E <= kMaxExperts, "gate_slots: experts must be in [1, %d]", kMaxExperts);
+    PARM_CHECK_ARG(E >= 1 && E <= 32, "gate_slots: experts must be in [1, 32]");
     PARM_CHECK_ARG(cap >= 1, "gate_slots: capacity must be >= 1");
-    gate_slots_kernel<<<1, kSlotThreads, 0, s>>>(expert_idx, n, k, E, cap, slot_idx, slot_src, fill);
+    if (E <= 8)
+        gate_slots_kernel<8><<<1, kSlotThreads, 0, s>>>(expert_idx, n, k, E, cap, slot_idx, slot_src, fill);
+    else
+        gate_slots_kernel<32><<<1, kSlotThreads, 0, s>>>(expert_idx, n, k, E, cap, slot_idx, slot_src, fill);
     PARM_CHECK_LAUNCH("gate_slots");
     return 0;
 }
@@ -264,7 +288,7 @@ size_t gate_wgrad_workspace(int n, int M, int E) {
 }
 
 int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, float* ws, size_t ws_bytes,
-               float* dwg, int accumulate, cudaStream_t s) {
+               float* dwgT, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(E <= 32, "gate_wgrad: at most 32 experts supported");
     const int chunks = n < 64 ? 1 : (n / 64 < 128 ? n / 64 : 128);
     PARM_CHECK_ARG(ws_bytes >= (size_t)chunks * M * E * sizeof(float), "gate_wgrad: workspace too small");
@@ -281,7 +305,7 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     const long long len = (long long)M * E;
     int blocks = (int)((len + 255) / 256);
     if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
-    sum_partials_kernel<<<blocks, 256, 0, s>>>(ws, chunks, len, dwg, accumulate);
+    sum_partials_kernel<<<blocks, 256, 0, s>>>(ws, chunks, len, dwgT, accumulate);
     PARM_CHECK_LAUNCH("gate_wgrad_sum");
     return 0;
 }

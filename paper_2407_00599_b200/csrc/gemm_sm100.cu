@@ -1,41 +1,40 @@
 // Grouped bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA),
 // the expert-FFN engine of the Parm MoE layer.
 //
-//   D_g[m][n] = sum_k A_g[m][k] * B_g[n][k]     for every group g (= local expert)
+// Every expert-row tensor of the layer lives in the AlltoAll receive layout
+//     [src_hi][src_lo][expert g][row r < L][col]            ("segmented rows")
+// so that each exchange is ONE message per peer; the GEMM reads and writes
+// that layout directly (5-D TMA maps, OOB rows zero-filled; row-remapped
+// epilogue), and skips 128-row tiles / 64-row K-blocks beyond each segment's
+// fill count (capacity padding carries no work).  Two problem kinds:
 //
-// A and B are each either K-major (row m / n contiguous along k) or MN-major
-// (stored transposed, k rows of contiguous m / n).  That single kernel covers
-// the six FFN GEMMs of one expert shard (reference dataplane.py:122-128 forward;
-// the backward the reference does not have):
-//   fwd  H  = relu(R W1)      A=R  (K)   B=W1t (K)   epilogue relu -> bf16
-//   fwd  Y  = H W2            A=H  (K)   B=W2t (K)   epilogue bf16
-//   bwd  dH = (dY W2^T).[H>0] A=dY (K)   B=W2t (MN)  epilogue relu-mask(aux=H) -> bf16
-//   bwd  dR = dH W1^T         A=dH (K)   B=W1t (MN)  epilogue bf16
-//   bwd dW1t = dH^T R         A=dH (MN)  B=R   (MN)  epilogue f32
-//   bwd dW2t = dY^T H         A=dY (MN)  B=H   (MN)  epilogue f32
+//   ROW   D[s][g][r][n] = sum_k A[s][g][r][k] * B[g][n][k]     (B = weights,
+//         K-major or MN-major)  -- fwd H = relu(R W1), Y = H W2, bwd
+//         dH = (dY W2^T).[H>0], dR = dH W1^T   (reference dataplane.py:122-128)
+//   WGT   D[g][m][n] = sum_{s,r} A[s][g][r][m] * B[s][g][r][n] -- dW1^T = dH^T R,
+//         dW2^T = dY^T H (both operands MN-major over the segmented K)
 //
-// Structure (one CTA per SM, persistent over tiles of 128 x BN):
+// Structure (one CTA per SM, persistent over 128 x BN tiles):
 //   warp 0      TMA producer (one lane), STAGES-deep smem ring, 128B swizzle
 //   warp 1      MMA issuer  (one lane), tcgen05.mma.cta_group::1.kind::f16,
 //               M=128 N=BN K=16, fp32 accumulators in TMEM (2 x BN columns,
 //               double-buffered so the epilogue of tile i overlaps MMA of i+1)
 //   warp 2      TMEM allocator
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
-//
-// Shape contract (enforced by the host wrapper): M % 128 == 0, N % BN == 0,
-// K % 64 == 0, 16-byte aligned bases/strides.  The runtime pads rows/embed/
-// hidden so every MoE shape satisfies it.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
+#include "../../include/parm_b200.h"
 #include "common.cuh"
 
 namespace parm {
 namespace gemm {
 
 enum Major : int { kKMajor = 0, kMNMajor = 1 };
+enum Kind : int { kRow = 0, kWgt = 1 };
 enum Epi : int { kEpiBF16 = 0, kEpiReluBF16 = 1, kEpiDReluBF16 = 2, kEpiF32 = 3, kEpiF32Acc = 4 };
 
 constexpr int BM = 128;
@@ -44,13 +43,16 @@ constexpr int kThreads = 256;
 constexpr int kSmemBudget = 196 * 1024;
 
 struct Params {
-    int M, N, K, groups;
-    int m_blocks, n_blocks, num_tiles;
+    int G, nhi, nlo, L;        // row space: segments (hi, lo), rows per segment
+    int M, N, K;               // ROW: K = reduction, N = cols; WGT: M x N output, K from row space
+    int m_tiles, n_blocks, num_tiles, k_iters;
+    float alpha;
     void* D;
-    long long ldd, gsd;         // D row stride / group stride (elements)
-    const bf16* aux;            // relu mask source for kEpiDReluBF16 (same shape as D)
-    long long ld_aux, gs_aux;
-    float alpha;                // D = alpha * A B^T (+ D for kEpiF32Acc)
+    long long d_ld, d_g, d_lo, d_hi;
+    const bf16* aux;
+    long long x_ld, x_g, x_lo, x_hi;
+    const int* fill;           // [hi][lo][g] valid rows, or null
+    int pairs;                 // CTA-pair kernel: max 256-row pair tiles per group
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -96,6 +98,15 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                            int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 
@@ -153,23 +164,156 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- tile bookkeeping
+struct Tile {
+    int g, hi, lo, m0, n0;
+};
+
+__device__ __forceinline__ Tile decode_tile(const Params& p, int tile, int kind, int bn) {
+    Tile t;
+    if (kind == kRow) {
+        const int per_seg = p.m_tiles * p.n_blocks;
+        const int per_g = p.nhi * p.nlo * per_seg;
+        t.g = tile / per_g;
+        int rem = tile - t.g * per_g;
+        const int seg = rem / per_seg;
+        rem -= seg * per_seg;
+        t.hi = seg / p.nlo;
+        t.lo = seg - t.hi * p.nlo;
+        t.m0 = (rem / p.n_blocks) * BM;
+        t.n0 = (rem % p.n_blocks) * bn;
+    } else {
+        const int per_g = p.m_tiles * p.n_blocks;
+        t.g = tile / per_g;
+        const int rem = tile - t.g * per_g;
+        t.hi = t.lo = 0;
+        t.m0 = (rem / p.n_blocks) * BM;
+        t.n0 = (rem % p.n_blocks) * bn;
+    }
+    return t;
+}
+
+// Fill counts are staged into shared memory once per CTA (kMaxFill entries): the
+// single-thread producer/MMA loops must not pay a global-load latency per K block.
+constexpr int kMaxFill = 2048;
+
+__device__ __forceinline__ int seg_fill(const Params& p, const int* sfill, int g, int hi, int lo) {
+    return p.fill ? sfill[(hi * p.nlo + lo) * p.G + g] : p.L;
+}
+
+// ROW tiles beyond the segment's fill carry no work.
+__device__ __forceinline__ bool row_tile_live(const Params& p, const int* sfill, const Tile& t) {
+    return t.m0 < seg_fill(p, sfill, t.g, t.hi, t.lo);
+}
+
+// WGT: K iteration it -> (hi, lo, row block); live iff the block holds filled rows.
+__device__ __forceinline__ bool wgt_k_live(const Params& p, const int* sfill, int g, int it, int& hi, int& lo,
+                                           int& r0) {
+    const int kt = (p.L + BK - 1) / BK;
+    const int seg = it / kt;
+    r0 = (it - seg * kt) * BK;
+    hi = seg / p.nlo;
+    lo = seg - hi * p.nlo;
+    return r0 < seg_fill(p, sfill, g, hi, lo);
+}
+
+// Epilogue of one accumulator tile for the calling thread's row: 32-column
+// chunks tcgen05.ld 32x32b -> registers -> fused op -> 16-byte global stores.
+// The ReLU-mask source (aux) of chunk c+1 is fetched while chunk c is
+// processed, so its global-load latency is exposed once per tile, not per chunk.
+template <int BN, int EPI>
+__device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long long drow, long long xrow,
+                                           bool row_ok, int n0, bool empty) {
+    constexpr int NC = BN / 32;
+    int4 ax_next[4];
+    if (EPI == kEpiDReluBF16 && row_ok) {
+        const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) ax_next[v] = __ldg(src + v);
+    }
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+        int4 ax_cur[4];
+        if (EPI == kEpiDReluBF16) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) ax_cur[v] = ax_next[v];
+            if (row_ok && c + 1 < NC) {
+                const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0 + (c + 1) * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) ax_next[v] = __ldg(src + v);
+            }
+        }
+        uint32_t r[32];
+        PARM_TMEM_LD32(taddr + c * 32, r);
+        tmem_ld_wait();
+        if (empty) {
+#pragma unroll
+            for (int v = 0; v < 32; ++v) r[v] = 0u;
+        }
+        if (!row_ok) continue;
+        const int col = n0 + c * 32;
+        if (EPI == kEpiF32 || EPI == kEpiF32Acc) {
+            float* dst = reinterpret_cast<float*>(p.D) + drow + col;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                float4 o = make_float4(p.alpha * __uint_as_float(r[4 * v]), p.alpha * __uint_as_float(r[4 * v + 1]),
+                                       p.alpha * __uint_as_float(r[4 * v + 2]),
+                                       p.alpha * __uint_as_float(r[4 * v + 3]));
+                if (EPI == kEpiF32Acc) {
+                    float4 prev = reinterpret_cast<float4*>(dst)[v];
+                    o.x += prev.x;
+                    o.y += prev.y;
+                    o.z += prev.z;
+                    o.w += prev.w;
+                }
+                reinterpret_cast<float4*>(dst)[v] = o;
+            }
+        } else {
+            bf16* dst = reinterpret_cast<bf16*>(p.D) + drow + col;
+            float f[32];
+#pragma unroll
+            for (int v = 0; v < 32; ++v) f[v] = p.alpha * __uint_as_float(r[v]);
+            if (EPI == kEpiReluBF16) {
+#pragma unroll
+                for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
+            }
+            if (EPI == kEpiDReluBF16) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    Vec8 a8;
+                    *reinterpret_cast<int4*>(&a8) = ax_cur[v];
+                    float a[8];
+                    vec8_to_f32(a8, a);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) f[8 * v + u] = a[u] > 0.0f ? f[8 * v + u] : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) st_vec8(dst + 8 * v, f32_to_vec8(f + 8 * v));
+        }
+    }
+}
+
 // ---------------------------------------------------------------- the kernel
-template <int BN, int MA, int MB, int EPI>
+template <int BN, int KIND, int MB, int EPI>
 struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (kSmemBudget - 1024) / kStageBytes > 8 ? 8 : (kSmemBudget - 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/ +
+                                      kMaxFill * 4;
 };
 
-template <int BN, int MA, int MB, int EPI>
+template <int BN, int KIND, int MB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                        const Params p) {
-    using C = Cfg<BN, MA, MB, EPI>;
+    moe_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                    const Params p) {
+    using C = Cfg<BN, KIND, MB, EPI>;
     constexpr int STAGES = C::kStages;
+    constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
+    constexpr int MBX = (KIND == kRow) ? MB : kMNMajor;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smem_a = smem;
@@ -179,9 +323,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + 256);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (p.fill)
+        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmap_a);
@@ -207,38 +354,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int k_blocks = p.K / BK;
-    const int tiles_per_group = p.m_blocks * p.n_blocks;
-
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const int g = tile / tiles_per_group;
-                const int rem = tile - g * tiles_per_group;
-                const int m0 = (rem / p.n_blocks) * BM;
-                const int n0 = (rem % p.n_blocks) * BN;
-                for (int kb = 0; kb < k_blocks; ++kb) {
+                const Tile t = decode_tile(p, tile, KIND, BN);
+                if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
+                for (int it = 0; it < p.k_iters; ++it) {
+                    int hi = t.hi, lo = t.lo, r0 = 0;
+                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                    const int k0 = kb * BK;
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
-                    if (MA == kKMajor) {
-                        tma_load_3d(&tmap_a, &full_bar[stage], sa, k0, m0, g);
+                    if (KIND == kRow) {
+                        const int k0 = it * BK;
+                        tma_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
+                        if (MB == kKMajor) {
+                            tma_load_3d(&tmap_b, &full_bar[stage], sb, k0, t.n0, t.g);
+                        } else {
+#pragma unroll
+                            for (int a = 0; a < BN / 64; ++a)
+                                tma_load_3d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), t.n0 + a * 64, k0, t.g);
+                        }
                     } else {
 #pragma unroll
                         for (int a = 0; a < BM / 64; ++a)
-                            tma_load_3d(&tmap_a, &full_bar[stage], sa + a * (BK * 128), m0 + a * 64, k0, g);
-                    }
-                    if (MB == kKMajor) {
-                        tma_load_3d(&tmap_b, &full_bar[stage], sb, k0, n0, g);
-                    } else {
+                            tma_load_5d(&tmap_a, &full_bar[stage], sa + a * (BK * 128), t.m0 + a * 64, r0, t.g, lo,
+                                        hi);
 #pragma unroll
                         for (int a = 0; a < BN / 64; ++a)
-                            tma_load_3d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), n0 + a * 64, k0, g);
+                            tma_load_5d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), t.n0 + a * 64, r0, t.g, lo,
+                                        hi);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -250,23 +399,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             // ------------------------------------------------ MMA issuer
-            constexpr uint32_t idesc = instr_desc<BN, MA, MB>();
+            constexpr uint32_t idesc = instr_desc<BN, MA, MBX>();
             // K-major: 8-row core groups 1024 B apart, K advance of 16 elems = 32 B.
             // MN-major: 64-element MN atoms BK*128 B apart, K advance of 16 rows = 2048 B.
             constexpr uint32_t a_lbo = (MA == kKMajor) ? 0 : BK * 128;
-            constexpr uint32_t b_lbo = (MB == kKMajor) ? 0 : BK * 128;
+            constexpr uint32_t b_lbo = (MBX == kKMajor) ? 0 : BK * 128;
             constexpr uint32_t a_kstep = (MA == kKMajor) ? 32 : 16 * 128;
-            constexpr uint32_t b_kstep = (MB == kKMajor) ? 32 : 16 * 128;
+            constexpr uint32_t b_kstep = (MBX == kKMajor) ? 32 : 16 * 128;
             int stage = 0;
             uint32_t phase = 0;
-            int it = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
-                const int as = it & 1;
-                const uint32_t aphase = (it >> 1) & 1;
+            int it_tile = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const Tile t = decode_tile(p, tile, KIND, BN);
+                if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
+                const int as = it_tile & 1;
+                const uint32_t aphase = (it_tile >> 1) & 1;
+                ++it_tile;
                 mbar_wait(&tempty_bar[as], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + as * BN;
-                for (int kb = 0; kb < k_blocks; ++kb) {
+                bool first = true;
+                for (int it = 0; it < p.k_iters; ++it) {
+                    int hi, lo, r0;
+                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
@@ -275,78 +430,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < BK / 16; ++k) {
                         uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
                         uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
-                        tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+                        tc_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
                     }
+                    first = false;
                     tc_commit(&empty_bar[stage]);
-                    if (kb == k_blocks - 1) tc_commit(&tfull_bar[as]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
+                tc_commit(&tfull_bar[as]);   // also fires for an all-skipped WGT tile (epilogue writes zeros)
             }
         }
     } else if (warp >= 4) {
         // ---------------------------------------------------- epilogue
         const int ew = warp & 3;  // TMEM lane quarter this warp may access
-        int it = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
-            const int g = tile / tiles_per_group;
-            const int rem = tile - g * tiles_per_group;
-            const int m0 = (rem / p.n_blocks) * BM;
-            const int n0 = (rem % p.n_blocks) * BN;
-            const int as = it & 1;
-            const uint32_t aphase = (it >> 1) & 1;
+        int it_tile = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const Tile t = decode_tile(p, tile, KIND, BN);
+            if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
+            const int as = it_tile & 1;
+            const uint32_t aphase = (it_tile >> 1) & 1;
+            ++it_tile;
+            bool empty = false;
+            if (KIND == kWgt && p.fill) {
+                empty = true;
+                for (int seg = 0; seg < p.nhi * p.nlo && empty; ++seg)
+                    empty = seg_fill(p, sfill, t.g, seg / p.nlo, seg % p.nlo) <= 0;
+            }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
-            const int row = m0 + ew * 32 + lane;
-            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                PARM_TMEM_LD32(taddr + c * 32, r);
-                tmem_ld_wait();
-                const int col = n0 + c * 32;
-                if (EPI == kEpiF32 || EPI == kEpiF32Acc) {
-                    float* dst = reinterpret_cast<float*>(p.D) + (long long)g * p.gsd + (long long)row * p.ldd + col;
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        float4 o = make_float4(p.alpha * __uint_as_float(r[4 * v]),
-                                               p.alpha * __uint_as_float(r[4 * v + 1]),
-                                               p.alpha * __uint_as_float(r[4 * v + 2]),
-                                               p.alpha * __uint_as_float(r[4 * v + 3]));
-                        if (EPI == kEpiF32Acc) {
-                            float4 prev = reinterpret_cast<float4*>(dst)[v];
-                            o.x += prev.x;
-                            o.y += prev.y;
-                            o.z += prev.z;
-                            o.w += prev.w;
-                        }
-                        reinterpret_cast<float4*>(dst)[v] = o;
-                    }
-                } else {
-                    bf16* dst = reinterpret_cast<bf16*>(p.D) + (long long)g * p.gsd + (long long)row * p.ldd + col;
-                    float f[32];
-#pragma unroll
-                    for (int v = 0; v < 32; ++v) f[v] = p.alpha * __uint_as_float(r[v]);
-                    if (EPI == kEpiReluBF16) {
-#pragma unroll
-                        for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
-                    }
-                    if (EPI == kEpiDReluBF16) {
-                        const bf16* ax = p.aux + (long long)g * p.gs_aux + (long long)row * p.ld_aux + col;
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            float a[8];
-                            vec8_to_f32(ld_vec8(ax + 8 * v), a);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) f[8 * v + u] = a[u] > 0.0f ? f[8 * v + u] : 0.0f;
-                        }
-                    }
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) st_vec8(dst + 8 * v, f32_to_vec8(f + 8 * v));
-                }
+            const int row = t.m0 + ew * 32 + lane;
+            const bool row_ok = (KIND == kWgt) || row < p.L;
+            long long drow, xrow = 0;
+            if (KIND == kRow) {
+                drow = (long long)t.g * p.d_g + (long long)t.lo * p.d_lo + (long long)t.hi * p.d_hi +
+                       (long long)row * p.d_ld;
+                xrow = (long long)t.g * p.x_g + (long long)t.lo * p.x_lo + (long long)t.hi * p.x_hi +
+                       (long long)row * p.x_ld;
+            } else {
+                drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
             }
+            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
+            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
             tc_fence_before();
             mbar_arrive(&tempty_bar[as]);
         }
@@ -357,6 +483,334 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     if (warp == 2) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"((uint32_t)C::kTmemCols)
+                     : "memory");
+    }
+}
+
+// ================================================================ CTA-pair kernel
+// cta_group::2: a cluster of two CTAs on a TPC computes a 256 x BN tile with one
+// tcgen05.mma.cta_group::2 (UMMA M=256) issued by the even ("leader") CTA.
+// Each CTA stages its own 128 A-rows and HALF of the B tile (BN/2 rows of N),
+// so per-SM shared-memory traffic per FLOP drops by 1/3 versus the 1-CTA
+// 128 x BN tile (the 1-CTA kernel is smem-bandwidth bound: ncu shows
+// l1tex/smem ~65% busy at ~1.1 PFLOP/s).  Accumulator rows 0-127 live in the
+// leader's TMEM, rows 128-255 in the peer's; each CTA's epilogue drains its own.
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// Arrive on the barrier at the same smem offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(rank)
+        : "memory");
+}
+
+// TMA load whose completion is signalled on the LEADER CTA's mbarrier (cta_group::2).
+__device__ __forceinline__ void tma2_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                             int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma2_load_5d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                             int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2),
+        "r"(c3), "r"(c4)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+template <int BN, int MA, int MB>
+__device__ __forceinline__ constexpr uint32_t instr_desc_pair() {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)MA << 15) | ((uint32_t)MB << 16) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+}
+
+// k-th live ROW tile of group g in (hi, lo, m-tile) order.
+__device__ __forceinline__ bool nth_live_row_tile(const Params& p, const int* sfill, int g, int k, int& hi, int& lo,
+                                                  int& m0) {
+    const int nseg = p.nhi * p.nlo;
+    for (int seg = 0; seg < nseg; ++seg) {
+        const int h = seg / p.nlo, l = seg - h * p.nlo;
+        const int f = seg_fill(p, sfill, g, h, l);
+        int live = (f + BM - 1) / BM;
+        if (live > p.m_tiles) live = p.m_tiles;
+        if (k < live) {
+            hi = h;
+            lo = l;
+            m0 = k * BM;
+            return true;
+        }
+        k -= live;
+    }
+    return false;
+}
+
+struct PairTile {
+    bool live;       // the pair has work (its first tile exists)
+    int g, hi, lo, m0, n0;   // this CTA's half: rows [m0, m0+128) of segment (hi, lo); m0 >= L/M -> dummy
+};
+
+__device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfill, int tile, int kind, int bn,
+                                               uint32_t rank) {
+    PairTile t;
+    const int per_g = p.pairs * p.n_blocks;     // pairs = max 256-row pair tiles per group
+    t.g = tile / per_g;
+    const int rem = tile - t.g * per_g;
+    const int pj = rem / p.n_blocks;
+    t.n0 = (rem % p.n_blocks) * bn;
+    t.hi = t.lo = 0;
+    if (kind == kRow) {
+        int h0, l0, m00;
+        t.live = nth_live_row_tile(p, sfill, t.g, 2 * pj, h0, l0, m00);
+        if (rank == 0) {
+            t.hi = h0;
+            t.lo = l0;
+            t.m0 = m00;
+        } else if (!nth_live_row_tile(p, sfill, t.g, 2 * pj + 1, t.hi, t.lo, t.m0)) {
+            t.hi = h0;
+            t.lo = l0;
+            t.m0 = p.L;              // dummy: fully out of bounds, zero-filled, never stored
+        }
+    } else {
+        t.m0 = (2 * pj + (int)rank) * BM;   // >= M -> dummy rows
+        t.live = true;
+    }
+    return t;
+}
+
+template <int BN, int KIND, int MB, int EPI>
+struct CfgPair {
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = (BN / 2) * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (kSmemBudget - 1024) / kStageBytes > 8 ? 8 : (kSmemBudget - 1024) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + kMaxFill * 4;
+};
+
+template <int BN, int KIND, int MB, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                         const Params p) {
+    using C = CfgPair<BN, KIND, MB, EPI>;
+    constexpr int STAGES = C::kStages;
+    constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
+    constexpr int MBX = (KIND == kRow) ? MB : kMNMajor;
+    constexpr int BNH = BN / 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + STAGES * C::kABytes;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* tfull_bar = empty_bar + STAGES;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + 256);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p.fill)
+        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair_id = blockIdx.x >> 1;
+    const int num_pairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 2);      // leader expect_tx arrival + peer arrival
+            mbar_init(&empty_bar[s], 1);     // leader's multicast commit
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull_bar[s], 1);
+            mbar_init(&tempty_bar[s], 2 * 128);   // both CTAs' epilogue threads (leader's copy used)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)C::kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+                if (!t.live) continue;
+                for (int it = 0; it < p.k_iters; ++it) {
+                    int hi = 0, lo = 0, r0 = 0;
+                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    if (leader)
+                        mbar_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
+                    else
+                        mbar_arrive_remote(&full_bar[stage], 0);
+                    uint8_t* sa = smem_a + stage * C::kABytes;
+                    uint8_t* sb = smem_b + stage * C::kBBytes;
+                    const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
+                    if (KIND == kRow) {
+                        const int k0 = it * BK;
+                        tma2_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
+                        if (MB == kKMajor) {
+                            tma2_load_3d(&tmap_b, &full_bar[stage], sb, k0, nb0, t.g);
+                        } else {
+#pragma unroll
+                            for (int a = 0; a < BNH / 64; ++a)
+                                tma2_load_3d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, k0, t.g);
+                        }
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < BM / 64; ++a)
+                            tma2_load_5d(&tmap_a, &full_bar[stage], sa + a * (BK * 128), t.m0 + a * 64, r0, t.g, lo,
+                                         hi);
+#pragma unroll
+                        for (int a = 0; a < BNH / 64; ++a)
+                            tma2_load_5d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, r0, t.g, lo,
+                                         hi);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ------------------------------------------------ MMA issuer (leader CTA only)
+            constexpr uint32_t idesc = instr_desc_pair<BN, MA, MBX>();
+            constexpr uint32_t a_lbo = (MA == kKMajor) ? 0 : BK * 128;
+            constexpr uint32_t b_lbo = (MBX == kKMajor) ? 0 : BK * 128;
+            constexpr uint32_t a_kstep = (MA == kKMajor) ? 32 : 16 * 128;
+            constexpr uint32_t b_kstep = (MBX == kKMajor) ? 32 : 16 * 128;
+            int stage = 0;
+            uint32_t phase = 0;
+            int it_tile = 0;
+            for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+                if (!t.live) continue;
+                const int as = it_tile & 1;
+                const uint32_t aphase = (it_tile >> 1) & 1;
+                ++it_tile;
+                mbar_wait(&tempty_bar[as], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + as * BN;
+                bool first = true;
+                for (int it = 0; it < p.k_iters; ++it) {
+                    int hi, lo, r0;
+                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
+                    const uint32_t sb = smem_u32(smem_b + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
+                        uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
+                        tc2_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+                    }
+                    first = false;
+                    tc2_commit_both(&empty_bar[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc2_commit_both(&tfull_bar[as]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------------------------------------------- epilogue (both CTAs, own TMEM rows)
+        const int ew = warp & 3;
+        int it_tile = 0;
+        for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+            const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+            if (!t.live) continue;
+            const int as = it_tile & 1;
+            const uint32_t aphase = (it_tile >> 1) & 1;
+            ++it_tile;
+            bool empty = false;
+            if (KIND == kWgt && p.fill) {
+                empty = true;
+                for (int seg = 0; seg < p.nhi * p.nlo && empty; ++seg)
+                    empty = seg_fill(p, sfill, t.g, seg / p.nlo, seg % p.nlo) <= 0;
+            }
+            mbar_wait(&tfull_bar[as], aphase);
+            tc_fence_after();
+            const int row = t.m0 + ew * 32 + lane;
+            const bool row_ok = (KIND == kWgt) ? row < p.M : row < p.L;
+            long long drow, xrow = 0;
+            if (KIND == kRow) {
+                drow = (long long)t.g * p.d_g + (long long)t.lo * p.d_lo + (long long)t.hi * p.d_hi +
+                       (long long)row * p.d_ld;
+                xrow = (long long)t.g * p.x_g + (long long)t.lo * p.x_lo + (long long)t.hi * p.x_hi +
+                       (long long)row * p.x_ld;
+            } else {
+                drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
+            }
+            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
+            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
+            tc_fence_before();
+            if (leader)
+                mbar_arrive(&tempty_bar[as]);
+            else
+                mbar_arrive_remote(&tempty_bar[as], 0);
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"((uint32_t)C::kTmemCols)
                      : "memory");
     }
@@ -376,107 +830,168 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 3-D bf16 tensor map: dims {inner, outer, groups}, 128B swizzle, box {64, box_outer, 1}.
-static int make_tmap(CUtensorMap* map, const void* base, long long inner, long long outer, long long groups,
-                     long long ld_elems, long long gs_elems, int box_outer) {
+// bf16 tensor map with 128B swizzle; dims[0] is contiguous; strides in elements for dims 1..rank-1.
+static int make_tmap(CUtensorMap* map, const void* base, int rank, const long long* dims, const long long* strides,
+                     int box1) {
     auto enc = get_encode();
     PARM_CHECK_ARG(enc != nullptr, "gemm: cuTensorMapEncodeTiled unavailable from the driver");
     PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, "gemm: operand base not 16-byte aligned");
-    PARM_CHECK_ARG((ld_elems * 2) % 16 == 0 && (gs_elems * 2) % 16 == 0, "gemm: strides not 16-byte multiples");
-    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)groups};
-    cuuint64_t strides[2] = {(cuuint64_t)(ld_elems * 2), (cuuint64_t)((groups > 1 ? gs_elems : ld_elems * outer) * 2)};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_outer, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+    cuuint64_t gd[5];
+    cuuint64_t gs[4];
+    cuuint32_t box[5];
+    cuuint32_t es[5];
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = (cuuint64_t)(dims[i] > 0 ? dims[i] : 1);
+        box[i] = i == 0 ? 64u : (i == 1 ? (cuuint32_t)box1 : 1u);
+        es[i] = 1;
+    }
+    for (int i = 0; i + 1 < rank; ++i) {
+        long long s = strides[i] > 0 ? strides[i] : 8;
+        PARM_CHECK_ARG((s * 2) % 16 == 0, "gemm: stride %lld (dim %d) not a 16-byte multiple", strides[i], i + 1);
+        gs[i] = (cuuint64_t)(s * 2);
+    }
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     PARM_CHECK_ARG(r == CUDA_SUCCESS, "gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
     return 0;
 }
 
-template <int BN, int MA, int MB, int EPI>
+template <int BN, int KIND, int MB, int EPI>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t stream) {
-    using C = Cfg<BN, MA, MB, EPI>;
-    auto kern = grouped_gemm_kernel<BN, MA, MB, EPI>;
+    using C = Cfg<BN, KIND, MB, EPI>;
+    auto kern = moe_gemm_kernel<BN, KIND, MB, EPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
         attr_set = true;
     }
     int grid = p.num_tiles < kNumSMs ? p.num_tiles : kNumSMs;
+    if (grid < 1) grid = 1;
     kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
-    PARM_CHECK_LAUNCH("grouped_gemm");
+    PARM_CHECK_LAUNCH("moe_gemm");
     return 0;
 }
 
-template <int MA, int MB, int EPI>
-static int dispatch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
-    if (bn == 256) return launch<256, MA, MB, EPI>(ta, tb, p, s);
-    if (bn == 128) return launch<128, MA, MB, EPI>(ta, tb, p, s);
-    return launch<64, MA, MB, EPI>(ta, tb, p, s);
+template <int BN, int KIND, int MB, int EPI>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t stream) {
+    using C = CfgPair<BN, KIND, MB, EPI>;
+    auto kern = moe_gemm_pair_kernel<BN, KIND, MB, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        attr_set = true;
+    }
+    int grid = 2 * (p.num_tiles < kNumSMs / 2 ? p.num_tiles : kNumSMs / 2);   // clusters of 2 CTAs
+    if (grid < 2) grid = 2;
+    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+    PARM_CHECK_LAUNCH("moe_gemm_pair");
+    return 0;
+}
+
+template <int KIND, int MB, int EPI>
+static int dispatch_bn(bool pair, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                       cudaStream_t s) {
+    if (pair) {
+        if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, p, s);
+        return launch_pair<128, KIND, MB, EPI>(ta, tb, p, s);
+    }
+    if (bn == 256) return launch<256, KIND, MB, EPI>(ta, tb, p, s);
+    if (bn == 128) return launch<128, KIND, MB, EPI>(ta, tb, p, s);
+    return launch<64, KIND, MB, EPI>(ta, tb, p, s);
+}
+
+// CTA pairs (cta_group::2) by default; PARM_GEMM_SINGLE_CTA=1 selects the 1-CTA kernel (A/B comparisons).
+static bool pair_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("PARM_GEMM_SINGLE_CTA");
+        mode = (e && e[0] == '1') ? 0 : 1;
+    }
+    return mode == 1;
 }
 
 }  // namespace gemm
 
-// Public entry (wrapped by the C ABI in capi.cu).
-int grouped_gemm(int major_a, int major_b, int epi, int M, int N, int K, int groups, const void* A, long long lda,
-                 long long gsa, const void* B, long long ldb, long long gsb, void* D, long long ldd, long long gsd,
-                 const void* aux, long long ld_aux, long long gs_aux, float alpha, cudaStream_t stream) {
+int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
     using namespace gemm;
-    PARM_CHECK_ARG(M > 0 && N > 0 && K > 0 && groups > 0, "gemm: empty problem M=%d N=%d K=%d G=%d", M, N, K, groups);
-    PARM_CHECK_ARG(M % BM == 0, "gemm: M=%d must be a multiple of %d", M, BM);
-    PARM_CHECK_ARG(N % 64 == 0, "gemm: N=%d must be a multiple of 64", N);
-    PARM_CHECK_ARG(K % BK == 0, "gemm: K=%d must be a multiple of %d", K, BK);
-    PARM_CHECK_ARG(epi >= 0 && epi <= 4, "gemm: bad epilogue %d", epi);
-    PARM_CHECK_ARG(epi != kEpiDReluBF16 || aux != nullptr, "gemm: relu-mask epilogue needs aux");
-    const int bn = (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : 64);
+    PARM_CHECK_ARG(q.kind == kRow || q.kind == kWgt, "gemm: bad kind %d", q.kind);
+    PARM_CHECK_ARG(q.groups > 0 && q.nhi > 0 && q.nlo > 0 && q.seg_len > 0, "gemm: empty row space");
+    PARM_CHECK_ARG(q.N > 0 && q.N % 64 == 0, "gemm: N=%d must be a positive multiple of 64", q.N);
+    PARM_CHECK_ARG(q.epi >= 0 && q.epi <= 4, "gemm: bad epilogue %d", q.epi);
+    PARM_CHECK_ARG(q.epi != kEpiDReluBF16 || q.aux.ptr != nullptr, "gemm: relu-mask epilogue needs aux");
+    PARM_CHECK_ARG(q.fill == nullptr || q.groups * q.nhi * q.nlo <= kMaxFill, "gemm: fill table too large");
+    Params p;
+    p.G = q.groups;
+    p.nhi = q.nhi;
+    p.nlo = q.nlo;
+    p.L = q.seg_len;
+    p.M = q.M;
+    p.N = q.N;
+    p.K = q.K;
+    p.alpha = q.alpha;
+    p.fill = q.fill;
+    p.D = const_cast<void*>(q.d.ptr);
+    p.d_ld = q.d.ld;
+    p.d_g = q.d.g_stride;
+    p.d_lo = q.d.lo_stride;
+    p.d_hi = q.d.hi_stride;
+    p.aux = reinterpret_cast<const bf16*>(q.aux.ptr);
+    p.x_ld = q.aux.ld;
+    p.x_g = q.aux.g_stride;
+    p.x_lo = q.aux.lo_stride;
+    p.x_hi = q.aux.hi_stride;
+    const int bn = (q.N % 256 == 0) ? 256 : (q.N % 128 == 0 ? 128 : 64);
+    const bool pair = pair_mode() && bn >= 128;
+    p.n_blocks = q.N / bn;
     CUtensorMap ta, tb;
     int rc;
-    // A: K-major stored [g][m][k] (inner k); MN-major stored [g][k][m] (inner m).
-    if (major_a == kKMajor)
-        rc = make_tmap(&ta, A, K, M, groups, lda, gsa, BM);
-    else
-        rc = make_tmap(&ta, A, M, K, groups, lda, gsa, BK);
-    if (rc) return rc;
-    if (major_b == kKMajor)
-        rc = make_tmap(&tb, B, K, N, groups, ldb, gsb, bn);
-    else
-        rc = make_tmap(&tb, B, N, K, groups, ldb, gsb, BK);
-    if (rc) return rc;
-    Params p;
-    p.M = M;
-    p.N = N;
-    p.K = K;
-    p.groups = groups;
-    p.m_blocks = M / BM;
-    p.n_blocks = N / bn;
-    p.num_tiles = p.m_blocks * p.n_blocks * groups;
-    p.D = D;
-    p.ldd = ldd;
-    p.gsd = gsd;
-    p.aux = reinterpret_cast<const bf16*>(aux);
-    p.ld_aux = ld_aux;
-    p.gs_aux = gs_aux;
-    p.alpha = alpha;
-    const int combo = major_a * 2 + major_b;
-    switch (combo) {
-        case 0:  // K,K : forward GEMMs
-            if (epi == kEpiReluBF16) return dispatch_bn<kKMajor, kKMajor, kEpiReluBF16>(bn, ta, tb, p, stream);
-            if (epi == kEpiBF16) return dispatch_bn<kKMajor, kKMajor, kEpiBF16>(bn, ta, tb, p, stream);
-            if (epi == kEpiF32) return dispatch_bn<kKMajor, kKMajor, kEpiF32>(bn, ta, tb, p, stream);
-            break;
-        case 1:  // K,MN : data-gradient GEMMs
-            if (epi == kEpiDReluBF16) return dispatch_bn<kKMajor, kMNMajor, kEpiDReluBF16>(bn, ta, tb, p, stream);
-            if (epi == kEpiBF16) return dispatch_bn<kKMajor, kMNMajor, kEpiBF16>(bn, ta, tb, p, stream);
-            break;
-        case 3:  // MN,MN : weight-gradient GEMMs
-            if (epi == kEpiF32) return dispatch_bn<kMNMajor, kMNMajor, kEpiF32>(bn, ta, tb, p, stream);
-            if (epi == kEpiF32Acc) return dispatch_bn<kMNMajor, kMNMajor, kEpiF32Acc>(bn, ta, tb, p, stream);
-            break;
-        default:
-            break;
+    if (q.kind == kRow) {
+        PARM_CHECK_ARG(q.K > 0 && q.K % BK == 0, "gemm: K=%d must be a positive multiple of %d", q.K, BK);
+        PARM_CHECK_ARG(q.epi <= kEpiDReluBF16, "gemm: row GEMMs produce bf16");
+        p.m_tiles = (q.seg_len + BM - 1) / BM;
+        p.pairs = (p.nhi * p.nlo * p.m_tiles + 1) / 2;
+        p.num_tiles = pair ? p.G * p.pairs * p.n_blocks : p.G * p.nhi * p.nlo * p.m_tiles * p.n_blocks;
+        p.k_iters = q.K / BK;
+        // A: [hi][lo][g][r][k] -> dims (K, L, G, nlo, nhi)
+        const long long ad[5] = {q.K, q.seg_len, q.groups, q.nlo, q.nhi};
+        const long long as[4] = {q.a.ld, q.a.g_stride, q.a.lo_stride, q.a.hi_stride};
+        if ((rc = make_tmap(&ta, q.a.ptr, 5, ad, as, BM))) return rc;
+        if (q.b_major == kKMajor) {   // B[g][n][k]
+            const long long bd[3] = {q.K, q.N, q.groups};
+            const long long bs[2] = {q.b.ld, q.b.g_stride};
+            rc = make_tmap(&tb, q.b.ptr, 3, bd, bs, pair ? bn / 2 : bn);
+        } else {                      // B[g][k][n]
+            const long long bd[3] = {q.N, q.K, q.groups};
+            const long long bs[2] = {q.b.ld, q.b.g_stride};
+            rc = make_tmap(&tb, q.b.ptr, 3, bd, bs, BK);
+        }
+        if (rc) return rc;
+        const int combo = q.b_major;
+        if (combo == kKMajor) {
+            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(pair, bn, ta, tb, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(pair, bn, ta, tb, p, stream);
+        } else {
+            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(pair, bn, ta, tb, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(pair, bn, ta, tb, p, stream);
+        }
+    } else {
+        PARM_CHECK_ARG(q.M > 0 && q.M % BM == 0, "gemm: M=%d must be a positive multiple of %d", q.M, BM);
+        PARM_CHECK_ARG(q.epi == kEpiF32 || q.epi == kEpiF32Acc, "gemm: weight GEMMs produce f32");
+        p.m_tiles = q.M / BM;
+        p.pairs = (p.m_tiles + 1) / 2;
+        p.num_tiles = pair ? p.G * p.pairs * p.n_blocks : p.G * p.m_tiles * p.n_blocks;
+        p.k_iters = p.nhi * p.nlo * ((q.seg_len + BK - 1) / BK);
+        const long long ad[5] = {q.M, q.seg_len, q.groups, q.nlo, q.nhi};
+        const long long as[4] = {q.a.ld, q.a.g_stride, q.a.lo_stride, q.a.hi_stride};
+        if ((rc = make_tmap(&ta, q.a.ptr, 5, ad, as, BK))) return rc;
+        const long long bd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
+        const long long bs[4] = {q.b.ld, q.b.g_stride, q.b.lo_stride, q.b.hi_stride};
+        if ((rc = make_tmap(&tb, q.b.ptr, 5, bd, bs, BK))) return rc;
+        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(pair, bn, ta, tb, p, stream);
+        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(pair, bn, ta, tb, p, stream);
     }
-    set_error("gemm: unsupported combination major_a=%d major_b=%d epi=%d", major_a, major_b, epi);
+    set_error("gemm: unsupported combination kind=%d b_major=%d epi=%d", q.kind, q.b_major, q.epi);
     return 1;
 }
 

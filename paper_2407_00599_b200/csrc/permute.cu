@@ -87,19 +87,26 @@ __global__ void __launch_bounds__(kRowThreads) combine_fwd_kernel(const SlotView
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
+        // Routing of all k picks first, so the row loads below are independent.
+        int sl[8], ex[8];
+        float wt[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
+            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
+            wt[j] = (sl[j] >= 0) ? combine_w[t * k + j] : 0.0f;
+        }
         for (int c = lane * 8; c < M; c += 256) {
             float acc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
-            for (int j = 0; j < k; ++j) {
-                const int s = slot_idx[t * k + j];
-                if (s < 0) continue;
-                const int e = expert_idx[t * k + j];
-                const float w = combine_w[t * k + j];
-                float f[8];
-                gather_slot(y, e, s, c, f);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) acc[u] = fmaf(w, f[u], acc[u]);
+            for (int j = 0; j < 8; ++j) {
+                if (sl[j] < 0) continue;
+                float f[8];
+                gather_slot(y, ex[j], sl[j], c, f);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = fmaf(wt[j], f[u], acc[u]);
             }
             st_vec8(out + t * ldo + c, f32_to_vec8(acc));
         }
@@ -117,22 +124,23 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(const bf16* __
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
         float dw[8];
+        int sl[8], ex[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dw[j] = 0.0f;
+        for (int j = 0; j < 8; ++j) {
+            dw[j] = 0.0f;
+            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
+            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
+        }
         for (int c = lane * 8; c < M; c += 256) {
             float g[8];
             vec8_to_f32(ld_vec8(dout + t * ldd + c), g);
-            for (int j = 0; j < k; ++j) {
-                const int s = slot_idx[t * k + j];
-                if (s < 0) continue;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (sl[j] < 0) continue;
                 float f[8];
-                gather_slot(y, expert_idx[t * k + j], s, c, f);
-                float d = 0.0f;
+                gather_slot(y, ex[j], sl[j], c, f);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) d = fmaf(g[u], f[u], d);
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    if (jj == j) dw[jj] += d;
+                for (int u = 0; u < 8; ++u) dw[j] = fmaf(g[u], f[u], dw[j]);
             }
         }
 #pragma unroll
@@ -162,12 +170,18 @@ template <int EMAX>
 __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(const SlotView dr, const int* __restrict__ expert_idx,
                                                                     const int* __restrict__ slot_idx,
                                                                     const float* __restrict__ dlogits,
-                                                                    const bf16* __restrict__ wg, int n, int k, int E,
+                                                                    const bf16* __restrict__ wgT, int n, int k, int E,
                                                                     int M, bf16* __restrict__ dx, long long ldx) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
+        int sl[8], ex[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
+            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
+        }
         float dl[EMAX];
         if (dlogits) {
 #pragma unroll
@@ -177,23 +191,23 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(const SlotVie
             float acc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
-            for (int j = 0; j < k; ++j) {
-                const int s = slot_idx[t * k + j];
-                if (s < 0) continue;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (sl[j] < 0) continue;
                 float f[8];
-                gather_slot(dr, expert_idx[t * k + j], s, c, f);
+                gather_slot(dr, ex[j], sl[j], c, f);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) acc[u] += f[u];
             }
-            if (dlogits) {
+            if (dlogits) {   // + dlogits[t] . Wg^T with Wg stored transposed (E, M)
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const bf16* wrow = wg + (long long)(c + u) * E;
-                    float g = 0.0f;
+                for (int e = 0; e < EMAX; ++e) {
+                    if (e < E) {
+                        float w[8];
+                        vec8_to_f32(ld_vec8(wgT + (long long)e * M + c), w);
 #pragma unroll
-                    for (int e = 0; e < EMAX; ++e)
-                        if (e < E) g = fmaf(dl[e], bf2f(wrow[e]), g);
-                    acc[u] += g;
+                        for (int u = 0; u < 8; ++u) acc[u] = fmaf(dl[e], w[u], acc[u]);
+                    }
                 }
             }
             st_vec8(dx + t * ldx + c, f32_to_vec8(acc));

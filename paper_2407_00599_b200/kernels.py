@@ -66,7 +66,7 @@ def gate_fwd(x: torch.Tensor, wg: torch.Tensor, k: int, expert_idx: torch.Tensor
     _need(x, torch.bfloat16, "tokens")
     _need(wg, torch.bfloat16, "gate weights")
     n, M = x.shape
-    E = wg.shape[1]
+    E = wg.shape[0]          # gate weights are stored transposed: (E, M)
     if x.stride(1) != 1 or not wg.is_contiguous():
         raise ValueError("tokens rows and gate weights must be contiguous")
     _lib.call("parm_gate_fwd", x.data_ptr(), x.stride(0), wg.data_ptr(), n, M, E, k, expert_idx.data_ptr(),
@@ -139,7 +139,7 @@ def gate_wgrad(x: torch.Tensor, dlogits: torch.Tensor, dwg: torch.Tensor, worksp
 
 
 class GemmTimer:
-    """Optional CUDA-event bracketing of every grouped GEMM launch (bench.py roofline).
+    """Optional CUDA-event bracketing of every GEMM launch (bench.py roofline).
 
     Events are recorded on the launching (current) stream, so the measured
     interval is the kernel's own duration in stream order.
@@ -157,48 +157,73 @@ class GemmTimer:
 
 gemm_timer: GemmTimer | None = None
 
+ROW, WGT = 0, 1
 
-def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d: torch.Tensor, epi: int,
-                 aux: torch.Tensor | None = None, alpha: float = 1.0) -> None:
-    """D_g = A_g B_g^T for 3-D (G, rows, cols) operands.
 
-    K-major A is (G, M, K); MN-major A is (G, K, M).  Same for B with N.
-    D is (G, M, N) bf16 or f32 according to ``epi``.
-    """
+def _rows(t: torch.Tensor | None) -> _lib.RowsC:
+    """parm_rows for a 5-D [hi][lo][g][r][c] view or a 3-D [g][r][c] tensor (unit inner stride)."""
+    if t is None:
+        return _lib.RowsC(None, 0, 0, 0, 0)
+    if t.stride(-1) != 1:
+        raise ValueError("GEMM operands need a unit inner stride")
+    if t.dim() == 5:
+        return _lib.RowsC(t.data_ptr(), t.stride(3), t.stride(2), t.stride(1), t.stride(0))
+    if t.dim() == 3:
+        return _lib.RowsC(t.data_ptr(), t.stride(1), t.stride(0), 0, 0)
+    raise ValueError(f"GEMM operand must be 3-D or 5-D, got {t.dim()}-D")
+
+
+def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill, flops) -> None:
+    desc = _lib.GemmDescC(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, float(alpha), 0, _rows(a), _rows(b),
+                          _rows(d), _rows(aux), _ptr(fill))
     if gemm_timer is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha)
+        _lib.call("parm_gemm", ctypes.byref(desc), _stream())
         e1.record()
-        G, Mx = a.shape[0], (a.shape[1] if major_a == KMAJOR else a.shape[2])
-        Kx = a.shape[2] if major_a == KMAJOR else a.shape[1]
-        Nx = b.shape[1] if major_b == KMAJOR else b.shape[2]
-        gemm_timer.pairs.append((e0, e1, 2 * G * Mx * Nx * Kx))   # executed (padded) FLOPs
+        gemm_timer.pairs.append((e0, e1, flops))
         return
-    _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha)
+    _lib.call("parm_gemm", ctypes.byref(desc), _stream())
 
 
-def _grouped_gemm(a, major_a, b, major_b, d, epi, aux, alpha) -> None:
+def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, epi: int,
+              aux: torch.Tensor | None = None, fill: torch.Tensor | None = None, alpha: float = 1.0) -> None:
+    """ROW GEMM: D[hi][lo][g][r][n] = alpha * A[hi][lo][g][r][:] . B[g][n][:] (5-D A/D, 3-D weights B)."""
     _need(a, torch.bfloat16, "A")
     _need(b, torch.bfloat16, "B")
-    G = a.shape[0]
+    _need(d, torch.bfloat16, "D")
+    nhi, nlo, G, L, Kd = a.shape
+    N = b.shape[1] if b_major == KMAJOR else b.shape[2]
+    if tuple(d.shape) != (nhi, nlo, G, L, N) or b.shape[0] != G:
+        raise ValueError(f"gemm_rows shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
+    if aux is not None and tuple(aux.shape) != tuple(d.shape):
+        raise ValueError("aux must be shaped like D")
+    _gemm(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill,
+          2 * nhi * nlo * G * L * N * Kd)
+
+
+def gemm_wgrad(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epi: int = EPI_F32,
+               fill: torch.Tensor | None = None, alpha: float = 1.0) -> None:
+    """WGT GEMM: D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n] (f32 D)."""
+    _need(a, torch.bfloat16, "A")
+    _need(b, torch.bfloat16, "B")
+    _need(d, torch.float32, "D")
+    nhi, nlo, G, L, M = a.shape
+    N = b.shape[4]
+    if tuple(b.shape[:4]) != (nhi, nlo, G, L) or tuple(d.shape) != (G, M, N):
+        raise ValueError(f"gemm_wgrad shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
+    _gemm(WGT, epi, MNMAJOR, G, nhi, nlo, L, M, N, 0, alpha, a, b, d, None, fill, 2 * nhi * nlo * G * L * M * N)
+
+
+def grouped_gemm(a: torch.Tensor, major_a: int, b: torch.Tensor, major_b: int, d: torch.Tensor, epi: int,
+                 aux: torch.Tensor | None = None, alpha: float = 1.0) -> None:
+    """Plain 3-D grouped GEMM D_g = A_g B_g^T (K-major A: (G, M, K); MN-major A: (G, K, M); same for B)."""
     if major_a == KMAJOR:
-        M, K = a.shape[1], a.shape[2]
+        u = lambda t: t.unsqueeze(0).unsqueeze(0)  # noqa: E731  (G, R, C) -> (1, 1, G, R, C)
+        gemm_rows(u(a), b, major_b, u(d), epi, aux=u(aux) if aux is not None else None, alpha=alpha)
     else:
-        K, M = a.shape[1], a.shape[2]
-    N = b.shape[1] if major_b == KMAJOR else b.shape[2]
-    Kb = b.shape[2] if major_b == KMAJOR else b.shape[1]
-    if Kb != K or b.shape[0] != G or tuple(d.shape) != (G, M, N):
-        raise ValueError(f"grouped_gemm shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
-    for t, nm in ((a, "A"), (b, "B"), (d, "D")):
-        if t.stride(2) != 1:
-            raise ValueError(f"{nm} needs a unit inner stride")
-    want = torch.float32 if epi in (EPI_F32, EPI_F32_ACC) else torch.bfloat16
-    _need(d, want, "D")
-    if aux is not None:
-        _need(aux, torch.bfloat16, "aux")
-    _lib.call("parm_grouped_gemm", major_a, major_b, epi, M, N, K, G, a.data_ptr(), a.stride(1), a.stride(0),
-              b.data_ptr(), b.stride(1), b.stride(0), d.data_ptr(), d.stride(1), d.stride(0), _ptr(aux),
-              aux.stride(1) if aux is not None else 0, aux.stride(0) if aux is not None else 0, float(alpha),
-              _stream())
+        if major_b != MNMAJOR:
+            raise ValueError("MN-major A needs MN-major B")
+        u = lambda t: t.unsqueeze(0).unsqueeze(0)  # noqa: E731
+        gemm_wgrad(u(a), u(b), d, epi, alpha=alpha)

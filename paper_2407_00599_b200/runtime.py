@@ -2,10 +2,11 @@
 
 ``MoELayer`` owns, for every rank this process executes, the bf16 expert
 shards (W1/W2 stored transposed so every forward GEMM operand is K-major),
-the gate weights, f32 gradient buffers and one preallocated buffer set per
-schedule.  ``forward(schedule, xs)`` / ``backward(douts)`` run the
-reference's schedules (moesched dataplane.py:220-413) as sm_100a kernels
-(libparm_b200.so) plus collectives from ``world.py``:
+the gate weights (stored transposed, (E, M)), f32 gradient buffers and one
+preallocated buffer set per schedule.  ``forward(schedule, xs)`` /
+``backward(douts)`` run the reference's schedules (moesched
+dataplane.py:220-413) as sm_100a kernels (libparm_b200.so) plus collectives
+from ``world.py``:
 
   baseline  gate | AG_esp(x) -> N_ESP gates -> dispatch -> A2A_ep -> FFN ->
             AR_esp -> A2A_ep -> own slot range -> combine           (DeepSpeed-MoE order)
@@ -13,6 +14,15 @@ reference's schedules (moesched dataplane.py:220-413) as sm_100a kernels
             A2A(ep&esp) -> FFN -> A2A(ep&esp) + ESP sum fused into combine -> AG_mp
   s2        gate(block) -> dispatch of own slot shard (pad to ceil(T/MP)*MP) ->
             fused A2A -> FFN -> A2A -> ESP sum -> AG_mp(slots) -> combine
+
+Data layout.  Every expert-row tensor (received tokens,
+hidden, outputs and their gradients) is the AlltoAll receive layout
+``[src_hi][src_lo][expert][row][col]`` — s1/s2: (P, 1, e_local, q, C) with
+src = the token owner; baseline: (N_EP, N_ESP, e_local, T, C) with (owner,
+gathered block) — so every exchange is ONE message per peer (NCCL P2P
+throughput collapses with message count) and the grouped GEMM reads/writes
+it directly through 5-D TMA maps.  Each source also ships its per-expert fill
+counts, so the GEMM skips tiles of unfilled capacity slots.
 
 Backward (no reference) is the adjoint of each sequence
 under the replicated-MP convention the paper uses (split <-> AllGather,
@@ -22,9 +32,8 @@ counted once.  The baseline processes each token N_MP times (its duplicated
 computation), so its expert weight gradients are scaled by 1/N_MP in the
 wgrad GEMM epilogue to report the same quantity.
 
-Padding: embed M and shard width H/ESP are padded to multiples of 128 and the
-per-expert row count to a multiple of 128 with zeros, so every shape meets
-the GEMM contract without changing results (zero rows/columns contribute 0).
+Padding: embed M and shard width H/ESP are padded to multiples of 128 with
+zeros, so every shape meets the GEMM contract without changing results.
 """
 
 from __future__ import annotations
@@ -37,7 +46,7 @@ import torch
 
 from . import kernels as K
 from .config import MoEConfig, ParallelLayout, check_compatible, derive_capacity, group_members
-from .world import LocalWorld, Msg, World, make_world
+from .world import Msg, World, make_world
 
 SCHEDULES = ("baseline", "s1", "s2")
 
@@ -86,28 +95,42 @@ class Routing:
     token_offset: int = 0
 
     @classmethod
-    def alloc(cls, n: int, k: int, E: int, cap: int, dev, token_offset: int = 0) -> "Routing":
+    def alloc(cls, n: int, k: int, E: int, cap: int, dev, token_offset: int = 0,
+              fill: torch.Tensor | None = None) -> "Routing":
         i32 = dict(dtype=torch.int32, device=dev)
         f32 = dict(dtype=torch.float32, device=dev)
         return cls(torch.empty(n, k, **i32), torch.empty(n, k, **f32), torch.empty(n, E, **f32),
-                   torch.empty(n, k, **i32), torch.empty(E, max(cap, 1), **i32), torch.empty(E, **i32), cap,
-                   token_offset)
+                   torch.empty(n, k, **i32), torch.empty(E, max(cap, 1), **i32),
+                   fill if fill is not None else torch.zeros(E, **i32), cap, token_offset)
 
-    def run(self, x: torch.Tensor, wg: torch.Tensor, k: int) -> None:
-        K.gate_fwd(x, wg, k, self.expert_idx, self.combine_w, self.probs)
-        K.gate_slots(self.expert_idx, wg.shape[1], self.cap, self.slot_idx, self.slot_src, self.fill)
+    def run(self, x: torch.Tensor, wg_t: torch.Tensor, k: int) -> None:
+        K.gate_fwd(x, wg_t, k, self.expert_idx, self.combine_w, self.probs)
+        K.gate_slots(self.expert_idx, wg_t.shape[0], self.cap, self.slot_idx, self.slot_src, self.fill)
 
 
 @dataclass
 class RankState:
     rank: int
-    gate: torch.Tensor            # (Mp, E) bf16
+    gate: torch.Tensor            # (E, Mp) bf16, transposed (one 16-B load per lane per expert)
     w1t: torch.Tensor             # (e_local, Hsp, Mp) bf16
     w2t: torch.Tensor             # (e_local, Mp, Hsp) bf16
-    dgate: torch.Tensor           # (Mp, E) f32
+    dgate: torch.Tensor           # (E, Mp) f32
     dw1t: torch.Tensor            # (e_local, Hsp, Mp) f32
     dw2t: torch.Tensor            # (e_local, Mp, Hsp) f32
     bufs: dict = field(default_factory=dict)
+
+
+@dataclass
+class StepGraph:
+    """A captured forward+backward step; ``outs``/``dxs`` alias the layer's buffers."""
+
+    graph: torch.cuda.CUDAGraph
+    outs: dict
+    dxs: dict
+    schedule: str
+
+    def replay(self) -> None:
+        self.graph.replay()
 
 
 class MoELayer:
@@ -127,8 +150,8 @@ class MoELayer:
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
         for r in self.ranks:
-            self.st[r] = RankState(r, torch.zeros(d.Mp, d.E, **bf), torch.zeros(d.e_local, d.Hsp, d.Mp, **bf),
-                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **bf), torch.zeros(d.Mp, d.E, **f32),
+            self.st[r] = RankState(r, torch.zeros(d.E, d.Mp, **bf), torch.zeros(d.e_local, d.Hsp, d.Mp, **bf),
+                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **bf), torch.zeros(d.E, d.Mp, **f32),
                                    torch.zeros(d.e_local, d.Hsp, d.Mp, **f32),
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
         self._last: str | None = None
@@ -146,7 +169,7 @@ class MoELayer:
             p = self.layout.esp_pos(r)
             g = torch.from_numpy(np.ascontiguousarray(weights.gate)).to(torch.float32)
             s.gate.zero_()
-            s.gate[:d.M].copy_(g.to(self.dev).to(torch.bfloat16))
+            s.gate[:, :d.M].copy_(g.t().to(self.dev).to(torch.bfloat16))
             s.w1t.zero_()
             s.w2t.zero_()
             for i, e in enumerate(self.local_experts(r)):
@@ -162,8 +185,8 @@ class MoELayer:
         for r, s in self.st.items():
             gen = torch.Generator(device=self.dev).manual_seed(seed * 7919 + r)
             s.gate.zero_()
-            s.gate[:d.M].copy_(torch.randn(d.M, d.E, generator=torch.Generator(device=self.dev).manual_seed(seed),
-                                           device=self.dev))
+            s.gate[:, :d.M].copy_(torch.randn(d.M, d.E, generator=torch.Generator(device=self.dev).manual_seed(seed),
+                                              device=self.dev).t())
             s.w1t.zero_()
             s.w2t.zero_()
             s.w1t[:, :d.Hs, :d.M].copy_(torch.randn(d.e_local, d.Hs, d.M, generator=gen, device=self.dev)
@@ -175,7 +198,7 @@ class MoELayer:
         """Gradients in the reference layout: dw1 (e_local, M, Hs), dw2 (e_local, Hs, M), dgate (M, E)."""
         d, s = self.d, self.st[rank]
         return {"dw1": s.dw1t[:, :d.Hs, :d.M].transpose(1, 2), "dw2": s.dw2t[:, :d.M, :d.Hs].transpose(1, 2),
-                "dgate": s.dgate[:d.M]}
+                "dgate": s.dgate[:, :d.M].t()}
 
     # ------------------------------------------------------------ buffers
     def _plan(self, schedule: str, r: int) -> dict:
@@ -184,58 +207,68 @@ class MoELayer:
             return s.bufs[schedule]
         d, dev = self.d, self.dev
         bf = dict(dtype=torch.bfloat16, device=dev)
-        b: dict = {}
-        b["x"] = torch.zeros(d.n, d.Mp, **bf)          # padded input (alias of caller's when M == Mp)
-        b["out"] = torch.zeros(d.n, d.Mp, **bf)
-        b["dout"] = torch.zeros(d.n, d.Mp, **bf)
-        b["dx"] = torch.zeros(d.n, d.Mp, **bf)
-        if schedule in ("s1", "s2") or d.P == 1:
-            if schedule == "s1" or d.P == 1:
-                q = math.ceil(d.T / d.MP)
-                rows_tok = d.n // d.MP
-                b["route"] = Routing.alloc(rows_tok, d.k, d.E, q, dev, token_offset=self.layout.mp_pos(r) * rows_tok)
-            else:
-                q = math.ceil(d.T / d.MP)
+        i32 = dict(dtype=torch.int32, device=dev)
+        el = d.e_local
+        b: dict = {"out": torch.zeros(d.n, d.Mp, **bf), "dx": torch.zeros(d.n, d.Mp, **bf)}
+        if d.M != d.Mp:
+            b["x"] = torch.zeros(d.n, d.Mp, **bf)
+            b["dout"] = torch.zeros(d.n, d.Mp, **bf)
+        if schedule == "_local" or schedule in ("s1", "s2"):
+            q = math.ceil(d.T / d.MP)
+            if schedule == "s2":
                 b["route"] = Routing.alloc(d.n, d.k, d.E, d.T, dev)
-            rows = d.P * q
-            rows_pad = _ceil_to(rows, 128)
-            b.update(q=q, rows=rows, rows_pad=rows_pad)
+            else:   # s1 (and P == 1): this MP rank's token slice, slot quota ceil(T / MP)
+                sl = d.n // d.MP
+                b["route"] = Routing.alloc(sl, d.k, d.E, q, dev, token_offset=self.layout.mp_pos(r) * sl)
+            b["q"] = q
             b["send"] = torch.zeros(d.E, q, d.Mp, **bf)
-            b["recv"] = torch.zeros(d.e_local, rows_pad, d.Mp, **bf)
-            b["dyrecv"] = torch.zeros(d.e_local, rows_pad, d.Mp, **bf)
-            b["ret"] = torch.zeros(d.P, d.e_local, q, d.Mp, **bf)
-            b["dret"] = torch.zeros(d.P, d.e_local, q, d.Mp, **bf)
-            if schedule == "s2" and d.P > 1:
-                b["comb"] = torch.zeros(d.E, q, d.Mp, **bf)
-                b["gath"] = torch.zeros(d.MP, d.E, q, d.Mp, **bf)
-                b["dcomb"] = torch.zeros(d.E, q, d.Mp, **bf)
-                b["dgath"] = torch.zeros(d.MP, d.E, q, d.Mp, **bf)
+            b["dsend"] = torch.zeros(d.E, q, d.Mp, **bf)
+            if d.P == 1:     # no exchange: the slot tensors ARE the GEMM operands
+                b["recv"] = b["send"].view(1, 1, d.E, q, d.Mp)
+                b["dyrecv"] = b["dsend"].view(1, 1, d.E, q, d.Mp)
+                b["fill_in"] = b["route"].fill.view(1, 1, d.E)
+            else:
+                b["recv"] = torch.zeros(d.P, 1, el, q, d.Mp, **bf)
+                b["dyrecv"] = torch.zeros(d.P, 1, el, q, d.Mp, **bf)
+                b["fill_in"] = torch.zeros(d.P, 1, el, **i32)
+            shape = (d.P, 1, el, q)
         else:  # baseline, P > 1
-            gs = d.ESP * d.T
-            rows = d.EP * gs
-            rows_pad = _ceil_to(rows, 128)
-            b.update(q=d.T, gs=gs, rows=rows, rows_pad=rows_pad)
+            b["q"] = d.T
             b["route"] = Routing.alloc(d.n, d.k, d.E, d.T, dev)
-            b["route_blk"] = [Routing.alloc(d.n, d.k, d.E, d.T, dev) for _ in range(d.ESP)]
+            b["blk_fill"] = torch.zeros(d.ESP, d.E, **i32)
+            b["route_blk"] = [Routing.alloc(d.n, d.k, d.E, d.T, dev, fill=b["blk_fill"][q]) for q in range(d.ESP)]
             b["xg"] = torch.zeros(d.ESP, d.n, d.Mp, **bf)
-            b["disp"] = torch.zeros(d.E, gs, d.Mp, **bf)
-            b["recv"] = torch.zeros(d.e_local, rows_pad, d.Mp, **bf)
-            b["dyrecv"] = torch.zeros(d.e_local, rows_pad, d.Mp, **bf)
-            b["ret"] = torch.zeros(d.E, gs, d.Mp, **bf)
+            b["disp"] = torch.zeros(d.ESP, d.E, d.T, d.Mp, **bf)             # [block q][e][slot]
+            b["recv"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # [owner][block][i][slot]
+            b["dyrecv"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
+            b["fill_in"] = torch.zeros(d.EP, d.ESP, el, **i32)
             b["dyown"] = torch.zeros(d.E, d.T, d.Mp, **bf)
             b["dyg"] = torch.zeros(d.ESP, d.E, d.T, d.Mp, **bf)
-            b["dd"] = torch.zeros(d.E, gs, d.Mp, **bf)
             b["dg"] = torch.zeros(d.ESP, d.n, d.Mp, **bf)
-        rp = b["rows_pad"]
-        b["h"] = torch.zeros(d.e_local, rp, d.Hsp, **bf)
-        b["y"] = torch.zeros(d.e_local, rp, d.Mp, **bf)
-        b["dh"] = torch.zeros(d.e_local, rp, d.Hsp, **bf)
-        b["dr"] = torch.zeros(d.e_local, rp, d.Mp, **bf)
+            shape = (d.EP, d.ESP, el, d.T)
+        b["h"] = torch.zeros(*shape, d.Hsp, **bf)
+        b["y"] = torch.zeros(*shape, d.Mp, **bf)
+        b["dh"] = torch.zeros(*shape, d.Hsp, **bf)
+        b["dr"] = torch.zeros(*shape, d.Mp, **bf)
+        if schedule == "baseline":
+            b["ret"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # owner side [holder j][block][i][slot]
+            b["dd"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
+        elif d.P == 1:
+            b["ret"] = b["y"].view(1, d.E, b["q"], d.Mp)
+            b["dret"] = b["dr"].view(1, d.E, b["q"], d.Mp)
+        else:
+            b["ret"] = torch.zeros(d.P, el, b["q"], d.Mp, **bf)
+            b["dret"] = torch.zeros(d.P, el, b["q"], d.Mp, **bf)
+            if schedule == "s2":
+                b["comb"] = torch.zeros(d.E, b["q"], d.Mp, **bf)
+                b["gath"] = torch.zeros(d.MP, d.E, b["q"], d.Mp, **bf)
+                b["dcomb"] = torch.zeros(d.E, b["q"], d.Mp, **bf)
+                b["dgath"] = torch.zeros(d.MP, d.E, b["q"], d.Mp, **bf)
         nr = b["route"].expert_idx.shape[0]
         b["dlogits"] = torch.zeros(nr, d.E, dtype=torch.float32, device=dev)
-        if self._ws_gate is None or self._ws_gate.numel() * 4 < K.gate_wgrad_workspace(d.n, d.Mp, d.E):
-            self._ws_gate = torch.empty(max(1, K.gate_wgrad_workspace(d.n, d.Mp, d.E) // 4), dtype=torch.float32,
-                                        device=dev)
+        need = K.gate_wgrad_workspace(d.n, d.Mp, d.E)
+        if self._ws_gate is None or self._ws_gate.numel() * 4 < need:
+            self._ws_gate = torch.empty(max(1, need // 4), dtype=torch.float32, device=dev)
         s.bufs[schedule] = b
         return b
 
@@ -252,53 +285,62 @@ class MoELayer:
 
     # ------------------------------------------------------------ FFN
     def _ffn_fwd(self, s: RankState, b: dict) -> None:
-        K.grouped_gemm(b["recv"], K.KMAJOR, s.w1t, K.KMAJOR, b["h"], K.EPI_RELU)
-        K.grouped_gemm(b["h"], K.KMAJOR, s.w2t, K.KMAJOR, b["y"], K.EPI_BF16)
+        K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU, fill=b["fill_in"])
+        K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"])
 
     def _ffn_bwd(self, s: RankState, b: dict, wscale: float = 1.0) -> None:
-        K.grouped_gemm(b["dyrecv"], K.KMAJOR, s.w2t, K.MNMAJOR, b["dh"], K.EPI_DRELU, aux=b["h"])
-        K.grouped_gemm(b["dyrecv"], K.MNMAJOR, b["h"], K.MNMAJOR, s.dw2t, K.EPI_F32, alpha=wscale)
-        K.grouped_gemm(b["dh"], K.MNMAJOR, b["recv"], K.MNMAJOR, s.dw1t, K.EPI_F32, alpha=wscale)
-        K.grouped_gemm(b["dh"], K.KMAJOR, s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16)
+        f = b["fill_in"]
+        K.gemm_rows(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DRELU, aux=b["h"], fill=f)
+        K.gemm_wgrad(b["dyrecv"], b["h"], s.dw2t, K.EPI_F32, fill=f, alpha=wscale)
+        K.gemm_wgrad(b["dh"], b["recv"], s.dw1t, K.EPI_F32, fill=f, alpha=wscale)
+        K.gemm_rows(b["dh"], s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16, fill=f)
 
     # ------------------------------------------------------------ message plans
-    def _fused_msgs(self, src_key: str, dst_key: str, schedule: str) -> list[Msg]:
-        """EP&ESP AlltoAll of the dumped dispatch (collectives.py:256-283):
-        destination d gets source s's expert block ep_pos(d); expert-major receive."""
+    def _owned(self, *ranks) -> bool:
+        return any(self.world.owns(r) for r in ranks)
+
+    def _buf(self, rank: int, schedule: str, key: str):
+        return self.st[rank].bufs[schedule][key] if self.world.owns(rank) else None
+
+    def _fused_msgs(self, schedule: str, send_key: str, recv_key: str, with_fill: bool,
+                    fill_key: str = "fill") -> list[Msg]:
+        """EP&ESP AlltoAll of the dumped dispatch (collectives.py:256-283): every
+        destination d receives from every source s the expert block ep_pos(d) —
+        one contiguous (e_local, q, M) message per pair — plus, forward, the
+        source's fill counts of those experts."""
         L, d = self.layout, self.d
+        el = d.e_local
         msgs = []
         for s in range(d.P):
             for dst in range(d.P):
-                if not (self.world.owns(s) or self.world.owns(dst)):
+                if not self._owned(s, dst):
                     continue
-                for i in range(d.e_local):
-                    e = L.ep_pos(dst) * d.e_local + i
-                    sv = self.st[s].bufs[schedule][src_key][e] if self.world.owns(s) else None
-                    if self.world.owns(dst):
-                        bq = self.st[dst].bufs[schedule]
-                        rv = bq[dst_key][i, s * bq["q"]:(s + 1) * bq["q"]]
-                    else:
-                        rv = None
-                    msgs.append(Msg(s, dst, sv, rv))
+                j = L.ep_pos(dst)
+                sv = self._buf(s, schedule, send_key)
+                rv = self._buf(dst, schedule, recv_key)
+                msgs.append(Msg(s, dst, None if sv is None else sv[j * el:(j + 1) * el],
+                                None if rv is None else rv[s, 0]))
+                if with_fill:
+                    fs = None
+                    if self.world.owns(s):
+                        bs = self.st[s].bufs[schedule]
+                        fs = bs["route"].fill if fill_key == "fill" else bs[fill_key]
+                    fr = self._buf(dst, schedule, "fill_in")
+                    msgs.append(Msg(s, dst, None if fs is None else fs[j * el:(j + 1) * el],
+                                    None if fr is None else fr[s, 0]))
         return msgs
 
-    def _return_msgs(self, src_key: str, dst_key: str, schedule: str) -> list[Msg]:
-        """Return AlltoAll (fused_combine's exchange): holder h sends rows of
-        owner o back to o, landing at ret[o][h][i]."""
+    def _return_msgs(self, schedule: str, src_key: str, dst_key: str) -> list[Msg]:
+        """Return AlltoAll (fused_combine's exchange): holder h sends owner o's rows back."""
         d = self.d
         msgs = []
         for h in range(d.P):
             for o in range(d.P):
-                if not (self.world.owns(h) or self.world.owns(o)):
+                if not self._owned(h, o):
                     continue
-                for i in range(d.e_local):
-                    if self.world.owns(h):
-                        bh = self.st[h].bufs[schedule]
-                        sv = bh[src_key][i, o * bh["q"]:(o + 1) * bh["q"]]
-                    else:
-                        sv = None
-                    rv = self.st[o].bufs[schedule][dst_key][h, i] if self.world.owns(o) else None
-                    msgs.append(Msg(h, o, sv, rv))
+                sv = self._buf(h, schedule, src_key)
+                rv = self._buf(o, schedule, dst_key)
+                msgs.append(Msg(h, o, None if sv is None else sv[o, 0], None if rv is None else rv[h]))
         return msgs
 
     def _ret_view(self, b: dict, key: str) -> K.SlotView:
@@ -326,6 +368,27 @@ class MoELayer:
         fn = {"baseline": self._bwd_baseline, "s1": self._bwd_s1, "s2": self._bwd_s2}[self._last]
         return fn(douts)
 
+    def capture_step(self, schedule: str, xs: dict, douts: dict, warmup: int = 2) -> StepGraph:
+        """Record one forward+backward of ``schedule`` (every kernel and every
+        NCCL call) into a CUDA graph over the layer's static buffers; replaying
+        it costs one host launch per step instead of ~30 kernel + comm launches.
+        ``xs``/``douts`` are the device tensors the graph reads (refill them
+        in place between replays)."""
+        for _ in range(warmup):            # allocate plans and settle NCCL state outside capture
+            self.forward(schedule, xs)
+            self.backward(douts)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                outs = self.forward(schedule, xs)
+                dxs = self.backward(douts)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        return StepGraph(g, outs, dxs, schedule)
+
     def routing(self, rank: int) -> Routing:
         """Routing of the last forward on ``rank``: its own block (baseline, s2)
         or its MP token slice (s1; ``token_offset`` locates the slice)."""
@@ -343,11 +406,9 @@ class MoELayer:
             b["xin"] = x
             rt = b["route"]
             rt.run(x, s.gate, d.k)
-            # slots straight into the expert-major FFN input (no exchange at P = 1)
-            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["recv"][:, :b["q"]])
+            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["send"])
             self._ffn_fwd(s, b)
-            view = K.SlotView(b["y"], e_local=d.E, stride_i=b["rows_pad"] * d.Mp, stride_slo=d.Mp)
-            K.combine_fwd(view, rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
+            K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
             outs[r] = b["out"][:, :d.M]
         self._last = schedule
         return outs
@@ -360,12 +421,11 @@ class MoELayer:
             b = s.bufs["_local"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            view = K.SlotView(b["y"], e_local=d.E, stride_i=b["rows_pad"] * d.Mp, stride_slo=d.Mp)
-            K.combine_bwd(dout, view, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dyrecv"][:, :b["q"]], scale=rt.combine_w)
+            K.combine_bwd(dout, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
             self._ffn_bwd(s, b)
-            dview = K.SlotView(b["dr"], e_local=d.E, stride_i=b["rows_pad"] * d.Mp, stride_slo=d.Mp)
-            K.dispatch_bwd(dview, rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E, b["dx"])
+            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+                           b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             res[r] = b["dx"][:, :d.M]
         return res
@@ -377,17 +437,16 @@ class MoELayer:
         for r in self.ranks:
             s, b = self.st[r], self._plan("s1", r)
             x = self._input(b, xs[r], "x")
-            b["xin"] = x
             m = L.mp_pos(r)
-            xs_ = x[m * sl:(m + 1) * sl]
+            xs_ = x[m * sl:(m + 1) * sl]                # MP split: this rank's token slice
             b["xslice"] = xs_
             rt = b["route"]
             rt.run(xs_, s.gate, d.k)
             K.dispatch_rows(xs_, rt.slot_src, d.k, rt.cap, 0, b["send"])
-        self.world.exchange(self._fused_msgs("send", "recv", "s1"))
+        self.world.exchange(self._fused_msgs("s1", "send", "recv", with_fill=True))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
-        self.world.exchange(self._return_msgs("y", "ret", "s1"))
+        self.world.exchange(self._return_msgs("s1", "y", "ret"))
         ins, outs = {}, {}
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
@@ -410,11 +469,11 @@ class MoELayer:
             ds = dout[m * sl:(m + 1) * sl]          # adjoint of AG_mp: own slice
             rt = b["route"]
             K.combine_bwd(ds, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(ds, rt.slot_src, d.k, rt.cap, 0, b["send"], scale=rt.combine_w)
-        self.world.exchange(self._fused_msgs("send", "dyrecv", "s1"))   # adjoint of ESP sum + A2A
+            K.dispatch_rows(ds, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
+        self.world.exchange(self._fused_msgs("s1", "dsend", "dyrecv", with_fill=False))  # adjoint of ESP sum + A2A
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
-        self.world.exchange(self._return_msgs("dr", "dret", "s1"))      # adjoint of dump + A2A
+        self.world.exchange(self._return_msgs("s1", "dr", "dret"))                  # adjoint of dump + A2A
         ins, outs, gins = {}, {}, {}
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s1"]
@@ -445,10 +504,15 @@ class MoELayer:
             rt = b["route"]
             rt.run(x, s.gate, d.k)
             K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"])
-        self.world.exchange(self._fused_msgs("send", "recv", "s2"))
+            # fill of this rank's slot shard [m*q, (m+1)*q): clamp(fill - m*q, 0, q) per expert
+            if "shard_fill" not in b:
+                b["shard_fill"] = torch.zeros(d.E, dtype=torch.int32, device=self.dev)
+            torch.sub(rt.fill, L.mp_pos(r) * b["q"], out=b["shard_fill"])
+            b["shard_fill"].clamp_(0, b["q"])
+        self.world.exchange(self._fused_msgs("s2", "send", "recv", with_fill=True, fill_key="shard_fill"))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
-        self.world.exchange(self._return_msgs("y", "ret", "s2"))
+        self.world.exchange(self._return_msgs("s2", "y", "ret"))
         ins, outs = {}, {}
         for r in self.ranks:
             b = self.st[r].bufs["s2"]
@@ -470,11 +534,11 @@ class MoELayer:
             rt = b["route"]
             K.combine_bwd(dout, self._gath_view(b, "gath"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             # adjoint of AG_mp over slots: only this rank's slot shard
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"], scale=rt.combine_w)
-        self.world.exchange(self._fused_msgs("send", "dyrecv", "s2"))
+            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["dsend"], scale=rt.combine_w)
+        self.world.exchange(self._fused_msgs("s2", "dsend", "dyrecv", with_fill=False))
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
-        self.world.exchange(self._return_msgs("dr", "dret", "s2"))
+        self.world.exchange(self._return_msgs("s2", "dr", "dret"))
         ins, outs = {}, {}
         for r in self.ranks:
             b = self.st[r].bufs["s2"]
@@ -490,6 +554,13 @@ class MoELayer:
         return {r: self.st[r].bufs["s2"]["dx"][:, :d.M] for r in self.ranks}
 
     # ------------------------------------------------------------ baseline
+    def _ret_own_view(self, b: dict, key: str, q: int) -> K.SlotView:
+        """Owner-side slots of gathered block q: row (e, s) = buf[ep_e][q][i_e][s]."""
+        d = self.d
+        el = d.e_local
+        return K.SlotView(b[key], e_local=el, stride_ep=d.ESP * el * d.T * d.Mp, stride_i=d.T * d.Mp,
+                          stride_slo=d.Mp, offset=q * el * d.T * d.Mp)
+
     def _fwd_baseline(self, xs: dict) -> dict:
         d, L = self.d, self.layout
         ins, outs = {}, {}
@@ -505,61 +576,58 @@ class MoELayer:
             for q in range(d.ESP):                               # re-gate every gathered block
                 rt = b["route_blk"][q]
                 rt.run(b["xg"][q], s.gate, d.k)
-                K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][:, q * d.T:(q + 1) * d.T])
-        self.world.exchange(self._ep_msgs_fwd())
+                K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][q])
+        self.world.exchange(self._ep_dispatch_msgs("disp", "recv", with_fill=True))
         ys = {}
         for r in self.ranks:
             b = self.st[r].bufs["baseline"]
             self._ffn_fwd(self.st[r], b)
             ys[r] = b["y"]
         self.world.allreduce("esp", ys)                          # ESP-AllReduce of shard partials
-        self.world.exchange(self._ep_msgs_ret())
+        self.world.exchange(self._ep_return_msgs("y", "ret"))
         for r in self.ranks:
             b = self.st[r].bufs["baseline"]
             rt = b["route"]
-            view = K.SlotView(b["ret"], e_local=d.E, stride_i=b["gs"] * d.Mp, stride_slo=d.Mp,
-                              offset=L.esp_pos(r) * d.T * d.Mp)  # own slot range (ESP split)
-            K.combine_fwd(view, rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
+            K.combine_fwd(self._ret_own_view(b, "ret", L.esp_pos(r)), rt.expert_idx, rt.slot_idx, rt.combine_w,
+                          b["out"])                              # own slot range (ESP split)
         self._last = "baseline"
         return {r: self.st[r].bufs["baseline"]["out"][:, :d.M] for r in self.ranks}
 
-    def _ep_msgs_fwd(self) -> list[Msg]:
-        """EP-AlltoAll of whole expert blocks: owner o -> holder h = EP member j."""
+    def _ep_dispatch_msgs(self, src_key: str, dst_key: str, with_fill: bool) -> list[Msg]:
+        """EP-AlltoAll of expert blocks: owner o -> holder h (EP member j), one
+        message per gathered block q (src [q][j-block] is contiguous)."""
         d, L = self.d, self.layout
+        el = d.e_local
         msgs = []
         for o in range(d.P):
-            grp = group_members(L, "ep", o)
-            for j, h in enumerate(grp):
-                if not (self.world.owns(o) or self.world.owns(h)):
+            for j, h in enumerate(group_members(L, "ep", o)):
+                if not self._owned(o, h):
                     continue
-                for i in range(d.e_local):
-                    sv = self.st[o].bufs["baseline"]["disp"][j * d.e_local + i] if self.world.owns(o) else None
-                    if self.world.owns(h):
-                        bh = self.st[h].bufs["baseline"]
-                        pos = L.ep_pos(o)
-                        rv = bh["recv"][i, pos * bh["gs"]:(pos + 1) * bh["gs"]]
-                    else:
-                        rv = None
-                    msgs.append(Msg(o, h, sv, rv))
+                pos = L.ep_pos(o)
+                sv = self._buf(o, "baseline", src_key)
+                rv = self._buf(h, "baseline", dst_key)
+                bf = self._buf(o, "baseline", "blk_fill")
+                rf = self._buf(h, "baseline", "fill_in")
+                for q in range(d.ESP):
+                    msgs.append(Msg(o, h, None if sv is None else sv[q, j * el:(j + 1) * el],
+                                    None if rv is None else rv[pos, q]))
+                    if with_fill:
+                        msgs.append(Msg(o, h, None if bf is None else bf[q, j * el:(j + 1) * el],
+                                        None if rf is None else rf[pos, q]))
         return msgs
 
-    def _ep_msgs_ret(self, src_key: str = "y", dst_key: str = "ret") -> list[Msg]:
+    def _ep_return_msgs(self, src_key: str, dst_key: str) -> list[Msg]:
+        """Return EP-AlltoAll: holder h sends owner o's (N_ESP, e_local, T) block in one message."""
         d, L = self.d, self.layout
         msgs = []
         for h in range(d.P):
-            grp = group_members(L, "ep", h)
-            for j, o in enumerate(grp):
-                if not (self.world.owns(o) or self.world.owns(h)):
+            for o in group_members(L, "ep", h):
+                if not self._owned(o, h):
                     continue
-                for i in range(d.e_local):
-                    if self.world.owns(h):
-                        bh = self.st[h].bufs["baseline"]
-                        sv = bh[src_key][i, j * bh["gs"]:(j + 1) * bh["gs"]]
-                    else:
-                        sv = None
-                    rv = self.st[o].bufs["baseline"][dst_key][L.ep_pos(h) * d.e_local + i] \
-                        if self.world.owns(o) else None
-                    msgs.append(Msg(h, o, sv, rv))
+                sv = self._buf(h, "baseline", src_key)
+                rv = self._buf(o, "baseline", dst_key)
+                msgs.append(Msg(h, o, None if sv is None else sv[L.ep_pos(o)],
+                                None if rv is None else rv[L.ep_pos(h)]))
         return msgs
 
     def _bwd_baseline(self, douts: dict) -> dict:
@@ -569,43 +637,23 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            view = K.SlotView(b["ret"], e_local=d.E, stride_i=b["gs"] * d.Mp, stride_slo=d.Mp,
-                              offset=L.esp_pos(r) * d.T * d.Mp)
-            K.combine_bwd(dout, view, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            K.combine_bwd(dout, self._ret_own_view(b, "ret", L.esp_pos(r)), rt.expert_idx, rt.slot_idx, rt.probs,
+                          b["dlogits"])
             K.dispatch_rows(dout, rt.slot_src, d.k, d.T, 0, b["dyown"], scale=rt.combine_w)
             ins[r], outs[r] = b["dyown"], b["dyg"]
         self.world.allgather("esp", ins, outs)                   # adjoint of the ESP split
-        # adjoint of the return EP-A2A: owner o sends range q of holder-h experts
-        msgs = []
-        for o in range(d.P):
-            grp = group_members(L, "ep", o)
-            for j, h in enumerate(grp):
-                if not (self.world.owns(o) or self.world.owns(h)):
-                    continue
-                for i in range(d.e_local):
-                    for q in range(d.ESP):
-                        sv = self.st[o].bufs["baseline"]["dyg"][q, j * d.e_local + i] if self.world.owns(o) else None
-                        if self.world.owns(h):
-                            bh = self.st[h].bufs["baseline"]
-                            lo = L.ep_pos(o) * bh["gs"] + q * d.T
-                            rv = bh["dyrecv"][i, lo:lo + d.T]
-                        else:
-                            rv = None
-                        msgs.append(Msg(o, h, sv, rv))
-        self.world.exchange(msgs)
+        self.world.exchange(self._ep_dispatch_msgs("dyg", "dyrecv", with_fill=False))  # adjoint of return A2A
         for r in self.ranks:                                     # AR adjoint = identity
             self._ffn_bwd(self.st[r], self.st[r].bufs["baseline"], wscale=1.0 / d.MP)
-        self.world.exchange(self._ep_msgs_ret("dr", "dd"))       # adjoint of the dispatch EP-A2A
+        self.world.exchange(self._ep_return_msgs("dr", "dd"))    # adjoint of the dispatch EP-A2A
         gins, gouts = {}, {}
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             for q in range(d.ESP):
                 rt = b["route_blk"][q]
-                view = K.SlotView(b["dd"], e_local=d.E, stride_i=b["gs"] * d.Mp, stride_slo=d.Mp,
-                                  offset=q * d.T * d.Mp)
                 own = q == L.esp_pos(r)
-                K.dispatch_bwd(view, rt.expert_idx, rt.slot_idx, b["dlogits"] if own else None,
-                               s.gate if own else None, d.E, b["dg"][q])
+                K.dispatch_bwd(self._ret_own_view(b, "dd", q), rt.expert_idx, rt.slot_idx,
+                               b["dlogits"] if own else None, s.gate if own else None, d.E, b["dg"][q])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             gins[r], gouts[r] = b["dg"], b["dx"]
         self.world.reduce_scatter("esp", gins, gouts)            # adjoint of the ESP-AllGather

@@ -58,3 +58,28 @@ for _ in range(20): torch.bmm(x, w1t.transpose(1,2))
 e1.record(); torch.cuda.synchronize()
 ms2 = e0.elapsed_time(e1) / 20
 print(f"torch.bmm same shape: {ms2*1e3:.1f} us  {fl/ms2/1e9:.1f} TFLOP/s", flush=True)
+
+# all six FFN GEMM shapes of the C2 P=1 step (8 experts, 2458 rows (+OOB tail), M=1024, H=4096), no fill skip
+E_, R_, M_, H_ = 8, 2458, 1024, 4096
+u = lambda t: t.unsqueeze(0).unsqueeze(0)
+xr = torch.randn(E_, R_, M_, device=dev).bfloat16(); w1 = torch.randn(E_, H_, M_, device=dev).bfloat16()
+w2 = torch.randn(E_, M_, H_, device=dev).bfloat16(); hh = torch.empty(E_, R_, H_, device=dev).bfloat16()
+yy = torch.empty(E_, R_, M_, device=dev).bfloat16(); dw1 = torch.empty(E_, H_, M_, device=dev)
+dw2 = torch.empty(E_, M_, H_, device=dev)
+cases = {
+    "fwd1 relu(X W1)": lambda: K.gemm_rows(u(xr), w1, K.KMAJOR, u(hh), K.EPI_RELU),
+    "fwd2 H W2":       lambda: K.gemm_rows(u(hh), w2, K.KMAJOR, u(yy), K.EPI_BF16),
+    "bwd dH (drelu)":  lambda: K.gemm_rows(u(yy), w2, K.MNMAJOR, u(hh), K.EPI_DRELU, aux=u(hh)),
+    "bwd dR":          lambda: K.gemm_rows(u(hh), w1, K.MNMAJOR, u(yy), K.EPI_BF16),
+    "wgrad dW2":       lambda: K.gemm_wgrad(u(yy), u(hh), dw2),
+    "wgrad dW1":       lambda: K.gemm_wgrad(u(hh), u(xr), dw1),
+}
+fl = 2 * E_ * R_ * M_ * H_
+for name, fn in cases.items():
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(10): fn()
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"{name:18s} {ms*1e3:8.1f} us  {fl/ms/1e9:8.1f} TFLOP/s", flush=True)
