@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 2
+#define PARM_ABI_VERSION 4
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -46,7 +46,9 @@ const char* parm_last_error(void);
 
 /* Gate, forward: logits (f64 accumulation of bf16 inputs), softmax, stable
  * top-k.  Replaces moesched.dataplane.gate (dataplane.py:86-103).
- * x: (n, M) bf16 row stride ldx; wg_t: gate weights TRANSPOSED, (E, M) bf16.
+ * x: (n, M) bf16 row stride ldx; wg_t: gate weights TRANSPOSED, (E, M) f64
+ * (the exact upcast of the bf16 weights: no per-element conversion in the
+ * f64 dot products).
  * Outputs: expert_idx (n, k) int32 in selection order, combine_w (n, k) f32
  * (= softmax score of the pick), probs (n, E) f32 (nullable). */
 int parm_gate_fwd(const void* x, long long ldx, const void* wg_t, int n, int M, int E, int k, int* expert_idx,
@@ -54,9 +56,11 @@ int parm_gate_fwd(const void* x, long long ldx, const void* wg_t, int n, int M, 
 
 /* Gate, slot pass: token-major capacity fill (dataplane.py:104-116).
  * slot_idx (n, k) int32 (-1 = dropped); slot_src (E, cap) int32 = t*k+j of
- * the pick occupying (e, slot) or -1; fill (E) = filled slots per expert. */
+ * the pick occupying (e, slot) or -1; fill (E) = filled slots per expert.
+ * workspace: parm_gate_slots_workspace(n, E) bytes (per-chunk counts). */
+size_t parm_gate_slots_workspace(int n, int E);
 int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
-                    void* stream);
+                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* Dispatch build by gather: out[e][s'] = x[t] (times scale[t*k+j] when scale
  * is non-null) for the pick in slot s = slot_lo + s', zeros when unfilled or
@@ -80,7 +84,8 @@ int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* 
                      void* stream);
 
 /* Dispatch backward: dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
- * (dlogits nullable; wg_t is (E, M)).  Adjoint of the dump + dispatch fill. */
+ * (dlogits nullable; wg_t is the (E, M) f32 upcast of the gate weights).
+ * Adjoint of the dump + dispatch fill. */
 int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
                       const void* wg_t, int n, int k, int E, int M, void* dx, long long ldx, void* stream);
 

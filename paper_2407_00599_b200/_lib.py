@@ -50,7 +50,8 @@ SIGNATURES = {
     "parm_abi_version": (_c_int, []),
     "parm_last_error": (ctypes.c_char_p, []),
     "parm_gate_fwd": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
-    "parm_gate_slots": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "parm_gate_slots_workspace": (_size, [_c_int, _c_int]),
+    "parm_gate_slots": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _size, _vp]),
     "parm_dispatch_rows": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                     _c_ll, _c_ll, _vp]),
     "parm_combine_fwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_ll,
@@ -65,7 +66,7 @@ SIGNATURES = {
     "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 4
 
 
 class ParmError(RuntimeError):

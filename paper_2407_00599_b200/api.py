@@ -106,8 +106,8 @@ def gate(tokens, gate_weights, k: int, capacity: int, token_offset: int = 0) -> 
         raise ValueError(f"top_k ({k}) exceeds number of experts ({n_experts})")
     Mp = _ceil(embed, 8)
     x = _bf16_dev(tokens, Mp)
-    wg = torch.zeros(n_experts, Mp, dtype=torch.bfloat16, device=x.device)   # transposed (E, M) on device
-    wg[:, :embed] = _bf16_dev(np.ascontiguousarray(np.asarray(gate_weights).T))
+    wg = torch.zeros(n_experts, Mp, dtype=torch.float64, device=x.device)   # transposed (E, M), f64 upcast of bf16
+    wg[:, :embed] = _bf16_dev(np.ascontiguousarray(np.asarray(gate_weights).T)).double()
     dev = x.device
     ei = torch.empty(n, k, dtype=torch.int32, device=dev)
     cw = torch.empty(n, k, dtype=torch.float32, device=dev)

@@ -19,7 +19,8 @@ void set_error(const char* fmt, ...) {
 const char* last_error() { return g_err; }
 
 int gate_fwd(const void*, long long, const void*, int, int, int, int, int*, float*, float*, cudaStream_t);
-int gate_slots(const int*, int, int, int, int, int*, int*, int*, cudaStream_t);
+size_t gate_slots_workspace(int, int);
+int gate_slots(const int*, int, int, int, int, int*, int*, int*, int*, size_t, cudaStream_t);
 size_t gate_wgrad_workspace(int, int, int);
 int gate_wgrad(const void*, long long, const float*, int, int, int, float*, size_t, float*, int, cudaStream_t);
 int dispatch_rows(const void*, long long, const int*, const float*, int, int, int, int, int, int, void*, long long,
@@ -56,9 +57,12 @@ int parm_gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, in
     return parm::gate_fwd(x, ldx, wg, n, M, E, k, expert_idx, combine_w, probs, S(stream));
 }
 
+size_t parm_gate_slots_workspace(int n, int E) { return parm::gate_slots_workspace(n, E); }
+
 int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
-                    void* stream) {
-    return parm::gate_slots(expert_idx, n, k, E, cap, slot_idx, slot_src, fill, S(stream));
+                    void* workspace, size_t workspace_bytes, void* stream) {
+    return parm::gate_slots(expert_idx, n, k, E, cap, slot_idx, slot_src, fill, reinterpret_cast<int*>(workspace),
+                            workspace_bytes, S(stream));
 }
 
 int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,

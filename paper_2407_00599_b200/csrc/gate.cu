@@ -20,7 +20,8 @@
 
 namespace parm {
 
-constexpr int kGateThreads = 256;
+constexpr int kGateThreads = 128;
+constexpr int kGateChunks = 4;   // 16-B x chunks per lane per 1024-column group
 
 // Warp-level reduce-scatter of 32 doubles: on return v[0] of lane L holds the
 // warp-wide sum of input index L.  31 double shuffles instead of 5 x 32.
@@ -38,13 +39,15 @@ __device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
     return v[0];
 }
 
-// One warp handles TPW = 32 / EMAX tokens; after the reduce-scatter lane
-// L = q * EMAX + e owns (token t0 + q, expert e): softmax max/sum over the
-// EMAX-lane group by shuffles, one exp and one divide per lane, stable rank
-// by comparing against the group's other lanes.
+// One warp handles TPW = 32 / EMAX tokens; every x load of a 1024-column group
+// of all TPW tokens is issued before the f64 FMAs (memory-level parallelism),
+// and each Wg^T vector is reused across the TPW tokens.  After the
+// reduce-scatter lane L = q * EMAX + e owns (token t0 + q, expert e): softmax
+// max/sum over the EMAX-lane group by shuffles, one exp and one divide per
+// lane, stable rank against the group's other lanes.
 template <int EMAX>
 __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __restrict__ x, long long ldx,
-                                                                 const bf16* __restrict__ wgT, int n, int M, int E,
+                                                                 const double* __restrict__ wgT, int n, int M, int E,
                                                                  int k, int* __restrict__ expert_idx,
                                                                  float* __restrict__ combine_w,
                                                                  float* __restrict__ probs) {
@@ -56,27 +59,46 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
         double v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.0;
-        for (int c = lane * 8; c < M; c += 256) {
-            float xv[TPW][8];
+        for (int g0 = 0; g0 < M; g0 += kGateChunks * 256) {
+            int4 xb[TPW][kGateChunks];
 #pragma unroll
-            for (int q = 0; q < TPW; ++q) {
-                if (t0 + q < n) {
-                    vec8_to_f32(ld_vec8(x + (long long)(t0 + q) * ldx + c), xv[q]);
-                } else {
+            for (int q = 0; q < TPW; ++q)
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) xv[q][u] = 0.0f;
+                for (int i = 0; i < kGateChunks; ++i) {
+                    const int c = g0 + lane * 8 + i * 256;
+                    xb[q][i] = (t0 + q < n && c < M)
+                                   ? __ldg(reinterpret_cast<const int4*>(x + (long long)(t0 + q) * ldx + c))
+                                   : make_int4(0, 0, 0, 0);
                 }
-            }
 #pragma unroll
-            for (int e = 0; e < EMAX; ++e) {
-                if (e < E) {
-                    float wv[8];
-                    vec8_to_f32(ld_vec8(wgT + (long long)e * M + c), wv);
+            for (int i = 0; i < kGateChunks; ++i) {
+                const int c = g0 + lane * 8 + i * 256;
+                if (c >= M) break;
+                float xv[TPW][8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const double w = (double)wv[u];
+                for (int q = 0; q < TPW; ++q) {
+                    Vec8 t8;
+                    *reinterpret_cast<int4*>(&t8) = xb[q][i];
+                    vec8_to_f32(t8, xv[q]);
+                }
 #pragma unroll
-                        for (int q = 0; q < TPW; ++q) v[q * EMAX + e] = fma((double)xv[q][u], w, v[q * EMAX + e]);
+                for (int u = 0; u < 8; u += 2) {
+                    double xd[TPW][2];
+#pragma unroll
+                    for (int q = 0; q < TPW; ++q) {
+                        xd[q][0] = (double)xv[q][u];
+                        xd[q][1] = (double)xv[q][u + 1];
+                    }
+#pragma unroll
+                    for (int e = 0; e < EMAX; ++e) {
+                        if (e < E) {   // Wg^T held as exact f64 upcasts: no per-element conversion here
+                            const double2 w = __ldg(reinterpret_cast<const double2*>(wgT + (long long)e * M + c + u));
+#pragma unroll
+                            for (int q = 0; q < TPW; ++q) {
+                                v[q * EMAX + e] = fma(xd[q][0], w.x, v[q * EMAX + e]);
+                                v[q * EMAX + e] = fma(xd[q][1], w.y, v[q * EMAX + e]);
+                            }
+                        }
                     }
                 }
             }
@@ -111,137 +133,207 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
     }
 }
 
-// Exclusive per-expert prefix count over tokens -> slots (single CTA, exact).
-// Two passes: warp w owns a contiguous token range; pass 1 counts its picks
-// per expert, a 32-entry scan per expert gives each warp its base, pass 2
-// assigns slots in token order with ballot prefixes.
-constexpr int kSlotThreads = 1024;
-constexpr int kMaxExperts = 64;
+// Exclusive per-expert prefix count over tokens -> slots, exact, in two
+// parallel passes over 256-token chunks (one CTA each):
+//   slot_count  per-chunk per-expert pick counts (+ slot_src := -1)
+//   slot_assign chunk base = sum of earlier chunks' counts, then ballot
+//               prefixes within the chunk in token order.
+constexpr int kSlotChunk = 256;
+constexpr int kSlotWarps = kSlotChunk / 32;
+
+__device__ __forceinline__ unsigned pick_mask(const int* __restrict__ expert_idx, int t, int n, int k, int (&ex)[8]) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        ex[j] = (t < n && j < k) ? __ldg(expert_idx + (long long)t * k + j) : -1;
+        if (ex[j] >= 0) m |= 1u << ex[j];
+    }
+    return m;
+}
 
 template <int EMAX>
-__global__ void __launch_bounds__(kSlotThreads) gate_slots_kernel(const int* __restrict__ expert_idx, int n, int k,
-                                                                   int E, int cap, int* __restrict__ slot_idx,
-                                                                   int* __restrict__ slot_src,
-                                                                   int* __restrict__ fill) {
-    __shared__ int warp_cnt[32][EMAX];
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int per = ((n + 32 * 32 - 1) / (32 * 32)) * 32;   // tokens per warp, multiple of 32
-    const int t_begin = warp * per;
-    const int t_end = min(n, t_begin + per);
+__global__ void __launch_bounds__(kSlotChunk) slot_count_kernel(const int* __restrict__ expert_idx, int n, int k,
+                                                                 int E, int cap, int* __restrict__ chunk_cnt,
+                                                                 int* __restrict__ slot_src) {
+    __shared__ int wc[kSlotWarps][EMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long tot = (long long)E * cap;
+    for (long long i = (long long)blockIdx.x * kSlotChunk + threadIdx.x; i < tot; i += (long long)gridDim.x * kSlotChunk)
+        slot_src[i] = -1;
+    int ex[8];
+    const unsigned m = pick_mask(expert_idx, blockIdx.x * kSlotChunk + threadIdx.x, n, k, ex);
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        const int c = __popc(__ballot_sync(0xffffffffu, (m >> e) & 1u));
+        if (lane == 0) wc[warp][e] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < kSlotWarps; ++w) s += wc[w][threadIdx.x];
+        chunk_cnt[blockIdx.x * E + threadIdx.x] = s;
+    }
+}
 
-    int cnt[EMAX];
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) cnt[e] = 0;
-    for (int base = t_begin; base < t_end; base += 32) {
-        const int t = base + lane;
-        unsigned pick = 0;  // bitmask of experts picked by token t (E <= EMAX <= 32 here)
-        if (t < t_end)
-            for (int j = 0; j < k; ++j) pick |= 1u << expert_idx[(long long)t * k + j];
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) cnt[e] += __popc(__ballot_sync(0xffffffffu, (pick >> e) & 1u));
-    }
-    if (lane == 0)
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) warp_cnt[warp][e] = cnt[e];
-    for (long long i = tid; i < (long long)E * cap; i += kSlotThreads) slot_src[i] = -1;
-    __syncthreads();
-    if (tid < E) {
-        int acc = 0;
-        for (int w = 0; w < 32; ++w) {
-            const int c = warp_cnt[w][tid];
-            warp_cnt[w][tid] = acc;
-            acc += c;
+template <int EMAX>
+__global__ void __launch_bounds__(kSlotChunk) slot_assign_kernel(const int* __restrict__ expert_idx, int n, int k,
+                                                                  int E, int cap, const int* __restrict__ chunk_cnt,
+                                                                  int* __restrict__ slot_idx,
+                                                                  int* __restrict__ slot_src, int* __restrict__ fill) {
+    __shared__ int base[EMAX];
+    __shared__ int wc[kSlotWarps][EMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x;
+    if (threadIdx.x < E) {
+        int s = 0;
+        for (int cc = 0; cc < c; ++cc) s += __ldg(chunk_cnt + cc * E + threadIdx.x);
+        base[threadIdx.x] = s;
+        if (c == gridDim.x - 1) {
+            const int total = s + __ldg(chunk_cnt + c * E + threadIdx.x);
+            fill[threadIdx.x] = total < cap ? total : cap;
         }
-        fill[tid] = acc < cap ? acc : cap;
+    }
+    const int t = c * kSlotChunk + threadIdx.x;
+    int ex[8];
+    const unsigned m = pick_mask(expert_idx, t, n, k, ex);
+    const unsigned lt = (1u << lane) - 1u;
+    int pre[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        const unsigned b = __ballot_sync(0xffffffffu, (m >> e) & 1u);
+        pre[e] = __popc(b & lt);
+        if (lane == 0) wc[warp][e] = __popc(b);
     }
     __syncthreads();
-    int run[EMAX];
+    if (threadIdx.x < E) {   // exclusive scan over warps, per expert
+        int s = base[threadIdx.x];
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) run[e] = warp_cnt[warp][e];
-    for (int base = t_begin; base < t_end; base += 32) {
-        const int t = base + lane;
-        int ex[8];
-        unsigned pick = 0;
+        for (int w = 0; w < kSlotWarps; ++w) {
+            const int v = wc[w][threadIdx.x];
+            wc[w][threadIdx.x] = s;
+            s += v;
+        }
+    }
+    __syncthreads();
+    if (t < n) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            ex[j] = (t < t_end && j < k) ? expert_idx[(long long)t * k + j] : -1;
-            if (ex[j] >= 0) pick |= 1u << ex[j];
-        }
+            if (j >= k) break;
+            const int e = ex[j];
+            int p = 0;
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-            const unsigned b = __ballot_sync(0xffffffffu, (pick >> e) & 1u);
-            if ((pick >> e) & 1u) {
-                const int slot = run[e] + __popc(b & lt_mask);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (ex[j] == e) {
-                        if (slot < cap) {
-                            slot_idx[(long long)t * k + j] = slot;
-                            slot_src[(long long)e * cap + slot] = t * k + j;
-                        } else {
-                            slot_idx[(long long)t * k + j] = -1;
-                        }
-                    }
-                }
+            for (int ee = 0; ee < EMAX; ++ee)
+                if (ee == e) p = pre[ee];
+            const int slot = wc[warp][e] + p;
+            if (slot < cap) {
+                slot_idx[(long long)t * k + j] = slot;
+                slot_src[(long long)e * cap + slot] = t * k + j;
+            } else {
+                slot_idx[(long long)t * k + j] = -1;
             }
-            run[e] += __popc(b);
         }
     }
 }
 
 // dWg^T partials: part[c][e][m] = sum_{t in chunk c} dlogits[t][e] * x[t][m].
+// 512 threads = 4 token sub-groups x 128 lanes of 8 columns; 16-B loads, four
+// tokens in flight per thread; sub-groups reduced through shared memory.
+constexpr int kWgCols = 1024;
+constexpr int kWgSub = 4;
+constexpr int kWgChunks = 64;
+
 template <int EMAX>
-__global__ void __launch_bounds__(256) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
+__global__ void __launch_bounds__(512) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
                                                                   const float* __restrict__ dlogits, int n, int M,
                                                                   int E, int chunk, float* __restrict__ part) {
-    __shared__ float dl[64][EMAX];
-    const int m = blockIdx.x * 256 + threadIdx.x;
-    const int c = blockIdx.y;
-    const int t_begin = c * chunk;
+    __shared__ float red[8][kWgCols / 8][8 + 1];     // one 8-expert block of one sub-group at a time
+    const int col_lane = threadIdx.x & 127;
+    const int sub = threadIdx.x >> 7;
+    const int c = blockIdx.x * kWgCols + col_lane * 8;
+    const int t_begin = blockIdx.y * chunk;
     const int t_end = min(n, t_begin + chunk);
-    float acc[EMAX];
+    float acc[EMAX][8];
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) acc[e] = 0.0f;
-    for (int tb = t_begin; tb < t_end; tb += 64) {
-        const int cnt = min(64, t_end - tb);
-        __syncthreads();
-        for (int i = threadIdx.x; i < 64 * EMAX; i += 256) {
-            const int tt = i / EMAX, e = i % EMAX;
-            dl[tt][e] = (tt < cnt && e < E) ? dlogits[(long long)(tb + tt) * E + e] : 0.0f;
-        }
-        __syncthreads();
-        if (m < M) {
-            for (int tt = 0; tt < cnt; ++tt) {
-                const float xv = bf2f(x[(long long)(tb + tt) * ldx + m]);
+    for (int e = 0; e < EMAX; ++e)
 #pragma unroll
-                for (int e = 0; e < EMAX; ++e) acc[e] = fmaf(xv, dl[tt][e], acc[e]);
+        for (int u = 0; u < 8; ++u) acc[e][u] = 0.0f;
+    if (c < M) {
+        for (int t = t_begin + sub; t < t_end; t += 4 * kWgSub) {
+            int4 xv[4];
+            float dl[4][EMAX];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int tt = t + q * kWgSub;
+                xv[q] = tt < t_end ? __ldg(reinterpret_cast<const int4*>(x + (long long)tt * ldx + c))
+                                   : make_int4(0, 0, 0, 0);
+#pragma unroll
+                for (int e = 0; e < EMAX; ++e) dl[q][e] = (tt < t_end && e < E) ? __ldg(dlogits + (long long)tt * E + e) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                Vec8 t8;
+                *reinterpret_cast<int4*>(&t8) = xv[q];
+                float f[8];
+                vec8_to_f32(t8, f);
+#pragma unroll
+                for (int e = 0; e < EMAX; ++e)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc[e][u] = fmaf(dl[q][e], f[u], acc[e][u]);
             }
         }
     }
-    if (m < M)
-        for (int e = 0; e < E; ++e) part[((long long)c * E + e) * M + m] = acc[e];
+    // Sub-groups fold into shared memory one after another (deterministic order), 8 experts at a time.
+#pragma unroll
+    for (int eb = 0; eb < EMAX; eb += 8) {
+        for (int g = 0; g < kWgSub; ++g) {
+            if (sub == g) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        red[e][col_lane][u] = (g == 0 ? 0.0f : red[e][col_lane][u]) + acc[eb + e][u];
+            }
+            __syncthreads();
+        }
+        if (sub == 0 && c < M) {
+            for (int e = 0; e < 8 && eb + e < E; ++e) {
+                float* dst = part + ((long long)blockIdx.y * E + eb + e) * M + c;
+                reinterpret_cast<float4*>(dst)[0] =
+                    make_float4(red[e][col_lane][0], red[e][col_lane][1], red[e][col_lane][2], red[e][col_lane][3]);
+                reinterpret_cast<float4*>(dst)[1] =
+                    make_float4(red[e][col_lane][4], red[e][col_lane][5], red[e][col_lane][6], red[e][col_lane][7]);
+            }
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void sum_partials_kernel(const float* __restrict__ part, int chunks, long long len, float* __restrict__ out,
                                     int accumulate) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
-        float s = accumulate ? out[i] : 0.0f;
-        for (int c = 0; c < chunks; ++c) s += part[(long long)c * len + i];
-        out[i] = s;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int c = 0;
+        for (; c + 4 <= chunks; c += 4) {
+            s0 += __ldg(part + (long long)c * len + i);
+            s1 += __ldg(part + (long long)(c + 1) * len + i);
+            s2 += __ldg(part + (long long)(c + 2) * len + i);
+            s3 += __ldg(part + (long long)(c + 3) * len + i);
+        }
+        for (; c < chunks; ++c) s0 += __ldg(part + (long long)c * len + i);
+        const float s = (s0 + s1) + (s2 + s3);
+        out[i] = accumulate ? out[i] + s : s;
     }
 }
 
 // ------------------------------------------------------------------ host
 template <int EMAX>
-static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wgT, int n, int M, int E, int k, int* ei,
+static void launch_gate_fwd(const bf16* x, long long ldx, const double* wgT, int n, int M, int E, int k, int* ei,
                             float* cw, float* probs, cudaStream_t s) {
     constexpr int TPW = 32 / EMAX;
     const int warps_needed = (n + TPW - 1) / TPW;
     int blocks = (warps_needed * 32 + kGateThreads - 1) / kGateThreads;
-    const int max_blocks = kNumSMs * 8;
+    const int max_blocks = kNumSMs * 16;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     gate_fwd_kernel<EMAX><<<blocks, kGateThreads, 0, s>>>(x, ldx, wgT, n, M, E, k, ei, cw, probs);
@@ -254,7 +346,7 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "gate: embed (%d) and row stride must be multiples of 8", M);
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
-    auto W = reinterpret_cast<const bf16*>(wgT);
+    auto W = reinterpret_cast<const double*>(wgT);
     if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 4)
@@ -269,43 +361,50 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     return 0;
 }
 
+size_t gate_slots_workspace(int n, int E) {
+    return (size_t)((n + kSlotChunk - 1) / kSlotChunk) * E * sizeof(int);
+}
+
 int gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
-               cudaStream_t s) {
+               int* ws, size_t ws_bytes, cudaStream_t s) {
     PARM_CHECK_ARG(k >= 1 && k <= 8, "gate_slots: top_k must be in [1, 8] (got %d)", k);
     PARM_CHECK_ARG(E >= 1 && E <= 32, "gate_slots: experts must be in [1, 32]");
     PARM_CHECK_ARG(cap >= 1, "gate_slots: capacity must be >= 1");
-    if (E <= 8)
-        gate_slots_kernel<8><<<1, kSlotThreads, 0, s>>>(expert_idx, n, k, E, cap, slot_idx, slot_src, fill);
-    else
-        gate_slots_kernel<32><<<1, kSlotThreads, 0, s>>>(expert_idx, n, k, E, cap, slot_idx, slot_src, fill);
+    PARM_CHECK_ARG(ws_bytes >= gate_slots_workspace(n, E), "gate_slots: workspace too small");
+    const int chunks = n > 0 ? (n + kSlotChunk - 1) / kSlotChunk : 1;
+    if (E <= 8) {
+        slot_count_kernel<8><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_src);
+        slot_assign_kernel<8><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
+    } else {
+        slot_count_kernel<32><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_src);
+        slot_assign_kernel<32><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
+    }
     PARM_CHECK_LAUNCH("gate_slots");
     return 0;
 }
 
 size_t gate_wgrad_workspace(int n, int M, int E) {
-    const int chunks = n < 64 ? 1 : (n / 64 < 128 ? n / 64 : 128);
-    return (size_t)chunks * M * E * sizeof(float);
+    return (size_t)kWgChunks * M * E * sizeof(float);
 }
 
 int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, float* ws, size_t ws_bytes,
                float* dwgT, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(E <= 32, "gate_wgrad: at most 32 experts supported");
-    const int chunks = n < 64 ? 1 : (n / 64 < 128 ? n / 64 : 128);
-    PARM_CHECK_ARG(ws_bytes >= (size_t)chunks * M * E * sizeof(float), "gate_wgrad: workspace too small");
-    const int chunk = (n + chunks - 1) / chunks;
-    dim3 grid((M + 255) / 256, chunks);
+    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "gate_wgrad: embed must be a multiple of 8");
+    PARM_CHECK_ARG(ws_bytes >= gate_wgrad_workspace(n, M, E), "gate_wgrad: workspace too small");
+    const int chunk = (n + kWgChunks - 1) / kWgChunks;
+    dim3 grid((M + kWgCols - 1) / kWgCols, kWgChunks);
     auto X = reinterpret_cast<const bf16*>(x);
     if (E <= 8)
-        gate_wgrad_partial_kernel<8><<<grid, 256, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<8><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     else if (E <= 16)
-        gate_wgrad_partial_kernel<16><<<grid, 256, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<16><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     else
-        gate_wgrad_partial_kernel<32><<<grid, 256, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<32><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     PARM_CHECK_LAUNCH("gate_wgrad_partial");
     const long long len = (long long)M * E;
     int blocks = (int)((len + 255) / 256);
-    if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
-    sum_partials_kernel<<<blocks, 256, 0, s>>>(ws, chunks, len, dwgT, accumulate);
+    sum_partials_kernel<<<blocks, 256, 0, s>>>(ws, kWgChunks, len, dwgT, accumulate);
     PARM_CHECK_LAUNCH("gate_wgrad_sum");
     return 0;
 }

@@ -53,6 +53,7 @@ struct Params {
     long long x_ld, x_g, x_lo, x_hi;
     const int* fill;           // [hi][lo][g] valid rows, or null
     int pairs;                 // CTA-pair kernel: max 256-row pair tiles per group
+    int debug;                 // PARM_GEMM_DEBUG bits (perf experiments only): 1 = no epilogue stores, 2 = no TMA
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -250,7 +251,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long
 #pragma unroll
             for (int v = 0; v < 32; ++v) r[v] = 0u;
         }
-        if (!row_ok) continue;
+        if (!row_ok || (p.debug & 1)) continue;
         const int col = n0 + c * 32;
         if (EPI == kEpiF32 || EPI == kEpiF32Acc) {
             float* dst = reinterpret_cast<float*>(p.D) + drow + col;
@@ -614,20 +615,140 @@ __device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfil
     return t;
 }
 
+// ---------------------------------------------------------------- TMA-store epilogue (pair kernel)
+// Each epilogue warp owns 32 accumulator rows.  Per 128-byte output chunk of
+// its rows (64 bf16 / 32 f32 columns) it drains TMEM, applies the fused op,
+// writes the chunk into a 128B-swizzled 4 KB staging buffer (conflict-free:
+// 8 consecutive rows cover all banks) and issues one bulk-tensor store; two
+// buffers per warp alternate so the store of chunk i overlaps chunk i+1.
+// Rows past the segment (or a dummy half-tile) are clipped by the TMA unit.
+constexpr int kEpiStageBytes = 32 * 128;
+
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int KIND, int EPI>
+__device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMap* tmap_d, uint32_t taddr, int lane,
+                                               int row0, int g, int lo, int hi, int n0, bool row_ok, long long xrow,
+                                               bool empty, uint8_t* stage, int& buf) {
+    constexpr bool F32 = (EPI == kEpiF32 || EPI == kEpiF32Acc);
+    constexpr int COLS = F32 ? 32 : 64;          // output columns per 128-byte chunk
+    constexpr int NCH = BN / COLS;
+    int4 ax_next[8];
+    if (EPI == kEpiDReluBF16 && row_ok) {
+        const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) ax_next[v] = __ldg(src + v);
+    }
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+        uint32_t pk[32];   // F32: 32 fp32 words; BF16: 32 packed bf16x2 words (64 columns)
+        if (F32) {
+            PARM_TMEM_LD32(taddr + ch * 32, pk);
+            tmem_ld_wait();
+#pragma unroll
+            for (int v = 0; v < 32; ++v)
+                pk[v] = empty ? 0u : __float_as_uint(p.alpha * __uint_as_float(pk[v]));
+        } else {
+            int4 ax_cur[8];
+            if (EPI == kEpiDReluBF16) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) ax_cur[v] = ax_next[v];
+                if (row_ok && ch + 1 < NCH) {
+                    const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0 + (ch + 1) * COLS);
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) ax_next[v] = __ldg(src + v);
+                }
+            }
+            uint32_t r0[32], r1[32];
+            PARM_TMEM_LD32(taddr + ch * 64, r0);
+            PARM_TMEM_LD32(taddr + ch * 64 + 32, r1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int v = 0; v < 32; ++v) {
+                float a = p.alpha * __uint_as_float(v < 16 ? r0[2 * v] : r1[2 * v - 32]);
+                float b = p.alpha * __uint_as_float(v < 16 ? r0[2 * v + 1] : r1[2 * v - 31]);
+                if (EPI == kEpiReluBF16) {
+                    a = fmaxf(a, 0.0f);
+                    b = fmaxf(b, 0.0f);
+                }
+                if (EPI == kEpiDReluBF16) {
+                    const uint32_t m = reinterpret_cast<const uint32_t*>(ax_cur)[v];   // bf16 pair of aux
+                    const float ma = __uint_as_float(m << 16), mb = __uint_as_float(m & 0xFFFF0000u);
+                    a = ma > 0.0f ? a : 0.0f;
+                    b = mb > 0.0f ? b : 0.0f;
+                }
+                pk[v] = pack_bf16x2(a, b);
+            }
+        }
+        uint8_t* sbuf = stage + buf * kEpiStageBytes;
+        if (lane == 0) bulk_wait_read1();       // the store that last used this buffer has read it
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            const int col = n0 + ch * COLS;
+            if (KIND == kRow)
+                tma_store_5d(tmap_d, sbuf, col, row0, g, lo, hi);
+            else if (EPI == kEpiF32Acc)
+                tma_reduce_add_3d(tmap_d, sbuf, col, row0, g);
+            else
+                tma_store_3d(tmap_d, sbuf, col, row0, g);
+            bulk_commit();
+        }
+        buf ^= 1;
+    }
+}
+
 template <int BN, int KIND, int MB, int EPI>
 struct CfgPair {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = (BN / 2) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (kSmemBudget - 1024) / kStageBytes > 8 ? 8 : (kSmemBudget - 1024) / kStageBytes;
+    static constexpr int kEpiBytes = 4 * 2 * kEpiStageBytes;      // 4 epilogue warps x 2 staging buffers
+    static constexpr int kStages = (kSmemBudget - kEpiBytes) / kStageBytes > 8 ? 8
+                                                                               : (kSmemBudget - kEpiBytes) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + kMaxFill * 4;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256 + kMaxFill * 4;
 };
 
 template <int BN, int KIND, int MB, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                         const Params p) {
+                         const __grid_constant__ CUtensorMap tmap_d, const Params p) {
     using C = CfgPair<BN, KIND, MB, EPI>;
     constexpr int STAGES = C::kStages;
     constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
@@ -643,6 +764,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + 256);
+    uint8_t* smem_epi = smem + STAGES * C::kStageBytes + 256 + kMaxFill * 4;   // 1024-aligned staging
+    smem_epi = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_epi) + 1023) & ~uintptr_t(1023));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -656,6 +779,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
+        prefetch_tmap(&tmap_d);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 2);      // leader expect_tx arrival + peer arrival
             mbar_init(&empty_bar[s], 1);     // leader's multicast commit
@@ -689,10 +813,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     int hi = 0, lo = 0, r0 = 0;
                     if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
                     mbar_wait(&empty_bar[stage], phase ^ 1);
+                    const bool no_tma = (p.debug & 2) != 0;
                     if (leader)
-                        mbar_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
+                        mbar_expect_tx(&full_bar[stage], no_tma ? 0u : 2u * C::kStageBytes);
                     else
                         mbar_arrive_remote(&full_bar[stage], 0);
+                    if (no_tma) {
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
                     const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
@@ -771,6 +903,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ---------------------------------------------------- epilogue (both CTAs, own TMEM rows)
         const int ew = warp & 3;
         int it_tile = 0;
+        int ebuf = 0;
+        uint8_t* my_stage = smem_epi + ew * 2 * kEpiStageBytes;
         for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
             const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
             if (!t.live) continue;
@@ -797,13 +931,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
-            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
+            (void)drow;
+            if (p.debug & 1) {
+                drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
+            } else {
+                drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
+                                              xrow, empty, my_stage, ebuf);
+            }
             tc_fence_before();
             if (leader)
                 mbar_arrive(&tempty_bar[as]);
             else
                 mbar_arrive_remote(&tempty_bar[as], 0);
         }
+        if (lane == 0) bulk_wait_all();
     }
 
     tc_fence_before();
@@ -832,7 +973,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // bf16 tensor map with 128B swizzle; dims[0] is contiguous; strides in elements for dims 1..rank-1.
 static int make_tmap(CUtensorMap* map, const void* base, int rank, const long long* dims, const long long* strides,
-                     int box1) {
+                     int box1, int esize = 2, int box0 = 64) {
     auto enc = get_encode();
     PARM_CHECK_ARG(enc != nullptr, "gemm: cuTensorMapEncodeTiled unavailable from the driver");
     PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(base) & 15) == 0, "gemm: operand base not 16-byte aligned");
@@ -842,15 +983,16 @@ static int make_tmap(CUtensorMap* map, const void* base, int rank, const long lo
     cuuint32_t es[5];
     for (int i = 0; i < rank; ++i) {
         gd[i] = (cuuint64_t)(dims[i] > 0 ? dims[i] : 1);
-        box[i] = i == 0 ? 64u : (i == 1 ? (cuuint32_t)box1 : 1u);
+        box[i] = i == 0 ? (cuuint32_t)box0 : (i == 1 ? (cuuint32_t)box1 : 1u);
         es[i] = 1;
     }
     for (int i = 0; i + 1 < rank; ++i) {
         long long s = strides[i] > 0 ? strides[i] : 8;
-        PARM_CHECK_ARG((s * 2) % 16 == 0, "gemm: stride %lld (dim %d) not a 16-byte multiple", strides[i], i + 1);
-        gs[i] = (cuuint64_t)(s * 2);
+        PARM_CHECK_ARG((s * esize) % 16 == 0, "gemm: stride %lld (dim %d) not a 16-byte multiple", strides[i], i + 1);
+        gs[i] = (cuuint64_t)(s * esize);
     }
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, box, es,
+    CUresult r = enc(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                     const_cast<void*>(base), gd, gs, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     PARM_CHECK_ARG(r == CUDA_SUCCESS, "gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -874,7 +1016,8 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
 }
 
 template <int BN, int KIND, int MB, int EPI>
-static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t stream) {
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const Params& p,
+                       cudaStream_t stream) {
     using C = CfgPair<BN, KIND, MB, EPI>;
     auto kern = moe_gemm_pair_kernel<BN, KIND, MB, EPI>;
     static bool attr_set = false;
@@ -884,17 +1027,17 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Param
     }
     int grid = 2 * (p.num_tiles < kNumSMs / 2 ? p.num_tiles : kNumSMs / 2);   // clusters of 2 CTAs
     if (grid < 2) grid = 2;
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, td, p);
     PARM_CHECK_LAUNCH("moe_gemm_pair");
     return 0;
 }
 
 template <int KIND, int MB, int EPI>
-static int dispatch_bn(bool pair, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                       cudaStream_t s) {
+static int dispatch_bn(bool pair, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+                       const Params& p, cudaStream_t s) {
     if (pair) {
-        if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, p, s);
-        return launch_pair<128, KIND, MB, EPI>(ta, tb, p, s);
+        if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, td, p, s);
+        return launch_pair<128, KIND, MB, EPI>(ta, tb, td, p, s);
     }
     if (bn == 256) return launch<256, KIND, MB, EPI>(ta, tb, p, s);
     if (bn == 128) return launch<128, KIND, MB, EPI>(ta, tb, p, s);
@@ -931,6 +1074,14 @@ int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
     p.K = q.K;
     p.alpha = q.alpha;
     p.fill = q.fill;
+    {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char* e = getenv("PARM_GEMM_DEBUG");
+            dbg = e ? atoi(e) : 0;
+        }
+        p.debug = dbg;
+    }
     p.D = const_cast<void*>(q.d.ptr);
     p.d_ld = q.d.ld;
     p.d_g = q.d.g_stride;
@@ -944,8 +1095,17 @@ int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
     const int bn = (q.N % 256 == 0) ? 256 : (q.N % 128 == 0 ? 128 : 64);
     const bool pair = pair_mode() && bn >= 128;
     p.n_blocks = q.N / bn;
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, td;
     int rc;
+    if (q.kind == kRow) {   // D: bf16 [hi][lo][g][r][n] -> dims (N, L, G, nlo, nhi), 32-row x 128 B store boxes
+        const long long dd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
+        const long long ds[4] = {q.d.ld, q.d.g_stride, q.d.lo_stride, q.d.hi_stride};
+        if ((rc = make_tmap(&td, q.d.ptr, 5, dd, ds, 32, 2, 64))) return rc;
+    } else {                // D: f32 [g][m][n] -> dims (N, M, G)
+        const long long dd[3] = {q.N, q.M, q.groups};
+        const long long ds[2] = {q.d.ld, q.d.g_stride};
+        if ((rc = make_tmap(&td, q.d.ptr, 3, dd, ds, 32, 4, 32))) return rc;
+    }
     if (q.kind == kRow) {
         PARM_CHECK_ARG(q.K > 0 && q.K % BK == 0, "gemm: K=%d must be a positive multiple of %d", q.K, BK);
         PARM_CHECK_ARG(q.epi <= kEpiDReluBF16, "gemm: row GEMMs produce bf16");
@@ -969,11 +1129,11 @@ int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
         if (rc) return rc;
         const int combo = q.b_major;
         if (combo == kKMajor) {
-            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(pair, bn, ta, tb, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(pair, bn, ta, tb, p, stream);
+            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
         } else {
-            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(pair, bn, ta, tb, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(pair, bn, ta, tb, p, stream);
+            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
         }
     } else {
         PARM_CHECK_ARG(q.M > 0 && q.M % BM == 0, "gemm: M=%d must be a positive multiple of %d", q.M, BM);
@@ -988,8 +1148,8 @@ int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
         const long long bd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
         const long long bs[4] = {q.b.ld, q.b.g_stride, q.b.lo_stride, q.b.hi_stride};
         if ((rc = make_tmap(&tb, q.b.ptr, 5, bd, bs, BK))) return rc;
-        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(pair, bn, ta, tb, p, stream);
-        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(pair, bn, ta, tb, p, stream);
+        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(pair, bn, ta, tb, td, p, stream);
+        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(pair, bn, ta, tb, td, p, stream);
     }
     set_error("gemm: unsupported combination kind=%d b_major=%d epi=%d", q.kind, q.b_major, q.epi);
     return 1;

@@ -14,220 +14,323 @@
 //   dispatch_bwd    dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
 //   esp_sum         S2: out[e, s] = sum_p Y_p[e, s] before the MP AllGather.
 //
-// All rows move as 16-byte vectors, one warp per row/token; accumulation f32.
+// All are HBM-streaming gathers: one warp per token/row, 16-byte vectors, and
+// every row load of a 1024-column group is issued before any is consumed
+// (KT picks x 4 chunks in flight per lane) — the memory-level parallelism
+// these kernels live on.  Accumulation is f32.
 #include "common.cuh"
 
 namespace parm {
 
 constexpr int kRowThreads = 256;
+constexpr int kChunks = 4;                  // 16-B chunks per lane per column group (1024 columns / warp)
+constexpr int kGroupCols = kChunks * 256;
 
 static int row_grid(long long rows) {
-    long long warps = rows;
-    long long blocks = (warps * 32 + kRowThreads - 1) / kRowThreads;
+    long long blocks = (rows * 32 + kRowThreads - 1) / kRowThreads;
     const long long cap = (long long)kNumSMs * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return (int)blocks;
 }
 
+__device__ __forceinline__ int4 ldg16(const bf16* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
+
+// ------------------------------------------------------------------ dispatch (gather into slots)
+// Four rows per warp iteration: their slot_src entries, then their token rows,
+// are loaded together.
 __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
     const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
     int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
     long long out_stride_s) {
+    constexpr int R = 4;
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     const long long rows = (long long)E * slots_out;
-    for (long long r = warp_global; r < rows; r += num_warps) {
-        const int e = (int)(r / slots_out);
-        const int sp = (int)(r - (long long)e * slots_out);
-        const int s = slot_lo + sp;
-        const int src = (s < cap) ? slot_src[(long long)e * cap + s] : -1;
-        bf16* dst = out + (long long)e * out_stride_e + (long long)sp * out_stride_s;
-        if (src < 0) {
-            const int4 z = make_int4(0, 0, 0, 0);
-            for (int c = lane * 8; c < M; c += 256) *reinterpret_cast<int4*>(dst + c) = z;
-        } else {
-            const int t = src / k;
-            const bf16* xr = x + (long long)t * ldx;
-            if (scale == nullptr) {
-                for (int c = lane * 8; c < M; c += 256)
-                    *reinterpret_cast<int4*>(dst + c) = __ldg(reinterpret_cast<const int4*>(xr + c));
-            } else {
-                const float w = scale[src];
-                for (int c = lane * 8; c < M; c += 256) {
-                    float f[8];
-                    vec8_to_f32(ld_vec8(xr + c), f);
+    for (long long r0 = warp_global * R; r0 < rows; r0 += num_warps * R) {
+        int src[R];
+        bf16* dst[R];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) f[u] *= w;
-                    st_vec8(dst + c, f32_to_vec8(f));
+        for (int q = 0; q < R; ++q) {
+            const long long r = r0 + q;
+            src[q] = -2;
+            if (r < rows) {
+                const int e = (int)(r / slots_out);
+                const int sp = (int)(r - (long long)e * slots_out);
+                const int s = slot_lo + sp;
+                src[q] = (s < cap) ? __ldg(slot_src + (long long)e * cap + s) : -1;
+                dst[q] = out + (long long)e * out_stride_e + (long long)sp * out_stride_s;
+            }
+        }
+        float w[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) w[q] = (scale != nullptr && src[q] >= 0) ? __ldg(scale + src[q]) : 1.0f;
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            int4 v[R][kChunks];
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int i = 0; i < kChunks; ++i) {
+                    const int c = g0 + lane * 8 + i * 256;
+                    v[q][i] = make_int4(0, 0, 0, 0);
+                    if (src[q] >= 0 && c < M) v[q][i] = ldg16(x + (long long)(src[q] / k) * ldx + c);
+                }
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                if (src[q] == -2) continue;
+#pragma unroll
+                for (int i = 0; i < kChunks; ++i) {
+                    const int c = g0 + lane * 8 + i * 256;
+                    if (c >= M) continue;
+                    if (scale != nullptr && src[q] >= 0) {
+                        Vec8 t;
+                        *reinterpret_cast<int4*>(&t) = v[q][i];
+                        float f[8];
+                        vec8_to_f32(t, f);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) f[u] *= w[q];
+                        st_vec8(dst[q] + c, f32_to_vec8(f));
+                    } else {
+                        *reinterpret_cast<int4*>(dst[q] + c) = v[q][i];
+                    }
                 }
             }
         }
     }
 }
 
-// Sum of the n_p partial rows of (e, s) into f (8 floats at column c).
-__device__ __forceinline__ void gather_slot(const SlotView& v, int e, int s, int c, float* f) {
+// ------------------------------------------------------------------ token-side gathers
+// Routing of one token's picks (lane-uniform).
+template <int KT>
+struct Picks {
+    int sl[KT];
+    int ex[KT];
+    float w[KT];
+    __device__ __forceinline__ void load(long long t, int k, const int* __restrict__ slot_idx,
+                                         const int* __restrict__ expert_idx, const float* __restrict__ cw) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) f[u] = 0.0f;
-    for (int p = 0; p < v.n_p; ++p) {
-        float g[8];
-        vec8_to_f32(ld_vec8(v.ptr + slot_offset(v, e, s, p) + c), g);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] += g[u];
-    }
-}
-
-__global__ void __launch_bounds__(kRowThreads) combine_fwd_kernel(const SlotView y, const int* __restrict__ expert_idx,
-                                                                   const int* __restrict__ slot_idx,
-                                                                   const float* __restrict__ combine_w, int n, int k,
-                                                                   int M, bf16* __restrict__ out, long long ldo) {
-    const int lane = threadIdx.x & 31;
-    const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
-    const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
-    for (long long t = warp_global; t < n; t += num_warps) {
-        // Routing of all k picks first, so the row loads below are independent.
-        int sl[8], ex[8];
-        float wt[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
-            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
-            wt[j] = (sl[j] >= 0) ? combine_w[t * k + j] : 0.0f;
+        for (int j = 0; j < KT; ++j) {
+            sl[j] = (j < k) ? __ldg(slot_idx + t * k + j) : -1;
+            ex[j] = (sl[j] >= 0) ? __ldg(expert_idx + t * k + j) : 0;
+            w[j] = (cw != nullptr && sl[j] >= 0) ? __ldg(cw + t * k + j) : 0.0f;
         }
-        for (int c = lane * 8; c < M; c += 256) {
-            float acc[8];
+    }
+};
+
+// Loads of one partial p of every pick for one 1024-column group, all in flight together.
+template <int KT>
+__device__ __forceinline__ void load_picks(const SlotView& v, const Picks<KT>& pk, int p, int g0, int lane, int M,
+                                           int4 (&buf)[KT][kChunks]) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
+    for (int j = 0; j < KT; ++j) {
+        const bf16* row = v.ptr + (pk.sl[j] >= 0 ? slot_offset(v, pk.ex[j], pk.sl[j], p) : 0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (sl[j] < 0) continue;
-                float f[8];
-                gather_slot(y, ex[j], sl[j], c, f);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc[u] = fmaf(wt[j], f[u], acc[u]);
-            }
-            st_vec8(out + t * ldo + c, f32_to_vec8(acc));
+        for (int i = 0; i < kChunks; ++i) {
+            const int c = g0 + lane * 8 + i * 256;
+            buf[j][i] = (pk.sl[j] >= 0 && c < M) ? ldg16(row + c) : make_int4(0, 0, 0, 0);
         }
     }
 }
 
-template <int EMAX>
-__global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(const bf16* __restrict__ dout, long long ldd,
-                                                                   const SlotView y, const int* __restrict__ expert_idx,
-                                                                   const int* __restrict__ slot_idx,
-                                                                   const float* __restrict__ probs, int n, int k, int E,
-                                                                   int M, float* __restrict__ dlogits) {
+__device__ __forceinline__ void fma_bf16x8(float* acc, float w, const int4& v) {
+    Vec8 t;
+    *reinterpret_cast<int4*>(&t) = v;
+    float f[8];
+    vec8_to_f32(t, f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = fmaf(w, f[u], acc[u]);
+}
+
+// 256 threads, <= 85 registers: three CTAs (24 warps) per SM keep enough row
+// loads in flight; the per-group accumulators are the only long-lived state.
+template <int KT>
+__global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_kernel(const SlotView y, const int* __restrict__ expert_idx,
+                                                                      const int* __restrict__ slot_idx,
+                                                                      const float* __restrict__ combine_w, int n, int k,
+                                                                      int M, bf16* __restrict__ out, long long ldo) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
-        float dw[8];
-        int sl[8], ex[8];
+        Picks<KT> pk;
+        pk.load(t, k, slot_idx, expert_idx, combine_w);
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            float acc[kChunks][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            dw[j] = 0.0f;
-            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
-            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
+            for (int i = 0; i < kChunks; ++i)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[i][u] = 0.0f;
+            for (int p = 0; p < y.n_p; ++p) {
+                int4 buf[KT][kChunks];
+                load_picks<KT>(y, pk, p, g0, lane, M, buf);
+#pragma unroll
+                for (int j = 0; j < KT; ++j)       // j ascending, like the reference's _combine
+#pragma unroll
+                    for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], pk.w[j], buf[j][i]);
+            }
+#pragma unroll
+            for (int i = 0; i < kChunks; ++i) {
+                const int c = g0 + lane * 8 + i * 256;
+                if (c < M) st_vec8(out + t * ldo + c, f32_to_vec8(acc[i]));
+            }
         }
-        for (int c = lane * 8; c < M; c += 256) {
-            float g[8];
-            vec8_to_f32(ld_vec8(dout + t * ldd + c), g);
+    }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16* __restrict__ dout, long long ldd,
+                                                                      const SlotView y, const int* __restrict__ expert_idx,
+                                                                      const int* __restrict__ slot_idx,
+                                                                      const float* __restrict__ probs, int n, int k,
+                                                                      int E, int M, float* __restrict__ dlogits) {
+    const int lane = threadIdx.x & 31;
+    const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
+    const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
+    for (long long t = warp_global; t < n; t += num_warps) {
+        Picks<KT> pk;
+        pk.load(t, k, slot_idx, expert_idx, nullptr);
+        float dw[KT];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (sl[j] < 0) continue;
-                float f[8];
-                gather_slot(y, ex[j], sl[j], c, f);
+        for (int j = 0; j < KT; ++j) dw[j] = 0.0f;
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            int4 gv[kChunks];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) dw[j] = fmaf(g[u], f[u], dw[j]);
+            for (int i = 0; i < kChunks; ++i) {
+                const int c = g0 + lane * 8 + i * 256;
+                gv[i] = c < M ? ldg16(dout + t * ldd + c) : make_int4(0, 0, 0, 0);
+            }
+            for (int p = 0; p < y.n_p; ++p) {     // <dOut, sum_p Y_p> = sum_p <dOut, Y_p>
+                int4 buf[KT][kChunks];
+                load_picks<KT>(y, pk, p, g0, lane, M, buf);
+#pragma unroll
+                for (int i = 0; i < kChunks; ++i) {
+                    Vec8 g8;
+                    *reinterpret_cast<int4*>(&g8) = gv[i];
+                    float g[8];
+                    vec8_to_f32(g8, g);
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) {
+                        Vec8 y8;
+                        *reinterpret_cast<int4*>(&y8) = buf[j][i];
+                        float f[8];
+                        vec8_to_f32(y8, f);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) dw[j] = fmaf(g[u], f[u], dw[j]);
+                    }
+                }
             }
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < KT; ++j)
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) dw[j] += __shfl_xor_sync(0xffffffffu, dw[j], off);
         // Softmax adjoint: dl_e = p_e * (dS_e - sum_e' p_e' dS_e'), dS nonzero on kept picks.
         if (lane < E) {
-            const float pe = probs[t * E + lane];
+            const float pe = __ldg(probs + t * E + lane);
             float dse = 0.0f, dot = 0.0f;
-            for (int j = 0; j < k; ++j) {
-                if (slot_idx[t * k + j] < 0) continue;
-                const int e = expert_idx[t * k + j];
-                float dj = 0.0f;
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    if (jj == j) dj = dw[jj];
-                dot += probs[t * E + e] * dj;
-                if (e == lane) dse = dj;
+            for (int j = 0; j < KT; ++j) {
+                if (pk.sl[j] < 0) continue;
+                dot += __ldg(probs + t * E + pk.ex[j]) * dw[j];
+                if (pk.ex[j] == lane) dse = dw[j];
             }
             dlogits[t * E + lane] = pe * (dse - dot);
         }
     }
 }
 
-template <int EMAX>
-__global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(const SlotView dr, const int* __restrict__ expert_idx,
-                                                                    const int* __restrict__ slot_idx,
-                                                                    const float* __restrict__ dlogits,
-                                                                    const bf16* __restrict__ wgT, int n, int k, int E,
-                                                                    int M, bf16* __restrict__ dx, long long ldx) {
+template <int KT, int EMAX>
+__global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_kernel(const SlotView dr,
+                                                                       const int* __restrict__ expert_idx,
+                                                                       const int* __restrict__ slot_idx,
+                                                                       const float* __restrict__ dlogits,
+                                                                       const float* __restrict__ wgT, int n, int k,
+                                                                       int E, int M, bf16* __restrict__ dx,
+                                                                       long long ldx) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
-        int sl[8], ex[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            sl[j] = (j < k) ? slot_idx[t * k + j] : -1;
-            ex[j] = (sl[j] >= 0) ? expert_idx[t * k + j] : 0;
-        }
+        Picks<KT> pk;
+        pk.load(t, k, slot_idx, expert_idx, nullptr);
         float dl[EMAX];
-        if (dlogits) {
 #pragma unroll
-            for (int e = 0; e < EMAX; ++e) dl[e] = (e < E) ? dlogits[t * E + e] : 0.0f;
-        }
-        for (int c = lane * 8; c < M; c += 256) {
-            float acc[8];
+        for (int e = 0; e < EMAX; ++e) dl[e] = (dlogits != nullptr && e < E) ? __ldg(dlogits + t * E + e) : 0.0f;
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            float acc[kChunks][8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
+            for (int i = 0; i < kChunks; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (sl[j] < 0) continue;
-                float f[8];
-                gather_slot(dr, ex[j], sl[j], c, f);
+                for (int u = 0; u < 8; ++u) acc[i][u] = 0.0f;
+            for (int p = 0; p < dr.n_p; ++p) {
+                int4 buf[KT][kChunks];
+                load_picks<KT>(dr, pk, p, g0, lane, M, buf);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) acc[u] += f[u];
+                for (int j = 0; j < KT; ++j)
+#pragma unroll
+                    for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], 1.0f, buf[j][i]);
             }
-            if (dlogits) {   // + dlogits[t] . Wg^T with Wg stored transposed (E, M)
+            if (dlogits != nullptr) {   // + dlogits[t] . Wg^T (f32 copy of the transposed gate weights)
 #pragma unroll
                 for (int e = 0; e < EMAX; ++e) {
                     if (e < E) {
-                        float w[8];
-                        vec8_to_f32(ld_vec8(wgT + (long long)e * M + c), w);
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) acc[u] = fmaf(dl[e], w[u], acc[u]);
+                        for (int i = 0; i < kChunks; ++i) {
+                            const int c = g0 + lane * 8 + i * 256;
+                            if (c < M) {
+                                const float4* wp = reinterpret_cast<const float4*>(wgT + (long long)e * M + c);
+                                const float4 w0 = __ldg(wp), w1 = __ldg(wp + 1);
+                                acc[i][0] = fmaf(dl[e], w0.x, acc[i][0]);
+                                acc[i][1] = fmaf(dl[e], w0.y, acc[i][1]);
+                                acc[i][2] = fmaf(dl[e], w0.z, acc[i][2]);
+                                acc[i][3] = fmaf(dl[e], w0.w, acc[i][3]);
+                                acc[i][4] = fmaf(dl[e], w1.x, acc[i][4]);
+                                acc[i][5] = fmaf(dl[e], w1.y, acc[i][5]);
+                                acc[i][6] = fmaf(dl[e], w1.z, acc[i][6]);
+                                acc[i][7] = fmaf(dl[e], w1.w, acc[i][7]);
+                            }
+                        }
                     }
                 }
             }
-            st_vec8(dx + t * ldx + c, f32_to_vec8(acc));
+#pragma unroll
+            for (int i = 0; i < kChunks; ++i) {
+                const int c = g0 + lane * 8 + i * 256;
+                if (c < M) st_vec8(dx + t * ldx + c, f32_to_vec8(acc[i]));
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(kRowThreads) esp_sum_kernel(const SlotView y, int E, int slots, int M,
-                                                               bf16* __restrict__ out) {
+__global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const SlotView y, int E, int slots, int M,
+                                                                  bf16* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     const long long rows = (long long)E * slots;
     for (long long r = warp_global; r < rows; r += num_warps) {
-        const int e = (int)(r / slots);
-        const int s = (int)(r - (long long)e * slots);
-        for (int c = lane * 8; c < M; c += 256) {
-            float f[8];
-            gather_slot(y, e, s, c, f);
-            st_vec8(out + r * M + c, f32_to_vec8(f));
+        Picks<1> pk;
+        pk.ex[0] = (int)(r / slots);
+        pk.sl[0] = (int)(r - (long long)pk.ex[0] * slots);
+        pk.w[0] = 1.0f;
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            float acc[kChunks][8];
+#pragma unroll
+            for (int i = 0; i < kChunks; ++i)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[i][u] = 0.0f;
+            for (int p = 0; p < y.n_p; ++p) {
+                int4 buf[1][kChunks];
+                load_picks<1>(y, pk, p, g0, lane, M, buf);
+#pragma unroll
+                for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], 1.0f, buf[0][i]);
+            }
+#pragma unroll
+            for (int i = 0; i < kChunks; ++i) {
+                const int c = g0 + lane * 8 + i * 256;
+                if (c < M) st_vec8(out + r * M + c, f32_to_vec8(acc[i]));
+            }
         }
     }
 }
@@ -248,7 +351,7 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
                    "dispatch_rows: rows must be 16-byte aligned (M=%d)", M);
     const long long rows = (long long)E * slots_out;
     if (rows == 0) return 0;
-    dispatch_rows_kernel<<<row_grid(rows), kRowThreads, 0, s>>>(
+    dispatch_rows_kernel<<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
         reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
         reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s);
     PARM_CHECK_LAUNCH("dispatch_rows");
@@ -258,9 +361,13 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
 int combine_fwd(const SlotView& y, const int* expert_idx, const int* slot_idx, const float* combine_w, int n, int k,
                 int M, void* out, long long ldo, cudaStream_t s) {
     if (int rc = check_view(y, M, "combine_fwd")) return rc;
+    PARM_CHECK_ARG(k >= 1 && k <= 8, "combine_fwd: top_k must be in [1, 8]");
     if (n == 0) return 0;
-    combine_fwd_kernel<<<row_grid(n), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M,
-                                                           reinterpret_cast<bf16*>(out), ldo);
+    auto O = reinterpret_cast<bf16*>(out);
+    if (k <= 2)
+        combine_fwd_kernel<2><<<row_grid(n), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+    else
+        combine_fwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     PARM_CHECK_LAUNCH("combine_fwd");
     return 0;
 }
@@ -271,12 +378,12 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     PARM_CHECK_ARG(k <= 8 && E <= 32, "combine_bwd: k<=8 and E<=32 required");
     if (n == 0) return 0;
     auto D = reinterpret_cast<const bf16*>(dout);
-    if (E <= 8)
-        combine_bwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+    if (k <= 2)
+        combine_bwd_kernel<2><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     else
-        combine_bwd_kernel<32><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
-                                                                   M, dlogits);
+        combine_bwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+                                                                  dlogits);
     PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
 }
@@ -284,17 +391,18 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
 int dispatch_bwd(const SlotView& dr, const int* expert_idx, const int* slot_idx, const float* dlogits, const void* wg,
                  int n, int k, int E, int M, void* dx, long long ldx, cudaStream_t s) {
     if (int rc = check_view(dr, M, "dispatch_bwd")) return rc;
-    PARM_CHECK_ARG(E <= 32, "dispatch_bwd: E<=32 required");
+    PARM_CHECK_ARG(E <= 32 && k <= 8, "dispatch_bwd: E<=32 and k<=8 required");
     PARM_CHECK_ARG(dlogits == nullptr || wg != nullptr, "dispatch_bwd: dlogits needs gate weights");
     if (n == 0) return 0;
-    auto W = reinterpret_cast<const bf16*>(wg);
+    auto W = reinterpret_cast<const float*>(wg);
     auto DX = reinterpret_cast<bf16*>(dx);
-    if (E <= 8)
-        dispatch_bwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M,
-                                                                   DX, ldx);
+    const int g = row_grid(n);
+    if (k <= 2 && E <= 8)
+        dispatch_bwd_kernel<2, 8><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
+    else if (k <= 2)
+        dispatch_bwd_kernel<2, 32><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
     else
-        dispatch_bwd_kernel<32><<<row_grid(n), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M,
-                                                                    DX, ldx);
+        dispatch_bwd_kernel<8, 32><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
     PARM_CHECK_LAUNCH("dispatch_bwd");
     return 0;
 }

@@ -64,7 +64,7 @@ def plain_view(t: torch.Tensor, e_local: int | None = None) -> SlotView:
 def gate_fwd(x: torch.Tensor, wg: torch.Tensor, k: int, expert_idx: torch.Tensor, combine_w: torch.Tensor,
              probs: torch.Tensor | None) -> None:
     _need(x, torch.bfloat16, "tokens")
-    _need(wg, torch.bfloat16, "gate weights")
+    _need(wg, torch.float64, "gate weights (f64 upcast, transposed (E, M))")
     n, M = x.shape
     E = wg.shape[0]          # gate weights are stored transposed: (E, M)
     if x.stride(1) != 1 or not wg.is_contiguous():
@@ -73,11 +73,17 @@ def gate_fwd(x: torch.Tensor, wg: torch.Tensor, k: int, expert_idx: torch.Tensor
               combine_w.data_ptr(), _ptr(probs), _stream())
 
 
+def gate_slots_workspace(n: int, E: int) -> int:
+    return int(_lib.load().parm_gate_slots_workspace(n, E))
+
+
 def gate_slots(expert_idx: torch.Tensor, E: int, cap: int, slot_idx: torch.Tensor, slot_src: torch.Tensor,
-               fill: torch.Tensor) -> None:
+               fill: torch.Tensor, workspace: torch.Tensor | None = None) -> None:
     n, k = expert_idx.shape
+    if workspace is None:
+        workspace = torch.empty(max(1, gate_slots_workspace(n, E) // 4), dtype=torch.int32, device=expert_idx.device)
     _lib.call("parm_gate_slots", expert_idx.data_ptr(), n, k, E, cap, slot_idx.data_ptr(), slot_src.data_ptr(),
-              fill.data_ptr(), _stream())
+              fill.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream())
 
 
 def dispatch_rows(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, out: torch.Tensor,
@@ -113,6 +119,9 @@ def combine_bwd(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, sl
 
 def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, dlogits: torch.Tensor | None,
                  wg: torch.Tensor | None, E: int, dx: torch.Tensor) -> None:
+    """wg: the (E, M) f32 upcast of the transposed gate weights (or None with dlogits None)."""
+    if wg is not None:
+        _need(wg, torch.float32, "gate weights (f32 upcast, transposed (E, M))")
     n, M = dx.shape
     k = expert_idx.shape[1]
     v = view.c()

@@ -93,19 +93,21 @@ class Routing:
     fill: torch.Tensor         # (E,) int32
     cap: int
     token_offset: int = 0
+    ws: torch.Tensor | None = None     # gate_slots per-chunk counts
 
     @classmethod
     def alloc(cls, n: int, k: int, E: int, cap: int, dev, token_offset: int = 0,
               fill: torch.Tensor | None = None) -> "Routing":
         i32 = dict(dtype=torch.int32, device=dev)
         f32 = dict(dtype=torch.float32, device=dev)
+        ws = torch.empty(max(1, K.gate_slots_workspace(n, E) // 4), **i32)
         return cls(torch.empty(n, k, **i32), torch.empty(n, k, **f32), torch.empty(n, E, **f32),
                    torch.empty(n, k, **i32), torch.empty(E, max(cap, 1), **i32),
-                   fill if fill is not None else torch.zeros(E, **i32), cap, token_offset)
+                   fill if fill is not None else torch.zeros(E, **i32), cap, token_offset, ws)
 
     def run(self, x: torch.Tensor, wg_t: torch.Tensor, k: int) -> None:
         K.gate_fwd(x, wg_t, k, self.expert_idx, self.combine_w, self.probs)
-        K.gate_slots(self.expert_idx, wg_t.shape[0], self.cap, self.slot_idx, self.slot_src, self.fill)
+        K.gate_slots(self.expert_idx, wg_t.shape[0], self.cap, self.slot_idx, self.slot_src, self.fill, self.ws)
 
 
 @dataclass
@@ -118,6 +120,8 @@ class RankState:
     dw1t: torch.Tensor            # (e_local, Hsp, Mp) f32
     dw2t: torch.Tensor            # (e_local, Mp, Hsp) f32
     bufs: dict = field(default_factory=dict)
+    gate64: torch.Tensor | None = None   # exact f64 / f32 upcasts of `gate` for the gate (f64 logits) and
+    gate32: torch.Tensor | None = None   # dispatch-backward kernels; refreshed by MoELayer.refresh_gate()
 
 
 @dataclass
@@ -156,6 +160,7 @@ class MoELayer:
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
         self._last: str | None = None
         self._ws_gate = None
+        self.refresh_gate()
 
     # ------------------------------------------------------------ weights
     def local_experts(self, rank: int) -> range:
@@ -177,6 +182,13 @@ class MoELayer:
                 w2 = np.ascontiguousarray(weights.w2[e][p * d.Hs:(p + 1) * d.Hs, :].T)   # (M, Hs)
                 s.w1t[i, :d.Hs, :d.M].copy_(torch.from_numpy(w1).to(torch.float32).to(self.dev).to(torch.bfloat16))
                 s.w2t[i, :d.M, :d.Hs].copy_(torch.from_numpy(w2).to(torch.float32).to(self.dev).to(torch.bfloat16))
+        self.refresh_gate()
+
+    def refresh_gate(self) -> None:
+        """Re-derive the f64/f32 upcasts of the bf16 gate weights (call after updating ``gate``)."""
+        for s in self.st.values():
+            s.gate64 = s.gate.double()
+            s.gate32 = s.gate.float()
 
     def init_random(self, seed: int = 0) -> None:
         """Synthetic weights drawn directly on the device with the reference's
@@ -193,6 +205,7 @@ class MoELayer:
                                         / math.sqrt(d.M))
             s.w2t[:, :d.M, :d.Hs].copy_(torch.randn(d.e_local, d.M, d.Hs, generator=gen, device=self.dev)
                                         / math.sqrt(d.H))
+        self.refresh_gate()
 
     def shard_grads(self, rank: int) -> dict:
         """Gradients in the reference layout: dw1 (e_local, M, Hs), dw2 (e_local, Hs, M), dgate (M, E)."""
@@ -405,7 +418,7 @@ class MoELayer:
             x = self._input(b, xs[r], "x")
             b["xin"] = x
             rt = b["route"]
-            rt.run(x, s.gate, d.k)
+            rt.run(x, s.gate64, d.k)
             K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["send"])
             self._ffn_fwd(s, b)
             K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
@@ -424,7 +437,7 @@ class MoELayer:
             K.combine_bwd(dout, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
             self._ffn_bwd(s, b)
-            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
                            b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             res[r] = b["dx"][:, :d.M]
@@ -441,7 +454,7 @@ class MoELayer:
             xs_ = x[m * sl:(m + 1) * sl]                # MP split: this rank's token slice
             b["xslice"] = xs_
             rt = b["route"]
-            rt.run(xs_, s.gate, d.k)
+            rt.run(xs_, s.gate64, d.k)
             K.dispatch_rows(xs_, rt.slot_src, d.k, rt.cap, 0, b["send"])
         self.world.exchange(self._fused_msgs("s1", "send", "recv", with_fill=True))
         for r in self.ranks:
@@ -479,7 +492,7 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["s1"]
             m = L.mp_pos(r)
             rt = b["route"]
-            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
                            b["dx"][m * sl:(m + 1) * sl])
             K.gate_wgrad(b["xslice"], b["dlogits"], s.dgate, self._ws_gate)
             ins[r], outs[r] = b["dx"][m * sl:(m + 1) * sl], b["dx"]
@@ -502,7 +515,7 @@ class MoELayer:
             x = self._input(b, xs[r], "x")
             b["xin"] = x
             rt = b["route"]
-            rt.run(x, s.gate, d.k)
+            rt.run(x, s.gate64, d.k)
             K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"])
             # fill of this rank's slot shard [m*q, (m+1)*q): clamp(fill - m*q, 0, q) per expert
             if "shard_fill" not in b:
@@ -548,7 +561,7 @@ class MoELayer:
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s2"]
             rt = b["route"]
-            K.dispatch_bwd(self._gath_view(b, "dgath"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+            K.dispatch_bwd(self._gath_view(b, "dgath"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
                            b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
         return {r: self.st[r].bufs["s2"]["dx"][:, :d.M] for r in self.ranks}
@@ -568,14 +581,14 @@ class MoELayer:
             s, b = self.st[r], self._plan("baseline", r)
             x = self._input(b, xs[r], "x")
             b["xin"] = x
-            b["route"].run(x, s.gate, d.k)                       # combine weights of the own block
+            b["route"].run(x, s.gate64, d.k)                       # combine weights of the own block
             ins[r], outs[r] = x, b["xg"]
         self.world.allgather("esp", ins, outs)                   # ESP-AllGather of raw tokens
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             for q in range(d.ESP):                               # re-gate every gathered block
                 rt = b["route_blk"][q]
-                rt.run(b["xg"][q], s.gate, d.k)
+                rt.run(b["xg"][q], s.gate64, d.k)
                 K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][q])
         self.world.exchange(self._ep_dispatch_msgs("disp", "recv", with_fill=True))
         ys = {}
@@ -653,7 +666,7 @@ class MoELayer:
                 rt = b["route_blk"][q]
                 own = q == L.esp_pos(r)
                 K.dispatch_bwd(self._ret_own_view(b, "dd", q), rt.expert_idx, rt.slot_idx,
-                               b["dlogits"] if own else None, s.gate if own else None, d.E, b["dg"][q])
+                               b["dlogits"] if own else None, s.gate32 if own else None, d.E, b["dg"][q])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             gins[r], gouts[r] = b["dg"], b["dx"]
         self.world.reduce_scatter("esp", gins, gouts)            # adjoint of the ESP-AllGather

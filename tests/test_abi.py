@@ -62,7 +62,7 @@ def test_argument_validation_without_a_gpu(lib):
     # validation happens on the host before any launch, with the reference's error wording
     _expect_arg_error(lib.parm_gate_fwd, None, 8, None, 4, 8, 2, 3, None, None, None, None,
                       match=r"top_k \(3\) exceeds number of experts \(2\)")
-    _expect_arg_error(lib.parm_gate_slots, None, 4, 9, 2, 4, None, None, None, None, match="top_k must be")
+    _expect_arg_error(lib.parm_gate_slots, None, 4, 9, 2, 4, None, None, None, None, 0, None, match="top_k must be")
     _expect_arg_error(lib.parm_dispatch_rows, None, 10, None, None, 1, 2, 4, 0, 4, 10, None, 10, 10, None,
                       match="16-byte aligned")
     _expect_arg_error(lib.parm_combine_fwd, None, None, None, None, 4, 1, 8, None, 8, None,
@@ -75,8 +75,8 @@ def test_argument_validation_without_a_gpu(lib):
 
 
 def test_gate_wgrad_workspace_query(lib):
-    assert lib.parm_gate_wgrad_workspace(8192, 1024, 8) == 128 * 1024 * 8 * 4
-    assert lib.parm_gate_wgrad_workspace(10, 64, 4) == 64 * 4 * 4
+    assert lib.parm_gate_wgrad_workspace(8192, 1024, 8) == 64 * 1024 * 8 * 4      # 64 token chunks
+    assert lib.parm_gate_slots_workspace(8192, 8) == 32 * 8 * 4                   # 256-token chunks
 
 
 def test_missing_library_fails_loudly(tmp_path):

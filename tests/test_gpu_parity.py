@@ -53,7 +53,7 @@ def test_gate_routing_bit_exact(cuda_lib, n, M, E, k, cap):
     x = O.round_bf16(rng.normal(size=(n, M)))
     wg = O.round_bf16(rng.normal(size=(M, E)))
     ref = O.gate(x, wg, k, cap)
-    xd, wd = _t(x), _t(wg.T)          # gate weights live transposed (E, M) on the device
+    xd, wd = _t(x), _t(wg.T).double()   # gate weights live transposed (E, M), f64 upcast of bf16
     ei = torch.empty(n, k, dtype=torch.int32, device="cuda")
     cw = torch.empty(n, k, dtype=torch.float32, device="cuda")
     pr = torch.empty(n, E, dtype=torch.float32, device="cuda")
