@@ -192,7 +192,11 @@ def pick_schedule(cfg, layout, requested: str):
 
     if requested != "auto":
         return requested, None
-    prof_path = ROOT / "profiles" / "nvlink_profile.csv"
+    # the profile calibrated at this world size (paper_2407_00599_b200/calibrate.py), else the
+    # another calibrated one (NVSwitch: per-pair bandwidth barely depends on P)
+    cands = [ROOT / "profiles" / f"nvlink_profile_p{p}.csv" for p in (layout.world_size, 8, 4, 2)]
+    cands = [c for c in cands if c.exists()]
+    prof_path = cands[0] if cands else ROOT / "profiles" / "nvlink_profile.csv"
     if prof_path.exists():
         prof = selector.load_profile(prof_path)
         src = str(prof_path.relative_to(ROOT))

@@ -39,6 +39,7 @@ zeros, so every shape meets the GEMM contract without changing results.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -137,6 +138,17 @@ class StepGraph:
         self.graph.replay()
 
 
+def _saa_phased(layout: ParallelLayout) -> bool:
+    """Whether S2's return runs as the phased SAA (see MoELayer._saa).
+
+    Default: sequential.  On one NVSwitch box the return A2A and the MP AllGather
+    share the same NVLink ports, and the phased overlap measured 8% slower than
+    back-to-back collectives over the P=4 selector sweep (profiles/selector_sweep_p4*).
+    PARM_SAA=phased selects the paper's overlapped form (balanced rotation when
+    N_EP divides the number of MP groups)."""
+    return os.environ.get("PARM_SAA", "seq") == "phased" and layout.mp_size > 1 and layout.ep_size > 1
+
+
 class MoELayer:
     """One MoE layer under MP+EP+ESP on the ranks this process owns."""
 
@@ -150,6 +162,7 @@ class MoELayer:
         self.dev = self.world.device
         self.d = Dims.of(cfg, layout)
         d = self.d
+        self.saa_phased = _saa_phased(layout)
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -274,9 +287,11 @@ class MoELayer:
             b["dret"] = torch.zeros(d.P, el, b["q"], d.Mp, **bf)
             if schedule == "s2":
                 b["comb"] = torch.zeros(d.E, b["q"], d.Mp, **bf)
-                b["gath"] = torch.zeros(d.MP, d.E, b["q"], d.Mp, **bf)
+                # phased SAA gathers per expert block: (EP, MP, e_local, q, M); else (MP, E, q, M)
+                gshape = (d.EP, d.MP, el, b["q"], d.Mp) if self.saa_phased else (d.MP, d.E, b["q"], d.Mp)
+                b["gath"] = torch.zeros(gshape, **bf)
                 b["dcomb"] = torch.zeros(d.E, b["q"], d.Mp, **bf)
-                b["dgath"] = torch.zeros(d.MP, d.E, b["q"], d.Mp, **bf)
+                b["dgath"] = torch.zeros(gshape, **bf)
         nr = b["route"].expert_idx.shape[0]
         b["dlogits"] = torch.zeros(nr, d.E, dtype=torch.float32, device=dev)
         need = K.gate_wgrad_workspace(d.n, d.Mp, d.E)
@@ -503,10 +518,56 @@ class MoELayer:
 
     # ------------------------------------------------------------ S2
     def _gath_view(self, b: dict, key: str) -> K.SlotView:
+        """MP-gathered slots: row (e, s) = g[ep_e][s // q][i_e][s % q] (phased SAA, per-block
+        gathers) or g[s // q][e][s % q] (one gather)."""
         d = self.d
-        q = b["q"]
+        q, el = b["q"], d.e_local
+        if self.saa_phased:
+            return K.SlotView(b[key], e_local=el, slot_div=q, stride_ep=d.MP * el * q * d.Mp, stride_i=q * d.Mp,
+                              stride_shi=el * q * d.Mp, stride_slo=d.Mp)
         return K.SlotView(b[key], e_local=d.E, slot_div=q, stride_i=q * d.Mp, stride_shi=d.E * q * d.Mp,
                           stride_slo=d.Mp)
+
+    def _saa(self, src_key: str, ret_key: str, comb_key: str, gath_key: str) -> None:
+        """S2's return AlltoAll + MP AllGather (SAA, collectives.py:315-353, paper §IV-D).
+
+        Phased: the return is cut into N_EP phases.  In phase j, MP group g (ranks
+        g*N_MP ...) receives expert block (g + j) mod N_EP from its N_ESP holders, ESP-sums
+        it and starts that block's MP AllGather on the MP communicator while phase j+1
+        is on the wire.  The reference phases by source rank (every rank receives from
+        rank p in phase p), which on a switch leaves all but one sender idle per phase;
+        the per-group rotation keeps every holder sending in every phase (exactly
+        balanced when N_EP divides the number of MP groups).  Sequential (default, see
+        _saa_phased): the A2A, one ESP sum, one AllGather.  Either way the data is
+        identical to AllGather(ESP-sum(AlltoAll)), as the reference's is."""
+        d, L = self.d, self.layout
+        el = d.e_local
+        msgs = self._return_msgs("s2", src_key, ret_key)
+        if not self.saa_phased:
+            self.world.exchange(msgs)
+            ins, outs = {}, {}
+            for r in self.ranks:
+                b = self.st[r].bufs["s2"]
+                K.esp_sum(self._ret_view(b, ret_key), b[comb_key])
+                ins[r], outs[r] = b[comb_key], b[gath_key]
+            self.world.allgather("mp", ins, outs)
+            return
+        a, c = (d.ESP, 1) if L.esp_contiguous else (1, d.EP)
+        handles = []
+        for j in range(d.EP):
+            self.world.exchange([m for m in msgs if L.ep_pos(m.src) == (m.dst // d.MP + j) % d.EP])
+            ins, outs = {}, {}
+            for r in self.ranks:
+                bj = (r // d.MP + j) % d.EP
+                b = self.st[r].bufs["s2"]
+                blk = el * b["q"] * d.Mp
+                view = K.SlotView(b[ret_key], e_local=el, n_p=d.ESP, stride_i=b["q"] * d.Mp, stride_p=c * blk,
+                                  stride_slo=d.Mp, offset=bj * a * blk)
+                K.esp_sum(view, b[comb_key][bj * el:(bj + 1) * el])
+                ins[r], outs[r] = b[comb_key][bj * el:(bj + 1) * el], b[gath_key][bj]
+            handles.append(self.world.allgather_async("mp", ins, outs))
+        for h in handles:
+            self.world.wait(h)
 
     def _fwd_s2(self, xs: dict) -> dict:
         d, L = self.d, self.layout
@@ -525,13 +586,7 @@ class MoELayer:
         self.world.exchange(self._fused_msgs("s2", "send", "recv", with_fill=True, fill_key="shard_fill"))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
-        self.world.exchange(self._return_msgs("s2", "y", "ret"))
-        ins, outs = {}, {}
-        for r in self.ranks:
-            b = self.st[r].bufs["s2"]
-            K.esp_sum(self._ret_view(b, "ret"), b["comb"])
-            ins[r], outs[r] = b["comb"], b["gath"]
-        self.world.allgather("mp", ins, outs)
+        self._saa("y", "ret", "comb", "gath")
         for r in self.ranks:
             b = self.st[r].bufs["s2"]
             rt = b["route"]
@@ -551,13 +606,7 @@ class MoELayer:
         self.world.exchange(self._fused_msgs("s2", "dsend", "dyrecv", with_fill=False))
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
-        self.world.exchange(self._return_msgs("s2", "dr", "dret"))
-        ins, outs = {}, {}
-        for r in self.ranks:
-            b = self.st[r].bufs["s2"]
-            K.esp_sum(self._ret_view(b, "dret"), b["dcomb"])
-            ins[r], outs[r] = b["dcomb"], b["dgath"]
-        self.world.allgather("mp", ins, outs)                            # adjoint of the slot split
+        self._saa("dr", "dret", "dcomb", "dgath")                       # A2A + adjoint of the slot split
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s2"]
             rt = b["route"]

@@ -62,6 +62,14 @@ class World:
     def reduce_scatter(self, kind: str, ins: dict, outs: dict) -> None:
         raise NotImplementedError
 
+    def allgather_async(self, kind: str, ins: dict, outs: dict):
+        """Start an allgather that may overlap later exchanges; finish with wait()."""
+        self.allgather(kind, ins, outs)
+        return None
+
+    def wait(self, handle) -> None:
+        pass
+
     def barrier(self) -> None:
         pass
 
@@ -156,6 +164,21 @@ class NcclWorld(World):
                 dst.reshape(-1).copy_(src.reshape(-1))
             return
         self.dist.all_gather_into_tensor(dst.reshape(-1), src.reshape(-1), group=pg)
+
+    def allgather_async(self, kind: str, ins: dict, outs: dict):
+        # Runs on the group's own NCCL stream: it overlaps P2P exchanges issued
+        # after it on the world communicator until wait() joins it back.
+        grp, pg = self.groups[kind]
+        src, dst = ins[self.rank], outs[self.rank]
+        if len(grp) == 1:
+            if dst.data_ptr() != src.data_ptr():
+                dst.reshape(-1).copy_(src.reshape(-1))
+            return None
+        return self.dist.all_gather_into_tensor(dst.reshape(-1), src.reshape(-1), group=pg, async_op=True)
+
+    def wait(self, handle) -> None:
+        if handle is not None:
+            handle.wait()
 
     def allreduce(self, kind: str, bufs: dict) -> None:
         grp, pg = self.groups[kind]

@@ -186,6 +186,17 @@ def test_layer_fwd_bwd_matches_oracle(cuda_lib, schedule, cfg_t, lay_t, contig):
         assert got_drops == drops
 
 
+@pytest.mark.parametrize("mode,cfg_t,lay_t", [
+    ("phased", (2, 64, 128, 256, 8, 2, 1.2), (2, 4, 2, 8)),   # balanced rotation
+    ("phased", (2, 64, 128, 128, 8, 2, 2.4), (4, 8, 1, 8)),   # unbalanced rotation (one MP group)
+    ("phased", (2, 64, 64, 128, 16, 4, 1.0), (2, 4, 4, 16)),  # P=16, k=4
+])
+def test_s2_saa_modes_match_oracle(cuda_lib, monkeypatch, mode, cfg_t, lay_t):
+    """Both SAA executions (phased per expert block / A2A then AllGather) give the oracle's S2."""
+    monkeypatch.setenv("PARM_SAA", mode)
+    test_layer_fwd_bwd_matches_oracle(cuda_lib, "s2", cfg_t, lay_t, True)
+
+
 def test_schedules_agree_when_no_slice_overflow(cuda_lib):
     """Without overflow all three schedules compute the same function (reference C1 criterion)."""
     cfg_t, lay_t = (4, 128, 256, 512, 4, 2, 2.4), (2, 2, 2, 4)

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--schedule", default="s1")
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--cfg", default=None, help="B,L,M,H,E,k,f (default: bench C2)")
+    ap.add_argument("--layout", default=None, help="MP,EP,ESP (default: bench layout)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -38,8 +40,18 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    cfg = MoEConfig(**bench.C2)
-    layout = bench.layout_for(args.gpus)
+    if args.cfg:
+        b, l, m, h, e, k, f = args.cfg.split(",")
+        cfg = MoEConfig(int(b), int(l), int(m), int(h), int(e), int(k), float(f))
+    else:
+        cfg = MoEConfig(**bench.C2)
+    if args.layout:
+        from paper_2407_00599_b200.config import ParallelLayout
+
+        mp, ep, esp = (int(v) for v in args.layout.split(","))
+        layout = ParallelLayout(mp, ep, esp, args.gpus)
+    else:
+        layout = bench.layout_for(args.gpus)
     w = NcclWorld(layout, dev) if world > 1 else LocalWorld(layout, dev)
     layer = MoELayer(cfg, layout, w)
     layer.init_random(0)
