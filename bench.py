@@ -244,6 +244,44 @@ def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev, use_graph=True
     return ms
 
 
+def bind_numa_local(dev) -> str | None:
+    """Pin this process to the CPUs local to the GPU's PCIe root so pinned host
+    buffers (allocated after this) sit on the GPU's NUMA node; returns the cpulist."""
+    import torch
+
+    p = torch.cuda.get_device_properties(dev)
+    path = Path(f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/local_cpulist")
+    try:
+        spec = path.read_text().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return spec
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def h2d_bandwidth(host, dev) -> float:
+    """GB/s of one pinned host -> device copy of `host` (CUDA events)."""
+    import torch
+
+    buf = torch.empty(host.shape, dtype=host.dtype, device=dev)
+    buf.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        buf.copy_(host, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return 5 * host.numel() * host.element_size() / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
 def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_graph=True):
     """Public-API step with host buffers: H2D of the step's tokens and upstream
     gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
@@ -262,11 +300,17 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
         f.record(comp)
     steps_fn = [make_step(layer, schedule, {r: dx[sl]}, {r: dd[sl]}, use_graph) for sl in range(2)]
 
+    copy_ev = []
+
     def prefetch(slot):
         with torch.cuda.stream(cps):
             cps.wait_event(free[slot])
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(cps)
             dx[slot].copy_(host_x, non_blocking=True)
             dd[slot].copy_(host_d, non_blocking=True)
+            c1.record(cps)
+            copy_ev.append((c0, c1))
             ready[slot].record(cps)
 
     def run(total):
@@ -284,6 +328,7 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
+    copy_ev.clear()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
     cps.wait_event(e0)
@@ -291,6 +336,7 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    time_e2e.h2d_ms = statistics.median(a.elapsed_time(b) for a, b in copy_ev)   # copy engine time per step
     if dist is not None:
         dist.barrier()
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -374,13 +420,21 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     roof = gemm_roofline(layer, schedule, xs, ds, max(3, min(args.steps, 10)), dist, dev)
     e2e = None
     if not args.no_e2e:
+        aff = os.sched_getaffinity(0)
+        numa = bind_numa_local(dev)                 # host buffers on the GPU's NUMA node
         hx = x.cpu().pin_memory()
         hd = dout.cpu().pin_memory()
-        e_ms, h2d, d2h = time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev, use_graph)
+        os.sched_setaffinity(0, aff)
+        h2d_gbs = h2d_bandwidth(hx, dev)
+        reps = [time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev, use_graph) + (time_e2e.h2d_ms,)
+                for _ in range(3)]
+        e_ms, h2d, d2h, h2d_ms = sorted(reps)[1]                      # median of 3 repetitions
         tps = tokens_per_step(cfg, layout)
         e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream)"}
+               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream)",
+               "h2d_gbs_measured": h2d_gbs, "host_numa_cpus": numa, "h2d_ms_per_step_in_loop": h2d_ms,
+               "repetitions_ms": [r[0] for r in reps]}
     if rank != 0:
         if dist is not None:
             dist.barrier()

@@ -207,15 +207,20 @@ __device__ __forceinline__ bool row_tile_live(const Params& p, const int* sfill,
     return t.m0 < seg_fill(p, sfill, t.g, t.hi, t.lo);
 }
 
-// WGT: K iteration it -> (hi, lo, row block); live iff the block holds filled rows.
-__device__ __forceinline__ bool wgt_k_live(const Params& p, const int* sfill, int g, int it, int& hi, int& lo,
-                                           int& r0) {
-    const int kt = (p.L + BK - 1) / BK;
-    const int seg = it / kt;
-    r0 = (it - seg * kt) * BK;
-    hi = seg / p.nlo;
-    lo = seg - hi * p.nlo;
-    return r0 < seg_fill(p, sfill, g, hi, lo);
+// The live K blocks of one tile, in order: ROW walks k0 = 0, BK, ... K; WGT walks each
+// segment's filled rows (r0 < fill) -- the (hi, lo, r0) bookkeeping is per segment, not per
+// block, so the single MMA-issuing thread spends its cycles issuing MMAs.
+template <int KIND, class F>
+__device__ __forceinline__ void for_each_kblock(const Params& p, const int* sfill, int g, F&& body) {
+    if (KIND == kRow) {
+        for (int it = 0; it < p.k_iters; ++it) body(0, 0, it * BK);
+    } else {
+        for (int hi = 0; hi < p.nhi; ++hi)
+            for (int lo = 0; lo < p.nlo; ++lo) {
+                const int f = min(seg_fill(p, sfill, g, hi, lo), p.L);
+                for (int r0 = 0; r0 < f; r0 += BK) body(hi, lo, r0);
+            }
+    }
 }
 
 // Epilogue of one accumulator tile for the calling thread's row: 32-column
@@ -363,15 +368,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
                 const Tile t = decode_tile(p, tile, KIND, BN);
                 if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
-                for (int it = 0; it < p.k_iters; ++it) {
-                    int hi = t.hi, lo = t.lo, r0 = 0;
-                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     mbar_expect_tx(&full_bar[stage], C::kStageBytes);
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
                     if (KIND == kRow) {
-                        const int k0 = it * BK;
+                        const int k0 = r0;
                         tma_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
                         if (MB == kKMajor) {
                             tma_load_3d(&tmap_b, &full_bar[stage], sb, k0, t.n0, t.g);
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         stage = 0;
                         phase ^= 1;
                     }
-                }
+                });
             }
         }
     } else if (warp == 1) {
@@ -420,9 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + as * BN;
                 bool first = true;
-                for (int it = 0; it < p.k_iters; ++it) {
-                    int hi, lo, r0;
-                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                for_each_kblock<KIND>(p, sfill, t.g, [&](int, int, int) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         stage = 0;
                         phase ^= 1;
                     }
-                }
+                });
                 tc_commit(&tfull_bar[as]);   // also fires for an all-skipped WGT tile (epilogue writes zeros)
             }
         }
@@ -809,9 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
                 const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
                 if (!t.live) continue;
-                for (int it = 0; it < p.k_iters; ++it) {
-                    int hi = 0, lo = 0, r0 = 0;
-                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     const bool no_tma = (p.debug & 2) != 0;
                     if (leader)
@@ -823,13 +822,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             stage = 0;
                             phase ^= 1;
                         }
-                        continue;
+                        return;
                     }
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
                     const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
                     if (KIND == kRow) {
-                        const int k0 = it * BK;
+                        const int k0 = r0;
                         tma2_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
                         if (MB == kKMajor) {
                             tma2_load_3d(&tmap_b, &full_bar[stage], sb, k0, nb0, t.g);
@@ -852,7 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         stage = 0;
                         phase ^= 1;
                     }
-                }
+                });
             }
         }
     } else if (warp == 1) {
@@ -876,9 +875,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + as * BN;
                 bool first = true;
-                for (int it = 0; it < p.k_iters; ++it) {
-                    int hi, lo, r0;
-                    if (KIND == kWgt && !wgt_k_live(p, sfill, t.g, it, hi, lo, r0)) continue;
+                for_each_kblock<KIND>(p, sfill, t.g, [&](int, int, int) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
@@ -895,7 +892,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         stage = 0;
                         phase ^= 1;
                     }
-                }
+                });
                 tc2_commit_both(&tfull_bar[as]);
             }
         }
