@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 4
+#define PARM_ABI_VERSION 5
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -84,7 +84,7 @@ int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* 
                      void* stream);
 
 /* Dispatch backward: dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
- * (dlogits nullable; wg_t is the (E, M) f32 upcast of the gate weights).
+ * (dlogits nullable; wg_t is the (E, M) bf16 gate weights, transposed).
  * Adjoint of the dump + dispatch fill. */
 int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
                       const void* wg_t, int n, int k, int E, int M, void* dx, long long ldx, void* stream);

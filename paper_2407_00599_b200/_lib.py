@@ -66,7 +66,7 @@ SIGNATURES = {
     "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
 }
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class ParmError(RuntimeError):

@@ -16,6 +16,9 @@
 //
 // Gate weights live on the device TRANSPOSED, wgT (E, M), so a lane's 8
 // consecutive columns of one expert are one 16-byte load.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace parm {
@@ -133,6 +136,144 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
     }
 }
 
+// FP64 tensor-core gate (DMMA, mma.m8n8k4.f64) for M % 128 == 0.  A block of
+// four warps owns 8 tokens; warp w and quad lane q own the contiguous column
+// range [(4w + q) * M/16, ...) of all 8 tokens, so every lane streams its own
+// x and Wg^T segments with 16-byte loads.  The MMA's k index is the quad lane,
+// mapped to a lane-dependent column -- the same mapping for the A (x) and B
+// (Wg^T) fragments, which is all a dot product needs.  One DMMA = 8 tokens x 8
+// experts x 4 columns of exact-product f64 FMAs; the four warps' partial
+// logits are summed in a fixed order in shared memory, then warp 0 runs the
+// softmax and the stable top-k for its 8 tokens (token g on quad g).
+constexpr int kDmmaWarps = 4;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NT>   // n-tiles of 8 experts (E <= 8 NT)
+__global__ void __launch_bounds__(kDmmaWarps * 32) gate_fwd_dmma_kernel(
+    const bf16* __restrict__ x, long long ldx, const double* __restrict__ wgT, int n, int M, int E, int k,
+    int* __restrict__ expert_idx, float* __restrict__ combine_w, float* __restrict__ probs) {
+    __shared__ double red[kDmmaWarps][NT][64];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const int span = M / (4 * kDmmaWarps);
+    const int col0 = (warp * 4 + q) * span;
+    const double* wr[NT];
+    bool wok[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int e = nt * 8 + g;
+        wok[nt] = e < E;
+        wr[nt] = wgT + (long long)(wok[nt] ? e : 0) * M + col0;
+    }
+    for (int t0 = blockIdx.x * 8; t0 < n; t0 += gridDim.x * 8) {
+        const int t = t0 + g;
+        const bool tok = t < n;
+        const bf16* xr = x + (long long)(tok ? t : 0) * ldx + col0;
+        double acc[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+        for (int j = 0; j < span; j += 8) {
+            const int4 xv = tok ? __ldg(reinterpret_cast<const int4*>(xr + j)) : make_int4(0, 0, 0, 0);
+            double2 wv[NT][4];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    wv[nt][i] = wok[nt] ? __ldg(reinterpret_cast<const double2*>(wr[nt] + j) + i) : make_double2(0, 0);
+            Vec8 x8;
+            *reinterpret_cast<int4*>(&x8) = xv;
+            float xf[8];
+            vec8_to_f32(x8, xf);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double a = (double)xf[u];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    dmma884(acc[nt][0], acc[nt][1], a, (u & 1) ? wv[nt][u >> 1].y : wv[nt][u >> 1].x);
+            }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            red[warp][nt][g * 8 + 2 * q] = acc[nt][0];
+            red[warp][nt][g * 8 + 2 * q + 1] = acc[nt][1];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // lane (g, q) owns token t0 + g, experts nt * 8 + 2q + h
+            double sc[NT][2];
+            double mx = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int idx = g * 8 + 2 * q + h;
+                    double s = red[0][nt][idx];
+#pragma unroll
+                    for (int w = 1; w < kDmmaWarps; ++w) s += red[w][nt][idx];
+                    sc[nt][h] = s;
+                    if (nt * 8 + 2 * q + h < E) mx = fmax(mx, s);
+                }
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            double sum = 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    sc[nt][h] = (nt * 8 + 2 * q + h < E) ? exp(sc[nt][h] - mx) : 0.0;
+                    sum += sc[nt][h];
+                }
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            int rank[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    sc[nt][h] = sc[nt][h] / sum;
+                    rank[nt][h] = 0;
+                }
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                for (int nt2 = 0; nt2 < NT; ++nt2)
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const double other = __shfl_sync(0xffffffffu, sc[nt2][h2], (g << 2) | qq);
+                        const int e2 = nt2 * 8 + 2 * qq + h2;
+                        if (e2 >= E) continue;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int e = nt * 8 + 2 * q + h;
+                                rank[nt][h] += (other > sc[nt][h]) || (other == sc[nt][h] && e2 < e);
+                            }
+                    }
+            if (tok) {
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = nt * 8 + 2 * q + h;
+                        if (e >= E) continue;
+                        if (rank[nt][h] < k) {
+                            expert_idx[(long long)t * k + rank[nt][h]] = e;
+                            combine_w[(long long)t * k + rank[nt][h]] = (float)sc[nt][h];
+                        }
+                        if (probs) probs[(long long)t * E + e] = (float)sc[nt][h];
+                    }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Exclusive per-expert prefix count over tokens -> slots, exact, in two
 // parallel passes over 256-token chunks (one CTA each):
 //   slot_count  per-chunk per-expert pick counts (+ slot_src := -1)
@@ -239,17 +380,18 @@ __global__ void __launch_bounds__(kSlotChunk) slot_assign_kernel(const int* __re
 // dWg^T partials: part[c][e][m] = sum_{t in chunk c} dlogits[t][e] * x[t][m].
 // 512 threads = 4 token sub-groups x 128 lanes of 8 columns; 16-B loads, four
 // tokens in flight per thread; sub-groups reduced through shared memory.
-constexpr int kWgCols = 1024;
+constexpr int kWgCols = 256;             // 32 column lanes x 8 columns per CTA
 constexpr int kWgSub = 4;
 constexpr int kWgChunks = 64;
+constexpr int kWgThreads = kWgCols / 8 * kWgSub;
 
 template <int EMAX>
-__global__ void __launch_bounds__(512) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
+__global__ void __launch_bounds__(kWgCols / 8 * kWgSub) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
                                                                   const float* __restrict__ dlogits, int n, int M,
                                                                   int E, int chunk, float* __restrict__ part) {
     __shared__ float red[8][kWgCols / 8][8 + 1];     // one 8-expert block of one sub-group at a time
-    const int col_lane = threadIdx.x & 127;
-    const int sub = threadIdx.x >> 7;
+    const int col_lane = threadIdx.x % (kWgCols / 8);
+    const int sub = threadIdx.x / (kWgCols / 8);
     const int c = blockIdx.x * kWgCols + col_lane * 8;
     const int t_begin = blockIdx.y * chunk;
     const int t_end = min(n, t_begin + chunk);
@@ -309,20 +451,33 @@ __global__ void __launch_bounds__(512) gate_wgrad_partial_kernel(const bf16* __r
     }
 }
 
-__global__ void sum_partials_kernel(const float* __restrict__ part, int chunks, long long len, float* __restrict__ out,
-                                    int accumulate) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int c = 0;
-        for (; c + 4 <= chunks; c += 4) {
-            s0 += __ldg(part + (long long)c * len + i);
-            s1 += __ldg(part + (long long)(c + 1) * len + i);
-            s2 += __ldg(part + (long long)(c + 2) * len + i);
-            s3 += __ldg(part + (long long)(c + 3) * len + i);
+// out[i] (+)= sum_c part[c][i]: a CTA owns 32 consecutive outputs; warp w sums
+// chunks w, w + 8, ... with all its loads in flight, then the eight warp sums
+// are added in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restrict__ part, int chunks, long long len,
+                                                           float* __restrict__ out, int accumulate) {
+    __shared__ float ws[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long i = (long long)blockIdx.x * 32 + lane;
+    float s = 0.0f;
+    if (i < len) {
+        float v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int c = warp + 8 * r;
+            v[r] = c < chunks ? __ldg(part + (long long)c * len + i) : 0.0f;
         }
-        for (; c < chunks; ++c) s0 += __ldg(part + (long long)c * len + i);
-        const float s = (s0 + s1) + (s2 + s3);
-        out[i] = accumulate ? out[i] + s : s;
+        for (int c = warp + 64; c < chunks; c += 8) s += __ldg(part + (long long)c * len + i);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) s += v[r];
+    }
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < len) {
+        float tot = ws[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) tot += ws[w][lane];
+        out[i] = accumulate ? out[i] + tot : tot;
     }
 }
 
@@ -339,6 +494,16 @@ static void launch_gate_fwd(const bf16* x, long long ldx, const double* wgT, int
     gate_fwd_kernel<EMAX><<<blocks, kGateThreads, 0, s>>>(x, ldx, wgT, n, M, E, k, ei, cw, probs);
 }
 
+// PARM_GATE_DMMA=0 selects the FP64-FMA gate kernel (A/B comparisons).
+static bool gate_dmma_enabled() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("PARM_GATE_DMMA");
+        mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return mode == 1;
+}
+
 int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E, int k, int* expert_idx,
              float* combine_w, float* probs, cudaStream_t s) {
     PARM_CHECK_ARG(k >= 1 && k <= E, "top_k (%d) exceeds number of experts (%d)", k, E);
@@ -347,7 +512,18 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
     auto W = reinterpret_cast<const double*>(wgT);
-    if (E <= 2)
+    if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
+        const int blocks = (int)std::min<long long>((n + 7) / 8, (long long)kNumSMs * 64);
+        if (E <= 8)
+            gate_fwd_dmma_kernel<1><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+                                                                       probs);
+        else if (E <= 16)
+            gate_fwd_dmma_kernel<2><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+                                                                       probs);
+        else
+            gate_fwd_dmma_kernel<4><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+                                                                       probs);
+    } else if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 4)
         launch_gate_fwd<4>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
@@ -396,15 +572,14 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     dim3 grid((M + kWgCols - 1) / kWgCols, kWgChunks);
     auto X = reinterpret_cast<const bf16*>(x);
     if (E <= 8)
-        gate_wgrad_partial_kernel<8><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<8><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     else if (E <= 16)
-        gate_wgrad_partial_kernel<16><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<16><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     else
-        gate_wgrad_partial_kernel<32><<<grid, 512, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        gate_wgrad_partial_kernel<32><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
     PARM_CHECK_LAUNCH("gate_wgrad_partial");
     const long long len = (long long)M * E;
-    int blocks = (int)((len + 255) / 256);
-    sum_partials_kernel<<<blocks, 256, 0, s>>>(ws, kWgChunks, len, dwgT, accumulate);
+    sum_partials_kernel<<<(int)((len + 31) / 32), 256, 0, s>>>(ws, kWgChunks, len, dwgT, accumulate);
     PARM_CHECK_LAUNCH("gate_wgrad_sum");
     return 0;
 }

@@ -107,13 +107,16 @@ struct Picks {
     int sl[KT];
     int ex[KT];
     float w[KT];
+    long long off[KT];   // element offset of the pick's row in partial 0 of the view (slot_offset once per token)
     __device__ __forceinline__ void load(long long t, int k, const int* __restrict__ slot_idx,
-                                         const int* __restrict__ expert_idx, const float* __restrict__ cw) {
+                                         const int* __restrict__ expert_idx, const float* __restrict__ cw,
+                                         const SlotView& v) {
 #pragma unroll
         for (int j = 0; j < KT; ++j) {
             sl[j] = (j < k) ? __ldg(slot_idx + t * k + j) : -1;
             ex[j] = (sl[j] >= 0) ? __ldg(expert_idx + t * k + j) : 0;
             w[j] = (cw != nullptr && sl[j] >= 0) ? __ldg(cw + t * k + j) : 0.0f;
+            off[j] = sl[j] >= 0 ? slot_offset(v, ex[j], sl[j], 0) : 0;
         }
     }
 };
@@ -124,7 +127,7 @@ __device__ __forceinline__ void load_picks(const SlotView& v, const Picks<KT>& p
                                            int4 (&buf)[KT][kChunks]) {
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
-        const bf16* row = v.ptr + (pk.sl[j] >= 0 ? slot_offset(v, pk.ex[j], pk.sl[j], p) : 0);
+        const bf16* row = v.ptr + pk.off[j] + (long long)p * v.stride_p;
 #pragma unroll
         for (int i = 0; i < kChunks; ++i) {
             const int c = g0 + lane * 8 + i * 256;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_kernel(const SlotV
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
         Picks<KT> pk;
-        pk.load(t, k, slot_idx, expert_idx, combine_w);
+        pk.load(t, k, slot_idx, expert_idx, combine_w, y);
         for (int g0 = 0; g0 < M; g0 += kGroupCols) {
             float acc[kChunks][8];
 #pragma unroll
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16*
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t = warp_global; t < n; t += num_warps) {
         Picks<KT> pk;
-        pk.load(t, k, slot_idx, expert_idx, nullptr);
+        pk.load(t, k, slot_idx, expert_idx, nullptr, y);
         float dw[KT];
 #pragma unroll
         for (int j = 0; j < KT; ++j) dw[j] = 0.0f;
@@ -240,65 +243,85 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16*
     }
 }
 
-template <int KT, int EMAX>
-__global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_kernel(const SlotView dr,
+// dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T.  A warp takes TB (4 for
+// k <= 2) tokens per pass over 256-column groups: their TB x KT row loads per partial
+// are all in flight together, and each 16-byte Wg^T load (bf16, the gate
+// weights as stored) feeds all four tokens -- the gate term's weight traffic
+// is 1/TB of a token-per-warp loop's.
+template <int KT, int TB, int EMAX>   // EMAX > 0: E <= EMAX, logit gradients kept in registers
+__global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const SlotView dr,
                                                                        const int* __restrict__ expert_idx,
                                                                        const int* __restrict__ slot_idx,
                                                                        const float* __restrict__ dlogits,
-                                                                       const float* __restrict__ wgT, int n, int k,
+                                                                       const bf16* __restrict__ wgT, int n, int k,
                                                                        int E, int M, bf16* __restrict__ dx,
                                                                        long long ldx) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
-    for (long long t = warp_global; t < n; t += num_warps) {
-        Picks<KT> pk;
-        pk.load(t, k, slot_idx, expert_idx, nullptr);
-        float dl[EMAX];
+    for (long long t0 = warp_global * TB; t0 < n; t0 += num_warps * TB) {
+        long long off[TB][KT];   // row offset in partial 0, -1 = dropped / no token
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) dl[e] = (dlogits != nullptr && e < E) ? __ldg(dlogits + t * E + e) : 0.0f;
-        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
-            float acc[kChunks][8];
+        for (int b = 0; b < TB; ++b)
 #pragma unroll
-            for (int i = 0; i < kChunks; ++i)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc[i][u] = 0.0f;
-            for (int p = 0; p < dr.n_p; ++p) {
-                int4 buf[KT][kChunks];
-                load_picks<KT>(dr, pk, p, g0, lane, M, buf);
-#pragma unroll
-                for (int j = 0; j < KT; ++j)
-#pragma unroll
-                    for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], 1.0f, buf[j][i]);
+            for (int j = 0; j < KT; ++j) {
+                const long long t = t0 + b;
+                const int sl = (t < n && j < k) ? __ldg(slot_idx + t * k + j) : -1;
+                off[b][j] = sl >= 0 ? slot_offset(dr, __ldg(expert_idx + t * k + j), sl, 0) : -1;
             }
-            if (dlogits != nullptr) {   // + dlogits[t] . Wg^T (f32 copy of the transposed gate weights)
+        float dl[TB][EMAX > 0 ? EMAX : 1];   // gate-logit gradients, held across the column groups when E <= EMAX
+        if (EMAX > 0) {
 #pragma unroll
-                for (int e = 0; e < EMAX; ++e) {
-                    if (e < E) {
+            for (int b = 0; b < TB; ++b)
 #pragma unroll
-                        for (int i = 0; i < kChunks; ++i) {
-                            const int c = g0 + lane * 8 + i * 256;
-                            if (c < M) {
-                                const float4* wp = reinterpret_cast<const float4*>(wgT + (long long)e * M + c);
-                                const float4 w0 = __ldg(wp), w1 = __ldg(wp + 1);
-                                acc[i][0] = fmaf(dl[e], w0.x, acc[i][0]);
-                                acc[i][1] = fmaf(dl[e], w0.y, acc[i][1]);
-                                acc[i][2] = fmaf(dl[e], w0.z, acc[i][2]);
-                                acc[i][3] = fmaf(dl[e], w0.w, acc[i][3]);
-                                acc[i][4] = fmaf(dl[e], w1.x, acc[i][4]);
-                                acc[i][5] = fmaf(dl[e], w1.y, acc[i][5]);
-                                acc[i][6] = fmaf(dl[e], w1.z, acc[i][6]);
-                                acc[i][7] = fmaf(dl[e], w1.w, acc[i][7]);
-                            }
+                for (int e = 0; e < (EMAX > 0 ? EMAX : 1); ++e)
+                    dl[b][e] = (dlogits != nullptr && t0 + b < n && e < E) ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
+        }
+        for (int c0 = 0; c0 < M; c0 += 256) {
+            const int c = c0 + lane * 8;
+            if (c >= M) continue;
+            float acc[TB][8];
+#pragma unroll
+            for (int b = 0; b < TB; ++b)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[b][u] = 0.0f;
+            for (int p = 0; p < dr.n_p; ++p) {
+                int4 buf[TB][KT];
+#pragma unroll
+                for (int b = 0; b < TB; ++b)
+#pragma unroll
+                    for (int j = 0; j < KT; ++j)
+                        buf[b][j] = off[b][j] >= 0 ? ldg16(dr.ptr + off[b][j] + (long long)p * dr.stride_p + c)
+                                                   : make_int4(0, 0, 0, 0);
+#pragma unroll
+                for (int b = 0; b < TB; ++b)
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) fma_bf16x8(acc[b], 1.0f, buf[b][j]);
+            }
+            if (dlogits != nullptr) {
+                if (EMAX > 0) {
+#pragma unroll
+                    for (int e = 0; e < (EMAX > 0 ? EMAX : 1); ++e) {
+                        if (e >= E) break;
+                        const int4 wv = ldg16(wgT + (long long)e * M + c);
+#pragma unroll
+                        for (int b = 0; b < TB; ++b) fma_bf16x8(acc[b], dl[b][e], wv);
+                    }
+                } else {
+#pragma unroll 2
+                    for (int e = 0; e < E; ++e) {
+                        const int4 wv = ldg16(wgT + (long long)e * M + c);
+#pragma unroll
+                        for (int b = 0; b < TB; ++b) {
+                            const float d = t0 + b < n ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
+                            fma_bf16x8(acc[b], d, wv);
                         }
                     }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < kChunks; ++i) {
-                const int c = g0 + lane * 8 + i * 256;
-                if (c < M) st_vec8(dx + t * ldx + c, f32_to_vec8(acc[i]));
-            }
+            for (int b = 0; b < TB; ++b)
+                if (t0 + b < n) st_vec8(dx + (t0 + b) * ldx + c, f32_to_vec8(acc[b]));
         }
     }
 }
@@ -314,6 +337,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const SlotView 
         pk.ex[0] = (int)(r / slots);
         pk.sl[0] = (int)(r - (long long)pk.ex[0] * slots);
         pk.w[0] = 1.0f;
+        pk.off[0] = slot_offset(y, pk.ex[0], pk.sl[0], 0);
         for (int g0 = 0; g0 < M; g0 += kGroupCols) {
             float acc[kChunks][8];
 #pragma unroll
@@ -394,15 +418,18 @@ int dispatch_bwd(const SlotView& dr, const int* expert_idx, const int* slot_idx,
     PARM_CHECK_ARG(E <= 32 && k <= 8, "dispatch_bwd: E<=32 and k<=8 required");
     PARM_CHECK_ARG(dlogits == nullptr || wg != nullptr, "dispatch_bwd: dlogits needs gate weights");
     if (n == 0) return 0;
-    auto W = reinterpret_cast<const float*>(wg);
+    auto W = reinterpret_cast<const bf16*>(wg);
     auto DX = reinterpret_cast<bf16*>(dx);
-    const int g = row_grid(n);
+    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "dispatch_bwd: rows must be 16-byte aligned (M=%d)", M);
     if (k <= 2 && E <= 8)
-        dispatch_bwd_kernel<2, 8><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
+        dispatch_bwd_kernel<2, 4, 8><<<row_grid((n + 3) / 4), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits,
+                                                                                      W, n, k, E, M, DX, ldx);
     else if (k <= 2)
-        dispatch_bwd_kernel<2, 32><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
+        dispatch_bwd_kernel<2, 4, 0><<<row_grid((n + 3) / 4), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits,
+                                                                                      W, n, k, E, M, DX, ldx);
     else
-        dispatch_bwd_kernel<8, 32><<<g, kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k, E, M, DX, ldx);
+        dispatch_bwd_kernel<8, 1, 0><<<row_grid(n), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k,
+                                                                            E, M, DX, ldx);
     PARM_CHECK_LAUNCH("dispatch_bwd");
     return 0;
 }

@@ -119,9 +119,9 @@ def combine_bwd(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, sl
 
 def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, dlogits: torch.Tensor | None,
                  wg: torch.Tensor | None, E: int, dx: torch.Tensor) -> None:
-    """wg: the (E, M) f32 upcast of the transposed gate weights (or None with dlogits None)."""
+    """wg: the transposed (E, M) bf16 gate weights (or None with dlogits None)."""
     if wg is not None:
-        _need(wg, torch.float32, "gate weights (f32 upcast, transposed (E, M))")
+        _need(wg, torch.bfloat16, "gate weights (bf16, transposed (E, M))")
     n, M = dx.shape
     k = expert_idx.shape[1]
     v = view.c()

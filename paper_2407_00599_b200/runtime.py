@@ -121,8 +121,7 @@ class RankState:
     dw1t: torch.Tensor            # (e_local, Hsp, Mp) f32
     dw2t: torch.Tensor            # (e_local, Mp, Hsp) f32
     bufs: dict = field(default_factory=dict)
-    gate64: torch.Tensor | None = None   # exact f64 / f32 upcasts of `gate` for the gate (f64 logits) and
-    gate32: torch.Tensor | None = None   # dispatch-backward kernels; refreshed by MoELayer.refresh_gate()
+    gate64: torch.Tensor | None = None   # exact f64 upcast of `gate` for the f64 logits (refresh_gate())
 
 
 @dataclass
@@ -198,10 +197,9 @@ class MoELayer:
         self.refresh_gate()
 
     def refresh_gate(self) -> None:
-        """Re-derive the f64/f32 upcasts of the bf16 gate weights (call after updating ``gate``)."""
+        """Re-derive the f64 upcast of the bf16 gate weights (call after updating ``gate``)."""
         for s in self.st.values():
             s.gate64 = s.gate.double()
-            s.gate32 = s.gate.float()
 
     def init_random(self, seed: int = 0) -> None:
         """Synthetic weights drawn directly on the device with the reference's
@@ -452,7 +450,7 @@ class MoELayer:
             K.combine_bwd(dout, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
             self._ffn_bwd(s, b)
-            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
+            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                            b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             res[r] = b["dx"][:, :d.M]
@@ -507,7 +505,7 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["s1"]
             m = L.mp_pos(r)
             rt = b["route"]
-            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
+            K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                            b["dx"][m * sl:(m + 1) * sl])
             K.gate_wgrad(b["xslice"], b["dlogits"], s.dgate, self._ws_gate)
             ins[r], outs[r] = b["dx"][m * sl:(m + 1) * sl], b["dx"]
@@ -610,7 +608,7 @@ class MoELayer:
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s2"]
             rt = b["route"]
-            K.dispatch_bwd(self._gath_view(b, "dgath"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate32, d.E,
+            K.dispatch_bwd(self._gath_view(b, "dgath"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                            b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
         return {r: self.st[r].bufs["s2"]["dx"][:, :d.M] for r in self.ranks}
@@ -715,7 +713,7 @@ class MoELayer:
                 rt = b["route_blk"][q]
                 own = q == L.esp_pos(r)
                 K.dispatch_bwd(self._ret_own_view(b, "dd", q), rt.expert_idx, rt.slot_idx,
-                               b["dlogits"] if own else None, s.gate32 if own else None, d.E, b["dg"][q])
+                               b["dlogits"] if own else None, s.gate if own else None, d.E, b["dg"][q])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
             gins[r], gouts[r] = b["dg"], b["dx"]
         self.world.reduce_scatter("esp", gins, gouts)            # adjoint of the ESP-AllGather
