@@ -38,6 +38,7 @@ def _digest() -> str:
                                                                            Path(__file__)]):
         h.update(p.name.encode())
         h.update(p.read_bytes())
+    h.update(os.environ.get("PARM_NVCC_DEFINES", "").encode())
     return h.hexdigest()
 
 
@@ -51,6 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     build_dir.mkdir(exist_ok=True)
     flags = ARCH_FLAGS + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                           "-I", str(ROOT / "include")]
+    flags += os.environ.get("PARM_NVCC_DEFINES", "").split()      # experiments only (e.g. -DPARM_EPI_BUFS=1)
     if verbose or os.environ.get("PARM_PTXAS_VERBOSE"):
         flags += ["-Xptxas", "-v"]
     for src in SOURCES:
