@@ -153,6 +153,74 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
+// Softmax + stable top-k of one token's logits held by a lane quad: lane
+// (g, q) owns experts nt * 8 + 2q + h of token t (the DMMA C-fragment layout).
+template <int NT>
+__device__ __forceinline__ void gate_topk_epilogue(double (&lg)[NT][2], int g, int q, int t, bool tok, int E, int k,
+                                                   int* __restrict__ expert_idx, float* __restrict__ combine_w,
+                                                   float* __restrict__ probs) {
+    double sc[NT][2];
+    double mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            sc[nt][h] = lg[nt][h];
+            if (nt * 8 + 2 * q + h < E) mx = fmax(mx, sc[nt][h]);
+        }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    double sum = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            sc[nt][h] = (nt * 8 + 2 * q + h < E) ? exp(sc[nt][h] - mx) : 0.0;
+            sum += sc[nt][h];
+        }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    int rank[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            sc[nt][h] = sc[nt][h] / sum;
+            rank[nt][h] = 0;
+        }
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int nt2 = 0; nt2 < NT; ++nt2)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const double other = __shfl_sync(0xffffffffu, sc[nt2][h2], (g << 2) | qq);
+                const int e2 = nt2 * 8 + 2 * qq + h2;
+                if (e2 >= E) continue;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = nt * 8 + 2 * q + h;
+                        rank[nt][h] += (other > sc[nt][h]) || (other == sc[nt][h] && e2 < e);
+                    }
+            }
+    if (tok) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = nt * 8 + 2 * q + h;
+                if (e >= E) continue;
+                if (rank[nt][h] < k) {
+                    expert_idx[(long long)t * k + rank[nt][h]] = e;
+                    combine_w[(long long)t * k + rank[nt][h]] = (float)sc[nt][h];
+                }
+                if (probs) probs[(long long)t * E + e] = (float)sc[nt][h];
+            }
+    }
+}
+
 template <int NT>   // n-tiles of 8 experts (E <= 8 NT)
 __global__ void __launch_bounds__(kDmmaWarps * 32) gate_fwd_dmma_kernel(
     const bf16* __restrict__ x, long long ldx, const double* __restrict__ wgT, int n, int M, int E, int k,
@@ -204,9 +272,7 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) gate_fwd_dmma_kernel(
         }
         __syncthreads();
         if (warp == 0) {
-            // lane (g, q) owns token t0 + g, experts nt * 8 + 2q + h
-            double sc[NT][2];
-            double mx = -INFINITY;
+            double lg[NT][2];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -215,62 +281,108 @@ __global__ void __launch_bounds__(kDmmaWarps * 32) gate_fwd_dmma_kernel(
                     double s = red[0][nt][idx];
 #pragma unroll
                     for (int w = 1; w < kDmmaWarps; ++w) s += red[w][nt][idx];
-                    sc[nt][h] = s;
-                    if (nt * 8 + 2 * q + h < E) mx = fmax(mx, s);
+                    lg[nt][h] = s;
                 }
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            double sum = 0.0;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    sc[nt][h] = (nt * 8 + 2 * q + h < E) ? exp(sc[nt][h] - mx) : 0.0;
-                    sum += sc[nt][h];
-                }
-            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-            int rank[NT][2];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    sc[nt][h] = sc[nt][h] / sum;
-                    rank[nt][h] = 0;
-                }
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-#pragma unroll
-                for (int nt2 = 0; nt2 < NT; ++nt2)
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        const double other = __shfl_sync(0xffffffffu, sc[nt2][h2], (g << 2) | qq);
-                        const int e2 = nt2 * 8 + 2 * qq + h2;
-                        if (e2 >= E) continue;
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const int e = nt * 8 + 2 * q + h;
-                                rank[nt][h] += (other > sc[nt][h]) || (other == sc[nt][h] && e2 < e);
-                            }
-                    }
-            if (tok) {
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = nt * 8 + 2 * q + h;
-                        if (e >= E) continue;
-                        if (rank[nt][h] < k) {
-                            expert_idx[(long long)t * k + rank[nt][h]] = e;
-                            combine_w[(long long)t * k + rank[nt][h]] = (float)sc[nt][h];
-                        }
-                        if (probs) probs[(long long)t * E + e] = (float)sc[nt][h];
-                    }
-            }
+            gate_topk_epilogue<NT>(lg, g, q, t, tok, E, k, expert_idx, combine_w, probs);
         }
         __syncthreads();
+    }
+}
+
+// Same DMMA formulation with Wg^T staged once per CTA in shared memory (f64,
+// E x M padded so the 32 lanes' B-fragment reads hit distinct bank pairs) and
+// one 8-token tile per warp: lane quad q owns the column quarter [qM/4, ...),
+// so a tile's whole reduction stays inside one warp (no cross-warp sum) and the
+// only global traffic is the x rows.  Used when the padded Wg^T fits in shared
+// memory; x chunks of 64 columns are loaded together ahead of their DMMAs.
+__device__ __forceinline__ int4 ldg_v4_ordered(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+constexpr int kGateSmemWarps = 8;
+
+
+__host__ __device__ constexpr long long gate_smem_stride(int M) { return M + 33; }   // doubles per expert row
+
+template <int NT>
+__global__ void __launch_bounds__(kGateSmemWarps * 32) gate_fwd_dmma_smem_kernel(
+    const bf16* __restrict__ x, long long ldx, const double* __restrict__ wgT, int n, int M, int E, int k,
+    int* __restrict__ expert_idx, float* __restrict__ combine_w, float* __restrict__ probs) {
+    extern __shared__ double sw[];
+    const int Q = M / 4;
+    const long long stride = gate_smem_stride(M);
+    // stage Wg^T: 8 double2 loads in flight per thread per batch (M even: a pair never straddles rows/quarters)
+    const int pairs = NT * 8 * M / 2;
+    for (int b0 = 0; b0 < pairs; b0 += 8 * blockDim.x) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = b0 + u * blockDim.x + threadIdx.x;
+            const int e = (2 * i) / M;
+            v[u] = (i < pairs && e < E) ? __ldg(reinterpret_cast<const double2*>(wgT) + i) : make_double2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = b0 + u * blockDim.x + threadIdx.x;
+            if (i >= pairs) break;
+            const int e = (2 * i) / M, c = 2 * i - e * M;
+            double* d = sw + e * stride + c + (c / Q) * 8;
+            d[0] = v[u].x;
+            d[1] = v[u].y;
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const double* wrow[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) wrow[nt] = sw + (nt * 8 + g) * stride + (long long)q * (Q + 8);
+    const int tiles = (n + 7) / 8;
+    for (int tile = blockIdx.x * kGateSmemWarps + warp; tile < tiles; tile += gridDim.x * kGateSmemWarps) {
+        const int t = tile * 8 + g;
+        const bool tok = t < n;
+        const bf16* xr = x + (long long)(tok ? t : 0) * ldx + (long long)q * Q;
+        double acc[2][NT][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+        int4 nxt[8];                            // chunk j0 + 64 is in flight while chunk j0 is consumed
+#pragma unroll
+        for (int i = 0; i < 8; ++i) nxt[i] = ldg_v4_ordered(xr + (8 * i < Q ? 8 * i : 0));
+        for (int j0 = 0; j0 < Q; j0 += 64) {
+            int4 xv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xv[i] = nxt[i];
+            if (j0 + 64 < Q) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) nxt[i] = ldg_v4_ordered(xr + (j0 + 64 + 8 * i < Q ? j0 + 64 + 8 * i : 0));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (j0 + 8 * i >= Q) break;
+                Vec8 x8;
+                *reinterpret_cast<int4*>(&x8) = tok ? xv[i] : make_int4(0, 0, 0, 0);
+                float xf[8];
+                vec8_to_f32(x8, xf);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int c = j0 + 8 * i + u;
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+                        dmma884(acc[u & 1][nt][0], acc[u & 1][nt][1], (double)xf[u], wrow[nt][c]);
+                }
+            }
+        }
+        double lg[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            lg[nt][0] = acc[0][nt][0] + acc[1][nt][0];
+            lg[nt][1] = acc[0][nt][1] + acc[1][nt][1];
+        }
+        gate_topk_epilogue<NT>(lg, g, q, t, tok, E, k, expert_idx, combine_w, probs);
     }
 }
 
@@ -512,7 +624,23 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
     auto W = reinterpret_cast<const double*>(wgT);
-    if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
+    const int nt_need = (E + 7) / 8;
+    const size_t smem_bytes = (size_t)(nt_need <= 2 ? nt_need : 4) * 8 * gate_smem_stride(M) * sizeof(double);
+    if (M % 64 == 0 && nt_need <= 2 && smem_bytes <= 200 * 1024 && gate_dmma_enabled()) {
+        const int tiles = (n + 7) / 8;
+        const int blocks = (int)std::min<long long>((tiles + kGateSmemWarps - 1) / kGateSmemWarps, kNumSMs * 2);
+        if (nt_need == 1) {
+            cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_bytes);
+            gate_fwd_dmma_smem_kernel<1><<<blocks, kGateSmemWarps * 32, smem_bytes, s>>>(X, ldx, W, n, M, E, k,
+                                                                                        expert_idx, combine_w, probs);
+        } else {
+            cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_bytes);
+            gate_fwd_dmma_smem_kernel<2><<<blocks, kGateSmemWarps * 32, smem_bytes, s>>>(X, ldx, W, n, M, E, k,
+                                                                                        expert_idx, combine_w, probs);
+        }
+    } else if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
         const int blocks = (int)std::min<long long>((n + 7) / 8, (long long)kNumSMs * 64);
         if (E <= 8)
             gate_fwd_dmma_kernel<1><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,

@@ -26,6 +26,14 @@ constexpr int kRowThreads = 256;
 constexpr int kChunks = 4;                  // 16-B chunks per lane per column group (1024 columns / warp)
 constexpr int kGroupCols = kChunks * 256;
 
+// Token loops that prefetch the next token's routing run on a resident grid
+// (every warp loops over several tokens, so the prefetch has a next token).
+static int resident_grid(long long tokens, int ctas_per_sm) {
+    long long blocks = (tokens * 32 + kRowThreads - 1) / kRowThreads;
+    const long long cap = (long long)kNumSMs * ctas_per_sm;
+    return (int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
 static int row_grid(long long rows) {
     long long blocks = (rows * 32 + kRowThreads - 1) / kRowThreads;
     const long long cap = (long long)kNumSMs * 16;
@@ -155,9 +163,11 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_kernel(const SlotV
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
+    Picks<KT> nx;
+    if (warp_global < n) nx.load(warp_global, k, slot_idx, expert_idx, combine_w, y);
     for (long long t = warp_global; t < n; t += num_warps) {
-        Picks<KT> pk;
-        pk.load(t, k, slot_idx, expert_idx, combine_w, y);
+        const Picks<KT> pk = nx;                    // this token's routing, fetched one iteration ago
+        if (t + num_warps < n) nx.load(t + num_warps, k, slot_idx, expert_idx, combine_w, y);
         for (int g0 = 0; g0 < M; g0 += kGroupCols) {
             float acc[kChunks][8];
 #pragma unroll
@@ -190,9 +200,11 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16*
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
+    Picks<KT> nx;
+    if (warp_global < n) nx.load(warp_global, k, slot_idx, expert_idx, nullptr, y);
     for (long long t = warp_global; t < n; t += num_warps) {
-        Picks<KT> pk;
-        pk.load(t, k, slot_idx, expert_idx, nullptr, y);
+        const Picks<KT> pk = nx;
+        if (t + num_warps < n) nx.load(t + num_warps, k, slot_idx, expert_idx, nullptr, y);
         float dw[KT];
 #pragma unroll
         for (int j = 0; j < KT; ++j) dw[j] = 0.0f;
@@ -389,9 +401,9 @@ int combine_fwd(const SlotView& y, const int* expert_idx, const int* slot_idx, c
     if (n == 0) return 0;
     auto O = reinterpret_cast<bf16*>(out);
     if (k <= 2)
-        combine_fwd_kernel<2><<<row_grid(n), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        combine_fwd_kernel<2><<<resident_grid(n, 3), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     else
-        combine_fwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        combine_fwd_kernel<8><<<resident_grid(n, 3), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     PARM_CHECK_LAUNCH("combine_fwd");
     return 0;
 }
@@ -403,10 +415,10 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     if (n == 0) return 0;
     auto D = reinterpret_cast<const bf16*>(dout);
     if (k <= 2)
-        combine_bwd_kernel<2><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        combine_bwd_kernel<2><<<resident_grid(n, 3), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     else
-        combine_bwd_kernel<8><<<row_grid(n), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        combine_bwd_kernel<8><<<resident_grid(n, 3), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
