@@ -427,8 +427,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         os.sched_setaffinity(0, aff)
         h2d_gbs = h2d_bandwidth(hx, dev)
         reps = [time_e2e(layer, schedule, hx, hd, args.steps, args.warmup, dist, dev, use_graph) + (time_e2e.h2d_ms,)
-                for _ in range(3)]
-        e_ms, h2d, d2h, h2d_ms = sorted(reps)[1]                      # median of 3 repetitions
+                for _ in range(5)]
+        e_ms, h2d, d2h, h2d_ms = sorted(reps)[2]                      # median of 5 repetitions
         tps = tokens_per_step(cfg, layout)
         e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
