@@ -380,7 +380,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     from paper_2407_00599_b200 import _lib
     from paper_2407_00599_b200.config import MoEConfig
     from paper_2407_00599_b200.runtime import MoELayer
-    from paper_2407_00599_b200.world import LocalWorld, NcclWorld
+    from paper_2407_00599_b200.world import LocalWorld, NcclWorld, PeerWorld
 
     dist = None
     torch.cuda.set_device(local_rank)
@@ -394,7 +394,20 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     layout = layout_for(args.gpus)
     if layout.world_size != world:
         raise SystemExit(f"--gpus {args.gpus} needs {args.gpus} ranks (got {world})")
-    w = NcclWorld(layout, dev) if world > 1 else LocalWorld(layout, dev)
+    transport = "local"
+    if world > 1:
+        transport = "nccl"
+        w = None
+        if os.environ.get("PARM_PEER", "1") != "0":
+            try:
+                w = PeerWorld(layout, dev)
+                transport = "nvlink-peer (S1) + nccl"
+            except Exception as exc:   # symmetric memory unavailable: NCCL for every exchange
+                print(f"peer memory unavailable ({exc}); using NCCL", file=sys.stderr)
+        if w is None:
+            w = NcclWorld(layout, dev)
+    else:
+        w = LocalWorld(layout, dev)
     layer = MoELayer(cfg, layout, w)
     layer.init_random(seed=0)
     g = torch.Generator(device=dev).manual_seed(1000 + rank // layout.mp_size)
@@ -475,6 +488,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         "selector": sel,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "launch_mode": "eager" if args.eager else "cuda_graph (one replay per step; NCCL calls captured)",
+        "transport": transport,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -21,25 +21,52 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 5
+#define PARM_ABI_VERSION 6
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
- *   row(e, s, p) = ptr + (e / e_local) * stride_ep + (e % e_local) * stride_i
- *                + p * stride_p + (s / slot_div) * stride_shi
- *                + (s % slot_div) * stride_slo            (element strides)  */
+ *   row(e, s, p) = base(e / e_local, p) + (e % e_local) * stride_i
+ *                + (s / slot_div) * stride_shi + (s % slot_div) * stride_slo
+ * with base(ep, p) = ptr + ep * stride_ep + p * stride_p for a local view
+ * (n_peer == 0), or peer[ep * peer_ep + p * peer_p] when the rows live in other
+ * GPUs' buffers mapped into this process (symmetric memory over NVLink;
+ * n_peer > 0).  Element strides. */
+#define PARM_MAX_PEERS 8
 typedef struct parm_slot_view {
     const void* ptr; /* bf16 */
     int e_local;
     int n_p;
     int slot_div;
-    int pad_;
+    int n_peer;
     long long stride_ep;
     long long stride_i;
     long long stride_p;
     long long stride_shi;
     long long stride_slo;
+    const void* peer[PARM_MAX_PEERS];
+    int peer_ep;
+    int peer_p;
 } parm_slot_view;
+
+/* Output rows written to n buffers of identical layout (fused AllGather). */
+typedef struct parm_row_fan {
+    void* ptr[PARM_MAX_PEERS]; /* bf16 */
+    int n;
+    int pad_;
+} parm_row_fan;
+
+/* Per-destination int32 tables, indexed like parm_slot_view.peer. */
+typedef struct parm_int_fan {
+    int* ptr[PARM_MAX_PEERS];
+} parm_int_fan;
+
+/* Device-side barrier over peers' signal pads (symmetric memory). */
+typedef struct parm_peer_signal {
+    void* pad[PARM_MAX_PEERS]; /* uint32 slots, this rank writes pad[j][rank] */
+    void* counter;             /* uint32 on this device: epoch, advanced by every barrier */
+    int rank;
+    int n;
+} parm_peer_signal;
 
 int parm_abi_version(void);
 const char* parm_last_error(void);
@@ -92,6 +119,34 @@ int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int
 /* S2: out (E, slots, M) = sum_p Y_p[e, s], the ESP sum of fused_combine
  * (collectives.py:302-310) materialised before the MP AllGather. */
 int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, void* stream);
+
+/* ---- peer-memory (NVLink symmetric buffers) variants: the collective fused
+ * into the kernel that produces or consumes the rows.  Buffers are mapped
+ * into this process (torch symmetric memory / CUDA IPC); the caller orders
+ * them with parm_peer_barrier. */
+
+/* Dispatch fused with the EP&ESP AlltoAll and its dump (collectives.py:256-283):
+ * slot rows of this source are stored into every holder's receive buffer,
+ * row(e, s, p) of `dst` for p < dst->n_p (the N_ESP holders of e's block),
+ * plus the per-segment fill counts clamp(fill[e] - slot_lo, 0, slots_out) into
+ * fill_dst->ptr[ep * dst->peer_ep + p * dst->peer_p][e % e_local]. */
+int parm_dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E,
+                            int cap, int slot_lo, int slots_out, int M, const parm_slot_view* dst, const int* fill,
+                            const parm_int_fan* fill_dst, void* stream);
+
+/* combine_fwd reading the expert outputs through a (peer) view -- the return
+ * AlltoAll + ESP sum fused into the combine -- and writing each output row to
+ * out->n buffers (the MP AllGather fused into the producer). */
+int parm_combine_fwd_fan(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
+                         int n, int k, int M, const parm_row_fan* out, long long ldo, void* stream);
+
+/* dispatch_bwd with the same fusions (return AlltoAll of dR + MP AllGather of dx). */
+int parm_dispatch_bwd_fan(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
+                          const void* wg_t, int n, int k, int E, int M, const parm_row_fan* dx, long long ldx,
+                          void* stream);
+
+/* Device-side barrier of the n peers (one tiny kernel; graph-capturable). */
+int parm_peer_barrier(const parm_peer_signal* sig, void* stream);
 
 /* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic two-pass).
  * accumulate != 0 adds into dwg. */

@@ -19,19 +19,37 @@ _vp = ctypes.c_void_p
 _size = ctypes.c_size_t
 
 
+MAX_PEERS = 8
+
+
 class SlotViewC(ctypes.Structure):
     _fields_ = [
         ("ptr", _vp),
         ("e_local", _c_int),
         ("n_p", _c_int),
         ("slot_div", _c_int),
-        ("pad_", _c_int),
+        ("n_peer", _c_int),
         ("stride_ep", _c_ll),
         ("stride_i", _c_ll),
         ("stride_p", _c_ll),
         ("stride_shi", _c_ll),
         ("stride_slo", _c_ll),
+        ("peer", _vp * MAX_PEERS),
+        ("peer_ep", _c_int),
+        ("peer_p", _c_int),
     ]
+
+
+class RowFanC(ctypes.Structure):
+    _fields_ = [("ptr", _vp * MAX_PEERS), ("n", _c_int), ("pad_", _c_int)]
+
+
+class IntFanC(ctypes.Structure):
+    _fields_ = [("ptr", _vp * MAX_PEERS)]
+
+
+class PeerSignalC(ctypes.Structure):
+    _fields_ = [("pad", _vp * MAX_PEERS), ("counter", _vp), ("rank", _c_int), ("n", _c_int)]
 
 
 class RowsC(ctypes.Structure):
@@ -64,9 +82,16 @@ SIGNATURES = {
     "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
     "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
     "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
+    "parm_dispatch_rows_peer": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                         ctypes.POINTER(SlotViewC), _vp, ctypes.POINTER(IntFanC), _vp]),
+    "parm_combine_fwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
+                                      ctypes.POINTER(RowFanC), _c_ll, _vp]),
+    "parm_dispatch_bwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
+                                       ctypes.POINTER(RowFanC), _c_ll, _vp]),
+    "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _vp]),
 }
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class ParmError(RuntimeError):
@@ -103,7 +128,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
 
 
 # Kernel launches each entry point issues on success (bench.py's gpu_launches).
-LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2}
+LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2, "parm_gate_slots": 2, "parm_dispatch_rows_peer": 2}
 launch_count = 0
 
 

@@ -32,6 +32,21 @@ int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const vo
                  long long, cudaStream_t);
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
 int moe_gemm(const parm_gemm_desc&, cudaStream_t);
+int dispatch_rows_peer(const void*, long long, const int*, const float*, int, int, int, int, int, int,
+                       const SlotView&, const int*, const IntFan*, cudaStream_t);
+int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, int, int, const RowFan&, long long,
+                    cudaStream_t);
+int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
+                     const RowFan&, long long, cudaStream_t);
+int peer_barrier(const PeerSignal&, cudaStream_t);
+
+template <class A, class B>
+static A abi_cast(const B* v) {
+    static_assert(sizeof(A) == sizeof(B), "C ABI struct layout mismatch");
+    A a;
+    std::memcpy(&a, v, sizeof(a));
+    return a;
+}
 
 static SlotView to_view(const parm_slot_view* v) {
     SlotView s;
@@ -114,6 +129,48 @@ int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, i
                     size_t workspace_bytes, float* dwg, int accumulate, void* stream) {
     return parm::gate_wgrad(x, ldx, dlogits, n, M, E, reinterpret_cast<float*>(workspace), workspace_bytes, dwg,
                             accumulate, S(stream));
+}
+
+int parm_dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E,
+                            int cap, int slot_lo, int slots_out, int M, const parm_slot_view* dst, const int* fill,
+                            const parm_int_fan* fill_dst, void* stream) {
+    if (!dst) {
+        parm::set_error("dispatch_rows_peer: null destination view");
+        return 1;
+    }
+    parm::IntFan fan{};
+    if (fill_dst) fan = parm::abi_cast<parm::IntFan>(fill_dst);
+    return parm::dispatch_rows_peer(x, ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, to_view(dst), fill,
+                                    fill_dst ? &fan : nullptr, S(stream));
+}
+
+int parm_combine_fwd_fan(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
+                         int n, int k, int M, const parm_row_fan* out, long long ldo, void* stream) {
+    if (!y || !out) {
+        parm::set_error("combine_fwd: null slot view or output fan");
+        return 1;
+    }
+    return parm::combine_fwd_fan(to_view(y), expert_idx, slot_idx, combine_w, n, k, M,
+                                 parm::abi_cast<parm::RowFan>(out), ldo, S(stream));
+}
+
+int parm_dispatch_bwd_fan(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
+                          const void* wg, int n, int k, int E, int M, const parm_row_fan* dx, long long ldx,
+                          void* stream) {
+    if (!dr || !dx) {
+        parm::set_error("dispatch_bwd: null slot view or output fan");
+        return 1;
+    }
+    return parm::dispatch_bwd_fan(to_view(dr), expert_idx, slot_idx, dlogits, wg, n, k, E, M,
+                                  parm::abi_cast<parm::RowFan>(dx), ldx, S(stream));
+}
+
+int parm_peer_barrier(const parm_peer_signal* sig, void* stream) {
+    if (!sig) {
+        parm::set_error("peer_barrier: null signal descriptor");
+        return 1;
+    }
+    return parm::peer_barrier(parm::abi_cast<parm::PeerSignal>(sig), S(stream));
 }
 
 int parm_gemm(const parm_gemm_desc* desc, void* stream) {

@@ -78,26 +78,63 @@ __device__ __forceinline__ Vec8 f32_to_vec8(const float* f) {
 //       + (s / slot_div) * stride_shi + (s % slot_div) * stride_slo
 // (strides in elements).  Covers every receive layout the three schedules
 // produce; n_p partials are summed in p order.
+constexpr int kMaxPeers = 8;
+
 struct SlotView {
     const bf16* ptr;
     int e_local;
     int n_p;
     int slot_div;
-    int pad_;
+    int n_peer;                  // 0: local view.  > 0: rows live in peers' buffers (NVLink-mapped)
     long long stride_ep;
     long long stride_i;
     long long stride_p;
     long long stride_shi;
     long long stride_slo;
+    const bf16* peer[kMaxPeers]; // n_peer > 0: partial (ep, p) is peer[ep * peer_ep + p * peer_p]
+    int peer_ep;                 //   (+ the in-buffer offset of expert i_e, slot s); stride_ep/stride_p unused
+    int peer_p;
 };
 
-__device__ __forceinline__ long long slot_offset(const SlotView& v, int e, int s, int p) {
-    int ep = e / v.e_local;
-    int i = e - ep * v.e_local;
-    int shi = s / v.slot_div;
-    int slo = s - shi * v.slot_div;
-    return (long long)ep * v.stride_ep + (long long)i * v.stride_i + (long long)p * v.stride_p +
-           (long long)shi * v.stride_shi + (long long)slo * v.stride_slo;
+// In-buffer offset of (expert e, slot s) excluding the block / partial terms.
+__device__ __forceinline__ long long slot_inbuf(const SlotView& v, int e, int s, int& ep) {
+    ep = e / v.e_local;
+    const int i = e - ep * v.e_local;
+    const int shi = s / v.slot_div;
+    const int slo = s - shi * v.slot_div;
+    return (long long)i * v.stride_i + (long long)shi * v.stride_shi + (long long)slo * v.stride_slo;
 }
+
+// Base of partial p of block ep (local: strides; peer view: that rank's mapped buffer).
+__device__ __forceinline__ const bf16* slot_base(const SlotView& v, int ep, int p) {
+    return v.n_peer ? v.peer[ep * v.peer_ep + p * v.peer_p]
+                    : v.ptr + (long long)ep * v.stride_ep + (long long)p * v.stride_p;
+}
+
+__device__ __forceinline__ const bf16* slot_row(const SlotView& v, int e, int s, int p) {
+    int ep;
+    const long long off = slot_inbuf(v, e, s, ep);
+    return slot_base(v, ep, p) + off;
+}
+
+// Output rows fanned out to up to kMaxPeers buffers with the same layout (a
+// row written to every MP peer = the MP AllGather fused into the producer).
+struct RowFan {
+    bf16* ptr[kMaxPeers];
+    int n;
+    int pad_;
+};
+
+// Per-destination int tables (fill counts), indexed like SlotView::peer.
+struct IntFan {
+    int* ptr[kMaxPeers];
+};
+
+struct PeerSignal {
+    void* pad[kMaxPeers];
+    void* counter;
+    int rank;
+    int n;
+};
 
 }  // namespace parm

@@ -46,11 +46,15 @@ __device__ __forceinline__ int4 ldg16(const bf16* p) { return __ldg(reinterpret_
 
 // ------------------------------------------------------------------ dispatch (gather into slots)
 // Four rows per warp iteration: their slot_src entries, then their token rows,
-// are loaded together.
+// are loaded together.  PEER: each row is stored straight into the receive
+// buffers of its N_ESP holders on other GPUs (NVLink stores through the
+// symmetric-memory mapping) -- the EP&ESP dispatch AlltoAll with its dump,
+// fused into the gather (collectives.py:256-283).
+template <bool PEER>
 __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
     const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
     int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
-    long long out_stride_s) {
+    long long out_stride_s, const __grid_constant__ SlotView dstv) {
     constexpr int R = 4;
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
@@ -59,6 +63,8 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
     for (long long r0 = warp_global * R; r0 < rows; r0 += num_warps * R) {
         int src[R];
         bf16* dst[R];
+        int dep[R];
+        long long doff[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             const long long r = r0 + q;
@@ -68,7 +74,15 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
                 const int sp = (int)(r - (long long)e * slots_out);
                 const int s = slot_lo + sp;
                 src[q] = (s < cap) ? __ldg(slot_src + (long long)e * cap + s) : -1;
-                dst[q] = out + (long long)e * out_stride_e + (long long)sp * out_stride_s;
+                if (PEER) {
+                    int ep;
+                    const long long off = slot_inbuf(dstv, e, sp, ep);
+                    dst[q] = const_cast<bf16*>(slot_base(dstv, ep, 0)) + off;
+                    dep[q] = ep;
+                    doff[q] = off;
+                } else {
+                    dst[q] = out + (long long)e * out_stride_e + (long long)sp * out_stride_s;
+                }
             }
         }
         float w[R];
@@ -91,6 +105,7 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
                 for (int i = 0; i < kChunks; ++i) {
                     const int c = g0 + lane * 8 + i * 256;
                     if (c >= M) continue;
+                    int4 o = v[q][i];
                     if (scale != nullptr && src[q] >= 0) {
                         Vec8 t;
                         *reinterpret_cast<int4*>(&t) = v[q][i];
@@ -98,9 +113,14 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
                         vec8_to_f32(t, f);
 #pragma unroll
                         for (int u = 0; u < 8; ++u) f[u] *= w[q];
-                        st_vec8(dst[q] + c, f32_to_vec8(f));
+                        const Vec8 r8 = f32_to_vec8(f);
+                        o = *reinterpret_cast<const int4*>(&r8);
+                    }
+                    if (PEER) {
+                        for (int pp = 0; pp < dstv.n_p; ++pp)
+                            *reinterpret_cast<int4*>(const_cast<bf16*>(slot_base(dstv, dep[q], pp)) + doff[q] + c) = o;
                     } else {
-                        *reinterpret_cast<int4*>(dst[q] + c) = v[q][i];
+                        *reinterpret_cast<int4*>(dst[q] + c) = o;
                     }
                 }
             }
@@ -115,7 +135,8 @@ struct Picks {
     int sl[KT];
     int ex[KT];
     float w[KT];
-    long long off[KT];   // element offset of the pick's row in partial 0 of the view (slot_offset once per token)
+    int ep[KT];          // expert-parallel block of the pick's expert
+    long long off[KT];   // in-buffer offset of the pick's row (slot_inbuf, once per token)
     __device__ __forceinline__ void load(long long t, int k, const int* __restrict__ slot_idx,
                                          const int* __restrict__ expert_idx, const float* __restrict__ cw,
                                          const SlotView& v) {
@@ -124,7 +145,8 @@ struct Picks {
             sl[j] = (j < k) ? __ldg(slot_idx + t * k + j) : -1;
             ex[j] = (sl[j] >= 0) ? __ldg(expert_idx + t * k + j) : 0;
             w[j] = (cw != nullptr && sl[j] >= 0) ? __ldg(cw + t * k + j) : 0.0f;
-            off[j] = sl[j] >= 0 ? slot_offset(v, ex[j], sl[j], 0) : 0;
+            off[j] = sl[j] >= 0 ? slot_inbuf(v, ex[j], sl[j], ep[j]) : 0;
+            if (sl[j] < 0) ep[j] = 0;
         }
     }
 };
@@ -135,7 +157,7 @@ __device__ __forceinline__ void load_picks(const SlotView& v, const Picks<KT>& p
                                            int4 (&buf)[KT][kChunks]) {
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
-        const bf16* row = v.ptr + pk.off[j] + (long long)p * v.stride_p;
+        const bf16* row = slot_base(v, pk.ep[j], p) + pk.off[j];
 #pragma unroll
         for (int i = 0; i < kChunks; ++i) {
             const int c = g0 + lane * 8 + i * 256;
@@ -153,13 +175,15 @@ __device__ __forceinline__ void fma_bf16x8(float* acc, float w, const int4& v) {
     for (int u = 0; u < 8; ++u) acc[u] = fmaf(w, f[u], acc[u]);
 }
 
-// 256 threads, <= 85 registers: three CTAs (24 warps) per SM keep enough row
-// loads in flight; the per-group accumulators are the only long-lived state.
+// 256 threads, <= 128 registers, a resident grid of two CTAs per SM looping over
+// tokens; the per-group accumulators are the only long-lived state.
 template <int KT>
-__global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_kernel(const SlotView y, const int* __restrict__ expert_idx,
+__global__ void __launch_bounds__(kRowThreads, 2) combine_fwd_kernel(const __grid_constant__ SlotView y,
+                                                                      const int* __restrict__ expert_idx,
                                                                       const int* __restrict__ slot_idx,
                                                                       const float* __restrict__ combine_w, int n, int k,
-                                                                      int M, bf16* __restrict__ out, long long ldo) {
+                                                                      int M, const __grid_constant__ RowFan out,
+                                                                      long long ldo) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -185,15 +209,17 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_kernel(const SlotV
 #pragma unroll
             for (int i = 0; i < kChunks; ++i) {
                 const int c = g0 + lane * 8 + i * 256;
-                if (c < M) st_vec8(out + t * ldo + c, f32_to_vec8(acc[i]));
+                if (c >= M) continue;
+                const Vec8 v8 = f32_to_vec8(acc[i]);
+                for (int f = 0; f < out.n; ++f) st_vec8(out.ptr[f] + t * ldo + c, v8);
             }
         }
     }
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16* __restrict__ dout, long long ldd,
-                                                                      const SlotView y, const int* __restrict__ expert_idx,
+__global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16* __restrict__ dout, long long ldd,
+                                                                      const __grid_constant__ SlotView y, const int* __restrict__ expert_idx,
                                                                       const int* __restrict__ slot_idx,
                                                                       const float* __restrict__ probs, int n, int k,
                                                                       int E, int M, float* __restrict__ dlogits) {
@@ -261,25 +287,28 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_bwd_kernel(const bf16*
 // weights as stored) feeds all four tokens -- the gate term's weight traffic
 // is 1/TB of a token-per-warp loop's.
 template <int KT, int TB, int EMAX>   // EMAX > 0: E <= EMAX, logit gradients kept in registers
-__global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const SlotView dr,
+__global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __grid_constant__ SlotView dr,
                                                                        const int* __restrict__ expert_idx,
                                                                        const int* __restrict__ slot_idx,
                                                                        const float* __restrict__ dlogits,
                                                                        const bf16* __restrict__ wgT, int n, int k,
-                                                                       int E, int M, bf16* __restrict__ dx,
+                                                                       int E, int M,
+                                                                       const __grid_constant__ RowFan dx,
                                                                        long long ldx) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     for (long long t0 = warp_global * TB; t0 < n; t0 += num_warps * TB) {
-        long long off[TB][KT];   // row offset in partial 0, -1 = dropped / no token
+        long long off[TB][KT];   // in-buffer row offset, -1 = dropped / no token
+        int epk[TB][KT];
 #pragma unroll
         for (int b = 0; b < TB; ++b)
 #pragma unroll
             for (int j = 0; j < KT; ++j) {
                 const long long t = t0 + b;
                 const int sl = (t < n && j < k) ? __ldg(slot_idx + t * k + j) : -1;
-                off[b][j] = sl >= 0 ? slot_offset(dr, __ldg(expert_idx + t * k + j), sl, 0) : -1;
+                epk[b][j] = 0;
+                off[b][j] = sl >= 0 ? slot_inbuf(dr, __ldg(expert_idx + t * k + j), sl, epk[b][j]) : -1;
             }
         float dl[TB][EMAX > 0 ? EMAX : 1];   // gate-logit gradients, held across the column groups when E <= EMAX
         if (EMAX > 0) {
@@ -303,7 +332,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const Slot
                 for (int b = 0; b < TB; ++b)
 #pragma unroll
                     for (int j = 0; j < KT; ++j)
-                        buf[b][j] = off[b][j] >= 0 ? ldg16(dr.ptr + off[b][j] + (long long)p * dr.stride_p + c)
+                        buf[b][j] = off[b][j] >= 0 ? ldg16(slot_base(dr, epk[b][j], p) + off[b][j] + c)
                                                    : make_int4(0, 0, 0, 0);
 #pragma unroll
                 for (int b = 0; b < TB; ++b)
@@ -332,13 +361,17 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const Slot
                 }
             }
 #pragma unroll
-            for (int b = 0; b < TB; ++b)
-                if (t0 + b < n) st_vec8(dx + (t0 + b) * ldx + c, f32_to_vec8(acc[b]));
+            for (int b = 0; b < TB; ++b) {
+                if (t0 + b >= n) continue;
+                const Vec8 v8 = f32_to_vec8(acc[b]);
+                for (int f = 0; f < dx.n; ++f) st_vec8(dx.ptr[f] + (t0 + b) * ldx + c, v8);
+            }
         }
     }
 }
 
-__global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const SlotView y, int E, int slots, int M,
+__global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const __grid_constant__ SlotView y, int E, int slots,
+                                                                  int M,
                                                                   bf16* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
@@ -349,7 +382,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const SlotView 
         pk.ex[0] = (int)(r / slots);
         pk.sl[0] = (int)(r - (long long)pk.ex[0] * slots);
         pk.w[0] = 1.0f;
-        pk.off[0] = slot_offset(y, pk.ex[0], pk.sl[0], 0);
+        pk.off[0] = slot_inbuf(y, pk.ex[0], pk.sl[0], pk.ep[0]);
         for (int g0 = 0; g0 < M; g0 += kGroupCols) {
             float acc[kChunks][8];
 #pragma unroll
@@ -373,8 +406,15 @@ __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const SlotView 
 
 // ------------------------------------------------------------------ host
 static int check_view(const SlotView& v, int M, const char* what) {
-    PARM_CHECK_ARG(v.ptr != nullptr, "%s: null slot view", what);
-    PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0, "%s: slot view base not 16-byte aligned", what);
+    PARM_CHECK_ARG(v.n_peer >= 0 && v.n_peer <= kMaxPeers, "%s: bad peer count %d", what, v.n_peer);
+    if (v.n_peer == 0) {
+        PARM_CHECK_ARG(v.ptr != nullptr, "%s: null slot view", what);
+        PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0, "%s: slot view base not 16-byte aligned", what);
+    } else {
+        for (int i = 0; i < v.n_peer; ++i)
+            PARM_CHECK_ARG(v.peer[i] != nullptr && (reinterpret_cast<uintptr_t>(v.peer[i]) & 15) == 0,
+                           "%s: peer buffer %d null or not 16-byte aligned", what, i);
+    }
     PARM_CHECK_ARG(v.e_local >= 1 && v.n_p >= 1 && v.slot_div >= 1, "%s: bad slot view", what);
     PARM_CHECK_ARG(M % 8 == 0, "%s: embed %d must be a multiple of 8", what, M);
     return 0;
@@ -387,23 +427,114 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
                    "dispatch_rows: rows must be 16-byte aligned (M=%d)", M);
     const long long rows = (long long)E * slots_out;
     if (rows == 0) return 0;
-    dispatch_rows_kernel<<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
+    SlotView none{};
+    dispatch_rows_kernel<false><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
         reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
-        reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s);
+        reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none);
     PARM_CHECK_LAUNCH("dispatch_rows");
     return 0;
 }
 
+// Per-segment fill counts of this source's slot range, stored into every holder's table.
+__global__ void fan_fill_kernel(const int* __restrict__ fill, int E, int slot_lo, int slots_out,
+                                const __grid_constant__ SlotView dstv, const __grid_constant__ IntFan fan) {
+    const int e = threadIdx.x;
+    if (e >= E) return;
+    int c = __ldg(fill + e) - slot_lo;
+    c = c < 0 ? 0 : (c > slots_out ? slots_out : c);
+    const int ep = e / dstv.e_local, i = e - ep * dstv.e_local;
+    for (int p = 0; p < dstv.n_p; ++p) fan.ptr[ep * dstv.peer_ep + p * dstv.peer_p][i] = c;
+}
+
+int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
+                       int slot_lo, int slots_out, int M, const SlotView& dst, const int* fill, const IntFan* fill_dst,
+                       cudaStream_t s) {
+    PARM_CHECK_ARG(dst.n_peer >= 1 && dst.n_peer <= kMaxPeers, "dispatch_rows_peer: destination must be a peer view");
+    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && dst.stride_i % 8 == 0 && dst.stride_slo % 8 == 0,
+                   "dispatch_rows_peer: rows must be 16-byte aligned (M=%d)", M);
+    PARM_CHECK_ARG(E <= 1024, "dispatch_rows_peer: too many experts");
+    const long long rows = (long long)E * slots_out;
+    if (rows > 0) {
+        dispatch_rows_kernel<true><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
+            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
+            dst);
+        PARM_CHECK_LAUNCH("dispatch_rows_peer");
+    }
+    if (fill != nullptr && fill_dst != nullptr) {
+        fan_fill_kernel<<<1, ((E + 31) / 32) * 32, 0, s>>>(fill, E, slot_lo, slots_out, dst, *fill_dst);
+        PARM_CHECK_LAUNCH("dispatch_rows_peer(fill)");
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ peer barrier
+// Every rank stores the next epoch into slot [rank] of every peer's signal pad
+// (release, system scope, after a system fence that publishes this rank's
+// earlier peer stores), then waits until every peer's epoch has reached its
+// own pad.  The epoch lives in device memory, so a replayed CUDA graph
+// advances it like an eager launch.  A watchdog traps instead of hanging.
+__global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
+    __shared__ unsigned epoch;
+    if (threadIdx.x == 0) {
+        unsigned* cnt = reinterpret_cast<unsigned*>(sig.counter);
+        epoch = *cnt + 1u;
+        *cnt = epoch;
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (j < sig.n) {
+        __threadfence_system();
+        unsigned* slot = reinterpret_cast<unsigned*>(sig.pad[j]) + sig.rank;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
+        const unsigned* mine = reinterpret_cast<const unsigned*>(sig.pad[sig.rank]) + j;
+        const long long t0 = clock64();
+        while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+            if ((int)(v - epoch) >= 0) break;
+            if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");   // ~4 s: a peer never arrived
+        }
+    }
+    __syncthreads();
+}
+
+int peer_barrier(const PeerSignal& sig, cudaStream_t s) {
+    PARM_CHECK_ARG(sig.n >= 1 && sig.n <= kMaxPeers && sig.rank >= 0 && sig.rank < sig.n,
+                   "peer_barrier: bad rank %d of %d", sig.rank, sig.n);
+    PARM_CHECK_ARG(sig.counter != nullptr, "peer_barrier: null epoch counter");
+    peer_barrier_kernel<<<1, 32, 0, s>>>(sig);
+    PARM_CHECK_LAUNCH("peer_barrier");
+    return 0;
+}
+
+int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, int, int, const RowFan&, long long,
+                    cudaStream_t);
+int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
+                     const RowFan&, long long, cudaStream_t);
+
+static RowFan one_fan(void* p) {
+    RowFan f{};
+    f.ptr[0] = reinterpret_cast<bf16*>(p);
+    f.n = 1;
+    return f;
+}
+
 int combine_fwd(const SlotView& y, const int* expert_idx, const int* slot_idx, const float* combine_w, int n, int k,
                 int M, void* out, long long ldo, cudaStream_t s) {
+    PARM_CHECK_ARG(out != nullptr, "combine_fwd: null output");
+    return combine_fwd_fan(y, expert_idx, slot_idx, combine_w, n, k, M, one_fan(out), ldo, s);
+}
+
+int combine_fwd_fan(const SlotView& y, const int* expert_idx, const int* slot_idx, const float* combine_w, int n,
+                    int k, int M, const RowFan& O, long long ldo, cudaStream_t s) {
     if (int rc = check_view(y, M, "combine_fwd")) return rc;
     PARM_CHECK_ARG(k >= 1 && k <= 8, "combine_fwd: top_k must be in [1, 8]");
+    PARM_CHECK_ARG(O.n >= 1 && O.n <= kMaxPeers, "combine_fwd: output fan of %d buffers", O.n);
     if (n == 0) return 0;
-    auto O = reinterpret_cast<bf16*>(out);
     if (k <= 2)
-        combine_fwd_kernel<2><<<resident_grid(n, 3), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        combine_fwd_kernel<2><<<resident_grid(n, 2), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     else
-        combine_fwd_kernel<8><<<resident_grid(n, 3), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        combine_fwd_kernel<8><<<resident_grid(n, 2), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     PARM_CHECK_LAUNCH("combine_fwd");
     return 0;
 }
@@ -415,10 +546,10 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     if (n == 0) return 0;
     auto D = reinterpret_cast<const bf16*>(dout);
     if (k <= 2)
-        combine_bwd_kernel<2><<<resident_grid(n, 3), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        combine_bwd_kernel<2><<<resident_grid(n, 2), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     else
-        combine_bwd_kernel<8><<<resident_grid(n, 3), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        combine_bwd_kernel<8><<<resident_grid(n, 2), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
@@ -426,12 +557,18 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
 
 int dispatch_bwd(const SlotView& dr, const int* expert_idx, const int* slot_idx, const float* dlogits, const void* wg,
                  int n, int k, int E, int M, void* dx, long long ldx, cudaStream_t s) {
+    PARM_CHECK_ARG(dx != nullptr, "dispatch_bwd: null output");
+    return dispatch_bwd_fan(dr, expert_idx, slot_idx, dlogits, wg, n, k, E, M, one_fan(dx), ldx, s);
+}
+
+int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
+                     const void* wg, int n, int k, int E, int M, const RowFan& DX, long long ldx, cudaStream_t s) {
     if (int rc = check_view(dr, M, "dispatch_bwd")) return rc;
+    PARM_CHECK_ARG(DX.n >= 1 && DX.n <= kMaxPeers, "dispatch_bwd: output fan of %d buffers", DX.n);
     PARM_CHECK_ARG(E <= 32 && k <= 8, "dispatch_bwd: E<=32 and k<=8 required");
     PARM_CHECK_ARG(dlogits == nullptr || wg != nullptr, "dispatch_bwd: dlogits needs gate weights");
     if (n == 0) return 0;
     auto W = reinterpret_cast<const bf16*>(wg);
-    auto DX = reinterpret_cast<bf16*>(dx);
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "dispatch_bwd: rows must be 16-byte aligned (M=%d)", M);
     if (k <= 2 && E <= 8)
         dispatch_bwd_kernel<2, 4, 8><<<row_grid((n + 3) / 4), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits,
@@ -448,6 +585,7 @@ int dispatch_bwd(const SlotView& dr, const int* expert_idx, const int* slot_idx,
 
 int esp_sum(const SlotView& y, int E, int slots, int M, void* out, cudaStream_t s) {
     if (int rc = check_view(y, M, "esp_sum")) return rc;
+    PARM_CHECK_ARG(y.n_peer == 0, "esp_sum: local views only");
     const long long rows = (long long)E * slots;
     if (rows == 0) return 0;
     esp_sum_kernel<<<row_grid(rows), kRowThreads, 0, s>>>(y, E, slots, M, reinterpret_cast<bf16*>(out));

@@ -47,11 +47,37 @@ class SlotView:
     stride_shi: int = 0
     stride_slo: int = 0
     offset: int = 0              # element offset added to base
+    peers: tuple | None = None   # peer view: per-rank buffer addresses (already offset), indexed ep*peer_ep + p*peer_p
+    peer_ep: int = 0
+    peer_p: int = 0
 
     def c(self) -> _lib.SlotViewC:
-        _need(self.base, torch.bfloat16, "slot view base")
-        return _lib.SlotViewC(self.base.data_ptr() + 2 * self.offset, self.e_local, self.n_p, self.slot_div, 0,
-                              self.stride_ep, self.stride_i, self.stride_p, self.stride_shi, self.stride_slo)
+        v = _lib.SlotViewC()
+        if self.peers is None:
+            _need(self.base, torch.bfloat16, "slot view base")
+            v.ptr = self.base.data_ptr() + 2 * self.offset
+        else:
+            if not 1 <= len(self.peers) <= _lib.MAX_PEERS:
+                raise ValueError(f"peer view over {len(self.peers)} ranks (max {_lib.MAX_PEERS})")
+            v.n_peer = len(self.peers)
+            for i, a in enumerate(self.peers):
+                v.peer[i] = a
+            v.peer_ep, v.peer_p = self.peer_ep, self.peer_p
+        v.e_local, v.n_p, v.slot_div = self.e_local, self.n_p, self.slot_div
+        v.stride_ep, v.stride_i, v.stride_p = self.stride_ep, self.stride_i, self.stride_p
+        v.stride_shi, v.stride_slo = self.stride_shi, self.stride_slo
+        return v
+
+
+def _fan(ptrs, cls=None):
+    f = (cls or _lib.RowFanC)()
+    if not 1 <= len(ptrs) <= _lib.MAX_PEERS:
+        raise ValueError(f"fan over {len(ptrs)} buffers (max {_lib.MAX_PEERS})")
+    for i, a in enumerate(ptrs):
+        f.ptr[i] = a
+    if hasattr(f, "n"):
+        f.n = len(ptrs)
+    return f
 
 
 def plain_view(t: torch.Tensor, e_local: int | None = None) -> SlotView:
@@ -127,6 +153,52 @@ def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tenso
     v = view.c()
     _lib.call("parm_dispatch_bwd", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(), _ptr(dlogits),
               _ptr(wg), n, k, E, M, dx.data_ptr(), dx.stride(0), _stream())
+
+
+def dispatch_rows_peer(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, slots_out: int,
+                       dst: SlotView, fill: torch.Tensor | None = None, fill_fan: list | None = None,
+                       scale: torch.Tensor | None = None) -> None:
+    """Dispatch fused with the EP&ESP AlltoAll: slot rows [slot_lo, slot_lo+slots_out) stored
+    into the holders' receive buffers through the peer view ``dst`` (n_p = N_ESP dump copies);
+    with ``fill`` the per-segment fill counts go to ``fill_fan`` (int32 addresses, view indexing)."""
+    _need(x, torch.bfloat16, "rows source")
+    E = slot_src.shape[0]
+    v = dst.c()
+    ff = _fan(fill_fan, _lib.IntFanC) if fill_fan is not None else None
+    _lib.call("parm_dispatch_rows_peer", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
+              slot_lo, slots_out, x.shape[1], ctypes.byref(v), _ptr(fill), None if ff is None else ctypes.byref(ff),
+              _stream())
+
+
+def combine_fwd_fan(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,
+                    out_ptrs: list, n: int, M: int, ldo: int) -> None:
+    """combine_fwd writing every output row to each address in ``out_ptrs`` (fused AllGather)."""
+    k = expert_idx.shape[1]
+    v = view.c()
+    f = _fan(out_ptrs)
+    _lib.call("parm_combine_fwd_fan", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(),
+              combine_w.data_ptr(), n, k, M, ctypes.byref(f), ldo, _stream())
+
+
+def dispatch_bwd_fan(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, dlogits: torch.Tensor | None,
+                     wg: torch.Tensor | None, E: int, dx_ptrs: list, n: int, M: int, ldx: int) -> None:
+    if wg is not None:
+        _need(wg, torch.bfloat16, "gate weights (bf16, transposed (E, M))")
+    k = expert_idx.shape[1]
+    v = view.c()
+    f = _fan(dx_ptrs)
+    _lib.call("parm_dispatch_bwd_fan", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(), _ptr(dlogits),
+              _ptr(wg), n, k, E, M, ctypes.byref(f), ldx, _stream())
+
+
+def peer_barrier(pads: list, counter: torch.Tensor, rank: int) -> None:
+    """Device-side barrier of len(pads) ranks (signal-pad addresses of every rank, this rank's epoch counter)."""
+    s = _lib.PeerSignalC()
+    for i, a in enumerate(pads):
+        s.pad[i] = a
+    s.counter = counter.data_ptr()
+    s.rank, s.n = rank, len(pads)
+    _lib.call("parm_peer_barrier", ctypes.byref(s), _stream())
 
 
 def esp_sum(view: SlotView, out: torch.Tensor) -> None:

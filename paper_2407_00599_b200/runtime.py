@@ -47,7 +47,7 @@ import torch
 
 from . import kernels as K
 from .config import MoEConfig, ParallelLayout, check_compatible, derive_capacity, group_members
-from .world import Msg, World, make_world
+from .world import Msg, PeerWorld, World, make_world
 
 SCHEDULES = ("baseline", "s1", "s2")
 
@@ -162,6 +162,8 @@ class MoELayer:
         self.d = Dims.of(cfg, layout)
         d = self.d
         self.saa_phased = _saa_phased(layout)
+        # S1 over NVLink peer memory (fused dispatch/return/AllGather) when the world maps peers
+        self.peer = (isinstance(self.world, PeerWorld) and d.P > 1 and os.environ.get("PARM_PEER", "1") != "0")
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -233,7 +235,14 @@ class MoELayer:
         bf = dict(dtype=torch.bfloat16, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
         el = d.e_local
-        b: dict = {"out": torch.zeros(d.n, d.Mp, **bf), "dx": torch.zeros(d.n, d.Mp, **bf)}
+        peer = self.peer and schedule == "s1"
+        W = self.world
+        b: dict = {}
+        if peer:     # symmetric buffers: every MP peer writes its slice rows into them (fused AllGather)
+            b["out"], b["out_peers"] = W.sym((d.n, d.Mp))
+            b["dx"], b["dx_peers"] = W.sym((d.n, d.Mp))
+        else:
+            b["out"], b["dx"] = torch.zeros(d.n, d.Mp, **bf), torch.zeros(d.n, d.Mp, **bf)
         if d.M != d.Mp:
             b["x"] = torch.zeros(d.n, d.Mp, **bf)
             b["dout"] = torch.zeros(d.n, d.Mp, **bf)
@@ -245,9 +254,14 @@ class MoELayer:
                 sl = d.n // d.MP
                 b["route"] = Routing.alloc(sl, d.k, d.E, q, dev, token_offset=self.layout.mp_pos(r) * sl)
             b["q"] = q
-            b["send"] = torch.zeros(d.E, q, d.Mp, **bf)
-            b["dsend"] = torch.zeros(d.E, q, d.Mp, **bf)
-            if d.P == 1:     # no exchange: the slot tensors ARE the GEMM operands
+            if not peer:
+                b["send"] = torch.zeros(d.E, q, d.Mp, **bf)
+                b["dsend"] = torch.zeros(d.E, q, d.Mp, **bf)
+            if peer:         # holders' receive buffers, written by the sources' dispatch kernels
+                b["recv"], b["recv_peers"] = W.sym((d.P, 1, el, q, d.Mp))
+                b["dyrecv"], b["dyrecv_peers"] = W.sym((d.P, 1, el, q, d.Mp))
+                b["fill_in"], b["fill_in_peers"] = W.sym((d.P, 1, el), torch.int32)
+            elif d.P == 1:   # no exchange: the slot tensors ARE the GEMM operands
                 b["recv"] = b["send"].view(1, 1, d.E, q, d.Mp)
                 b["dyrecv"] = b["dsend"].view(1, 1, d.E, q, d.Mp)
                 b["fill_in"] = b["route"].fill.view(1, 1, d.E)
@@ -271,10 +285,16 @@ class MoELayer:
             b["dg"] = torch.zeros(d.ESP, d.n, d.Mp, **bf)
             shape = (d.EP, d.ESP, el, d.T)
         b["h"] = torch.zeros(*shape, d.Hsp, **bf)
-        b["y"] = torch.zeros(*shape, d.Mp, **bf)
         b["dh"] = torch.zeros(*shape, d.Hsp, **bf)
-        b["dr"] = torch.zeros(*shape, d.Mp, **bf)
-        if schedule == "baseline":
+        if peer:             # expert outputs, gathered by the owners' combine / dispatch-backward kernels
+            b["y"], b["y_peers"] = W.sym((*shape, d.Mp))
+            b["dr"], b["dr_peers"] = W.sym((*shape, d.Mp))
+        else:
+            b["y"] = torch.zeros(*shape, d.Mp, **bf)
+            b["dr"] = torch.zeros(*shape, d.Mp, **bf)
+        if peer:
+            pass
+        elif schedule == "baseline":
             b["ret"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # owner side [holder j][block][i][slot]
             b["dd"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
         elif d.P == 1:
@@ -456,8 +476,81 @@ class MoELayer:
             res[r] = b["dx"][:, :d.M]
         return res
 
+    # ------------------------------------------------------------ S1 over peer memory
+    def _peer_view(self, b: dict, key: str, r: int) -> K.SlotView:
+        """Rows (e, s, p) of source r in the holders' (P, 1, e_local, q, M) buffers `key`:
+        partial p of expert e lives on rank_of(ep_e, p), at that rank's segment [r]."""
+        d, L = self.d, self.layout
+        q, el = b["q"], d.e_local
+        off = 2 * r * el * q * d.Mp
+        pe, pp = (d.ESP, 1) if L.esp_contiguous else (1, d.EP)
+        return K.SlotView(None, e_local=el, n_p=d.ESP, stride_i=q * d.Mp, stride_slo=d.Mp,
+                          peers=tuple(a + off for a in b[key + "_peers"]), peer_ep=pe, peer_p=pp)
+
+    def _mp_fan(self, b: dict, key: str, r: int) -> list[int]:
+        """Row r-slice of every MP peer's (n, M) buffer `key` (the fused MP AllGather)."""
+        d, L = self.d, self.layout
+        off = 2 * L.mp_pos(r) * (d.n // d.MP) * d.Mp
+        return [b[key + "_peers"][m] + off for m in group_members(L, "mp", r)]
+
+    def _fwd_s1_peer(self, xs: dict) -> dict:
+        d, L = self.d, self.layout
+        sl, el = d.n // d.MP, d.e_local
+        for r in self.ranks:
+            s, b = self.st[r], self._plan("s1", r)
+            x = self._input(b, xs[r], "x")
+            m = L.mp_pos(r)
+            xs_ = x[m * sl:(m + 1) * sl]
+            b["xslice"] = xs_
+            rt = b["route"]
+            rt.run(xs_, s.gate64, d.k)
+            K.dispatch_rows_peer(xs_, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "recv", r),
+                                 fill=rt.fill, fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
+        self.world.peer_barrier()                                     # receive buffers complete
+        for r in self.ranks:
+            self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
+        self.world.peer_barrier()                                     # expert outputs complete
+        for r in self.ranks:
+            b = self.st[r].bufs["s1"]
+            rt = b["route"]
+            K.combine_fwd_fan(self._peer_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.combine_w,
+                              self._mp_fan(b, "out", r), sl, d.Mp, d.Mp)
+        self.world.peer_barrier()                                     # every MP slice gathered
+        self._last = "s1"
+        return {r: self.st[r].bufs["s1"]["out"][:, :d.M] for r in self.ranks}
+
+    def _bwd_s1_peer(self, douts: dict) -> dict:
+        d, L = self.d, self.layout
+        sl = d.n // d.MP
+        for r in self.ranks:
+            s, b = self.st[r], self.st[r].bufs["s1"]
+            dout = self._input(b, douts[r], "dout")
+            m = L.mp_pos(r)
+            ds = dout[m * sl:(m + 1) * sl]
+            rt = b["route"]
+            K.combine_bwd(ds, self._peer_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            K.dispatch_rows_peer(ds, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "dyrecv", r),
+                                 scale=rt.combine_w)
+        self.world.peer_barrier()
+        for r in self.ranks:
+            self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
+        self.world.peer_barrier()
+        gins = {}
+        for r in self.ranks:
+            s, b = self.st[r], self.st[r].bufs["s1"]
+            rt = b["route"]
+            K.dispatch_bwd_fan(self._peer_view(b, "dr", r), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+                               self._mp_fan(b, "dx", r), sl, d.Mp, d.Mp)
+            K.gate_wgrad(b["xslice"], b["dlogits"], s.dgate, self._ws_gate)
+            gins[r] = s.dgate
+        self.world.allreduce("mp", gins)                                 # slices gate different tokens
+        self.world.peer_barrier()                                        # every MP slice of dx gathered
+        return {r: self.st[r].bufs["s1"]["dx"][:, :d.M] for r in self.ranks}
+
     # ------------------------------------------------------------ S1
     def _fwd_s1(self, xs: dict) -> dict:
+        if self.peer:
+            return self._fwd_s1_peer(xs)
         d, L = self.d, self.layout
         sl = d.n // d.MP
         for r in self.ranks:
@@ -486,6 +579,8 @@ class MoELayer:
         return {r: self.st[r].bufs["s1"]["out"][:, :d.M] for r in self.ranks}
 
     def _bwd_s1(self, douts: dict) -> dict:
+        if self.peer:
+            return self._bwd_s1_peer(douts)
         d, L = self.d, self.layout
         sl = d.n // d.MP
         for r in self.ranks:

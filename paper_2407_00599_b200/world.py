@@ -197,6 +197,56 @@ class NcclWorld(World):
         self.dist.barrier()
 
 
+class PeerWorld(NcclWorld):
+    """NcclWorld plus NVLink peer memory: buffers allocated as torch symmetric
+    memory are mapped into every rank of the box, so the permute kernels store
+    dispatch rows straight into the holders' receive buffers and gather expert
+    outputs straight from them (the schedules' AlltoAlls and MP AllGathers fused
+    into the kernels, DESIGN.md §(e)).  Ordering is a device-side barrier over
+    the symmetric signal pads (``parm_peer_barrier``, one tiny kernel, graph-
+    capturable).  NCCL stays for the small gate-gradient AllReduce and for the
+    baseline schedule (the DeepSpeed-ordered reference stays on NCCL)."""
+
+    PAD_SLOT = 2048          # u32 index of this runtime's barrier slots inside each signal pad
+
+    def __init__(self, layout: ParallelLayout, device: torch.device | str | None = None):
+        super().__init__(layout, device)
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if layout.world_size > 8:
+            raise ValueError("peer memory is supported within one 8-GPU box")
+        self.symm = symm_mem
+        self.group_name = self.dist.group.WORLD.group_name
+        self._handles = []
+        sync, hs = self._alloc((64,), torch.int32)
+        self._sync = sync
+        pad = hs.get_signal_pad(self.rank, (layout.world_size,), torch.int32, self.PAD_SLOT)
+        pad.zero_()
+        self.pads = [a + 4 * self.PAD_SLOT for a in hs.signal_pad_ptrs]
+        self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+
+    def _alloc(self, shape, dtype):
+        t = self.symm.empty(*shape, dtype=dtype, device=self.device)
+        t.zero_()
+        torch.cuda.synchronize(self.device)      # zeroed before any peer can see (and write) it
+        h = self.symm.rendezvous(t, self.group_name)
+        self._handles.append(h)
+        return t, h
+
+    def sym(self, shape, dtype=torch.bfloat16) -> tuple[torch.Tensor, list[int]]:
+        """A zeroed symmetric buffer and the address of every rank's copy (rank order).
+        Collective: every rank allocates the same buffers in the same order."""
+        t, h = self._alloc(tuple(shape), dtype)
+        return t, [int(a) for a in h.buffer_ptrs]
+
+    def peer_barrier(self) -> None:
+        from . import kernels as K
+
+        K.peer_barrier(self.pads, self.counter, self.rank)
+
+
 def make_world(layout: ParallelLayout, device=None) -> World:
     """NCCL world when torch.distributed spans exactly the layout, else emulate locally."""
     try:
@@ -210,4 +260,4 @@ def make_world(layout: ParallelLayout, device=None) -> World:
     return LocalWorld(layout, device)
 
 
-__all__ = ["Msg", "World", "LocalWorld", "NcclWorld", "make_world", "group_members"]
+__all__ = ["Msg", "World", "LocalWorld", "NcclWorld", "PeerWorld", "make_world", "group_members"]

@@ -32,7 +32,8 @@ def test_header_lists_the_boundary():
     fns = header_functions()
     for required in ("parm_gate_fwd", "parm_gate_slots", "parm_dispatch_rows", "parm_combine_fwd",
                      "parm_combine_bwd", "parm_dispatch_bwd", "parm_esp_sum", "parm_gate_wgrad",
-                     "parm_gemm", "parm_last_error", "parm_abi_version"):
+                     "parm_gemm", "parm_last_error", "parm_abi_version", "parm_dispatch_rows_peer",
+                     "parm_combine_fwd_fan", "parm_dispatch_bwd_fan", "parm_peer_barrier"):
         assert required in fns
 
 
@@ -47,7 +48,10 @@ def test_every_declared_symbol_is_exported_and_typed(lib):
 
 
 def test_struct_layouts_match_header(lib):
-    assert ctypes.sizeof(_lib.SlotViewC) == 8 + 4 * 4 + 5 * 8
+    assert ctypes.sizeof(_lib.SlotViewC) == 8 + 4 * 4 + 5 * 8 + 8 * 8 + 2 * 4
+    assert ctypes.sizeof(_lib.RowFanC) == 8 * 8 + 8
+    assert ctypes.sizeof(_lib.IntFanC) == 8 * 8
+    assert ctypes.sizeof(_lib.PeerSignalC) == 8 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.RowsC) == 8 + 4 * 8
     assert ctypes.sizeof(_lib.GemmDescC) == 12 * 4 + 4 * ctypes.sizeof(_lib.RowsC) + 8
 

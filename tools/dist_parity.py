@@ -2,9 +2,12 @@
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tools/dist_parity.py
 
-Each rank runs MoELayer over NcclWorld (real NCCL collectives over NVLink),
-checks its own routing (bit-exact), forward (max_rel_error <= 1e-2) and
-gradients (normwise <= 2e-2) against the CPU oracle, and rank 0 prints OK.
+Each rank runs MoELayer over NcclWorld (real NCCL collectives over NVLink)
+and over PeerWorld (S1's dispatch/return/AllGather fused into the kernels
+through NVLink symmetric memory), checks its own routing (bit-exact), forward
+(max_rel_error <= 1e-2) and gradients (normwise <= 2e-2) against the CPU
+oracle, replays a captured CUDA-graph step of the peer path against its eager
+result, and rank 0 prints OK.
 With --backend gloo it runs on CPU processes and checks only the message
 plans (the CUDA kernels are not available there).
 """
@@ -25,7 +28,7 @@ sys.path.insert(0, str(ROOT))
 from oracle import moe_oracle as O  # noqa: E402
 from paper_2407_00599_b200.config import MoEConfig, ParallelLayout  # noqa: E402
 from paper_2407_00599_b200.runtime import MoELayer  # noqa: E402
-from paper_2407_00599_b200.world import NcclWorld  # noqa: E402
+from paper_2407_00599_b200.world import NcclWorld, PeerWorld  # noqa: E402
 
 CASES = {
     2: [((2, 64, 128, 256, 8, 2, 1.2), (2, 1, 2), True), ((2, 64, 128, 256, 4, 2, 1.2), (1, 2, 1), True),
@@ -42,50 +45,71 @@ def main() -> int:
     dist.init_process_group("nccl", device_id=dev)
     rank, P = dist.get_rank(), dist.get_world_size()
     failures = []
+    worlds = os.environ.get("PARM_DIST_WORLDS", "nccl,peer").split(",")
     for cfg_t, (mp, ep, esp), contig in CASES.get(P, []):
-        cfg = MoEConfig(*cfg_t)
-        layout = ParallelLayout(mp, ep, esp, P, esp_contiguous=contig)
-        B, L, M, H, E, k, f = cfg_t
-        n = B * L
-        w = O.Weights.generate(M, H, E, seed=5)
-        w = O.Weights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
-        rng = np.random.default_rng(6)
-        G = P // mp
-        inputs = O.round_bf16(rng.normal(size=(G, n, M)))
-        douts = O.round_bf16(rng.normal(size=(G, n, M)))
-        layer = MoELayer(cfg, layout, NcclWorld(layout, dev))
-        layer.load_weights(w)
-        olay = O.Layout(mp, ep, esp, P, esp_contiguous=contig)
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
-        for s in ("baseline", "s1", "s2"):
-            out = layer.forward(s, {rank: t(inputs[rank // mp])})[rank].float().cpu().numpy()
-            rt = layer.routing(rank)
-            si = rt.slot_idx.cpu().numpy()
-            dx = layer.backward({rank: t(douts[rank // mp])})[rank].float().cpu().numpy()
-            gr = {kk: v.float().cpu().numpy() for kk, v in layer.shard_grads(rank).items()}
-            torch.cuda.synchronize()
-            ref, caches, _ = O.schedule_forward(s, n, w, k, f, olay, inputs)
-            rg = O.schedule_backward(s, caches, w, olay, douts)[rank]
-            cch = caches[rank][layout.mp_pos(rank)][0] if (s == "s1") else caches[rank][0][0]
-            tag = f"P={P} {cfg_t} {(mp, ep, esp)} contig={contig} {s} rank {rank}"
-            if not np.array_equal(si, cch.routing.slot_index):
-                failures.append(f"{tag}: routing mismatch")
-            e = O.max_rel_error(out, ref[rank])
-            if e > 1e-2:
-                failures.append(f"{tag}: forward err {e:.3e}")
-            for key, got in (("dx", dx), ("dw1", gr["dw1"]), ("dw2", gr["dw2"]), ("dgate", gr["dgate"])):
-                r = rg[key]
-                ge = np.linalg.norm(got - r) / max(np.linalg.norm(r), 1e-30)
-                if ge > 2e-2:
-                    failures.append(f"{tag}: {key} err {ge:.3e}")
+        for wk in worlds:
+            cfg = MoEConfig(*cfg_t)
+            layout = ParallelLayout(mp, ep, esp, P, esp_contiguous=contig)
+            B, L, M, H, E, k, f = cfg_t
+            n = B * L
+            w = O.Weights.generate(M, H, E, seed=5)
+            w = O.Weights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
+            rng = np.random.default_rng(6)
+            G = P // mp
+            inputs = O.round_bf16(rng.normal(size=(G, n, M)))
+            douts = O.round_bf16(rng.normal(size=(G, n, M)))
+            layer = MoELayer(cfg, layout, (PeerWorld if wk == "peer" else NcclWorld)(layout, dev))
+            layer.load_weights(w)
+            olay = O.Layout(mp, ep, esp, P, esp_contiguous=contig)
+            t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
+            verbose = os.environ.get("PARM_DIST_VERBOSE") == "1"
+            for s in (("baseline", "s1", "s2") if wk == "nccl" else ("s1",)):
+                if verbose:
+                    print(f"rank {rank}: {wk} {cfg_t} {(mp, ep, esp)} {s}", flush=True)
+                out = layer.forward(s, {rank: t(inputs[rank // mp])})[rank].float().cpu().numpy()
+                rt = layer.routing(rank)
+                si = rt.slot_idx.cpu().numpy()
+                dx = layer.backward({rank: t(douts[rank // mp])})[rank].float().cpu().numpy()
+                gr = {kk: v.float().cpu().numpy() for kk, v in layer.shard_grads(rank).items()}
+                torch.cuda.synchronize()
+                ref, caches, _ = O.schedule_forward(s, n, w, k, f, olay, inputs)
+                rg = O.schedule_backward(s, caches, w, olay, douts)[rank]
+                cch = caches[rank][layout.mp_pos(rank)][0] if (s == "s1") else caches[rank][0][0]
+                tag = f"P={P} {wk} {cfg_t} {(mp, ep, esp)} contig={contig} {s} rank {rank}"
+                if not np.array_equal(si, cch.routing.slot_index):
+                    failures.append(f"{tag}: routing mismatch")
+                e = O.max_rel_error(out, ref[rank])
+                if e > 1e-2:
+                    failures.append(f"{tag}: forward err {e:.3e}")
+                for key, got in (("dx", dx), ("dw1", gr["dw1"]), ("dw2", gr["dw2"]), ("dgate", gr["dgate"])):
+                    r = rg[key]
+                    ge = np.linalg.norm(got - r) / max(np.linalg.norm(r), 1e-30)
+                    if ge > 2e-2:
+                        failures.append(f"{tag}: {key} err {ge:.3e}")
+                if verbose:
+                    print(f"rank {rank}: eager done", flush=True)
+                if wk == "peer":      # the captured step (barrier epochs advance on replay) == eager
+                    xin, din = t(inputs[rank // mp]), t(douts[rank // mp])
+                    g = layer.capture_step(s, {rank: xin}, {rank: din}, warmup=1)
+                    for _ in range(3):
+                        g.replay()
+                    torch.cuda.synchronize()
+                    o2 = g.outs[rank].float().cpu().numpy()
+                    d2 = g.dxs[rank].float().cpu().numpy()
+                    if not (np.array_equal(o2, out) and np.array_equal(d2, dx)):
+                        failures.append(f"{tag}: graph replay differs from eager")
     allf = [None] * P
     dist.all_gather_object(allf, failures)
     bad = [x for fs in allf for x in fs]
     if rank == 0:
-        print("\n".join(bad) if bad else f"DIST PARITY OK (P={P}, {len(CASES.get(P, []))} layouts x 3 schedules)")
+        print("\n".join(bad) if bad else f"DIST PARITY OK (P={P}, {len(CASES.get(P, []))} layouts x 3 schedules, "
+                                         f"worlds {worlds})")
     dist.barrier()
-    dist.destroy_process_group()
-    return 1 if bad else 0
+    torch.cuda.synchronize()
+    # symmetric-memory mappings of several PeerWorlds can stall process-group teardown
+    # at interpreter exit; the result is final here, so leave without it
+    sys.stdout.flush()
+    os._exit(1 if bad else 0)
 
 
 if __name__ == "__main__":
