@@ -162,7 +162,7 @@ class MoELayer:
         self.d = Dims.of(cfg, layout)
         d = self.d
         self.saa_phased = _saa_phased(layout)
-        # S1 over NVLink peer memory (fused dispatch/return/AllGather) when the world maps peers
+        # S1/S2 over NVLink peer memory (fused dispatch/return/AllGather) when the world maps peers
         self.peer = (isinstance(self.world, PeerWorld) and d.P > 1 and os.environ.get("PARM_PEER", "1") != "0")
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
@@ -235,10 +235,10 @@ class MoELayer:
         bf = dict(dtype=torch.bfloat16, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
         el = d.e_local
-        peer = self.peer and schedule == "s1"
+        peer = self.peer and schedule in ("s1", "s2")
         W = self.world
         b: dict = {}
-        if peer:     # symmetric buffers: every MP peer writes its slice rows into them (fused AllGather)
+        if peer and schedule == "s1":   # symmetric: every MP peer writes its slice rows into them (fused AllGather)
             b["out"], b["out_peers"] = W.sym((d.n, d.Mp))
             b["dx"], b["dx_peers"] = W.sym((d.n, d.Mp))
         else:
@@ -662,7 +662,67 @@ class MoELayer:
         for h in handles:
             self.world.wait(h)
 
+    def _shard_view(self, b: dict, key: str, r: int) -> K.SlotView:
+        """S2 over peer memory: slot s of expert e (full-block capacity) was dispatched by MP
+        member s // q of r's group, so its row lives on holder rank_of(ep_e, p) in that member's
+        segment; the MP members are consecutive ranks, so the shard index is a plain stride."""
+        d, L = self.d, self.layout
+        q, el = b["q"], d.e_local
+        seg = el * q * d.Mp
+        r0 = group_members(L, "mp", r)[0]
+        pe, pp = (d.ESP, 1) if L.esp_contiguous else (1, d.EP)
+        return K.SlotView(None, e_local=el, n_p=d.ESP, slot_div=q, stride_i=q * d.Mp, stride_shi=seg,
+                          stride_slo=d.Mp, peers=tuple(a + 2 * r0 * seg for a in b[key + "_peers"]),
+                          peer_ep=pe, peer_p=pp)
+
+    def _fwd_s2_peer(self, xs: dict) -> dict:
+        d, L = self.d, self.layout
+        el = d.e_local
+        for r in self.ranks:
+            s, b = self.st[r], self._plan("s2", r)
+            x = self._input(b, xs[r], "x")
+            b["xin"] = x
+            rt = b["route"]
+            rt.run(x, s.gate64, d.k)
+            # this MP rank's slot shard [m q, (m+1) q) straight into the holders (dispatch + A2A + dump)
+            K.dispatch_rows_peer(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
+                                 self._peer_view(b, "recv", r), fill=rt.fill,
+                                 fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
+        self.world.peer_barrier()
+        for r in self.ranks:
+            self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
+        self.world.peer_barrier()
+        for r in self.ranks:      # return A2A + ESP sum + MP AllGather of the slots, fused into the combine
+            b = self.st[r].bufs["s2"]
+            rt = b["route"]
+            K.combine_fwd(self._shard_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
+        self._last = "s2"
+        return {r: self.st[r].bufs["s2"]["out"][:, :d.M] for r in self.ranks}
+
+    def _bwd_s2_peer(self, douts: dict) -> dict:
+        d, L = self.d, self.layout
+        for r in self.ranks:
+            s, b = self.st[r], self.st[r].bufs["s2"]
+            dout = self._input(b, douts[r], "dout")
+            rt = b["route"]
+            K.combine_bwd(dout, self._shard_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            K.dispatch_rows_peer(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
+                                 self._peer_view(b, "dyrecv", r), scale=rt.combine_w)
+        self.world.peer_barrier()
+        for r in self.ranks:
+            self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
+        self.world.peer_barrier()
+        for r in self.ranks:
+            s, b = self.st[r], self.st[r].bufs["s2"]
+            rt = b["route"]
+            K.dispatch_bwd(self._shard_view(b, "dr", r), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+                           b["dx"])
+            K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
+        return {r: self.st[r].bufs["s2"]["dx"][:, :d.M] for r in self.ranks}
+
     def _fwd_s2(self, xs: dict) -> dict:
+        if self.peer:
+            return self._fwd_s2_peer(xs)
         d, L = self.d, self.layout
         for r in self.ranks:
             s, b = self.st[r], self._plan("s2", r)
@@ -688,6 +748,8 @@ class MoELayer:
         return {r: self.st[r].bufs["s2"]["out"][:, :d.M] for r in self.ranks}
 
     def _bwd_s2(self, douts: dict) -> dict:
+        if self.peer:
+            return self._bwd_s2_peer(douts)
         d, L = self.d, self.layout
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s2"]

@@ -246,6 +246,12 @@ class PeerWorld(NcclWorld):
 
         K.peer_barrier(self.pads, self.counter, self.rank)
 
+    def release(self) -> None:
+        """Drop every symmetric buffer but the barrier's (after the layers using them are gone)."""
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        del self._handles[1:]
+
 
 def make_world(layout: ParallelLayout, device=None) -> World:
     """NCCL world when torch.distributed spans exactly the layout, else emulate locally."""

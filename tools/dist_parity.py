@@ -63,7 +63,7 @@ def main() -> int:
             olay = O.Layout(mp, ep, esp, P, esp_contiguous=contig)
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
             verbose = os.environ.get("PARM_DIST_VERBOSE") == "1"
-            for s in (("baseline", "s1", "s2") if wk == "nccl" else ("s1",)):
+            for s in (("baseline", "s1", "s2") if wk == "nccl" else ("s1", "s2")):
                 if verbose:
                     print(f"rank {rank}: {wk} {cfg_t} {(mp, ep, esp)} {s}", flush=True)
                 out = layer.forward(s, {rank: t(inputs[rank // mp])})[rank].float().cpu().numpy()

@@ -27,7 +27,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2407_00599_b200.config import MoEConfig, ParallelLayout, check_compatible  # noqa: E402
 from paper_2407_00599_b200.runtime import MoELayer  # noqa: E402
 from paper_2407_00599_b200.selector import load_profile, select_schedule  # noqa: E402
-from paper_2407_00599_b200.world import NcclWorld  # noqa: E402
+from paper_2407_00599_b200.world import NcclWorld, PeerWorld  # noqa: E402
 
 
 def time_schedule(layer, schedule, x, d, dev, steps=5):
@@ -80,7 +80,8 @@ def main():
     for i, (cfg, lay) in enumerate(pts):
         key = (lay.mp_size, lay.ep_size, lay.esp_size)
         if key not in worlds:                       # one set of communicators per layout
-            worlds[key] = NcclWorld(lay, dev)
+            peer = os.environ.get("PARM_PEER", "0") == "1"
+            worlds[key] = (PeerWorld if peer else NcclWorld)(lay, dev)
         layer = MoELayer(cfg, lay, worlds[key])
         layer.init_random(i)
         gen = torch.Generator(device=dev).manual_seed(100 + rank // lay.mp_size)
@@ -96,6 +97,8 @@ def main():
                      "measured_best": best, "speedup_chosen": t["baseline"] / t[rep.chosen],
                      "speedup_best": t["baseline"] / t[best]})
         del layer
+        if isinstance(worlds[key], PeerWorld):
+            worlds[key].release()
         torch.cuda.empty_cache()
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
@@ -118,7 +121,9 @@ def main():
         with open(args.out.replace(".csv", "_summary.json"), "w") as fh:
             json.dump(summary, fh, indent=1)
     dist.barrier()
-    dist.destroy_process_group()
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    os._exit(0)        # symmetric-memory mappings can stall process-group teardown
 
 
 if __name__ == "__main__":
