@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 6
+#define PARM_ABI_VERSION 7
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -93,10 +93,12 @@ int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* sl
  * is non-null) for the pick in slot s = slot_lo + s', zeros when unfilled or
  * s >= cap.  Writes straight into an AlltoAll send layout.  Replaces the
  * GateOutput.dispatch fill (dataplane.py:101,112) and S2's slot split + pad
- * (dataplane.py:373-378); with scale it is the adjoint of the combine. */
+ * (dataplane.py:373-378); with scale it is the adjoint of the combine.
+ * fill (nullable, per expert): rows s' >= ceil128(clamp(fill[e] - slot_lo, 0,
+ * slots_out)) are left untouched -- no GEMM tile reads them. */
 int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
                        int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
-                       long long out_stride_s, void* stream);
+                       long long out_stride_s, const int* fill, void* stream);
 
 /* Combine: out[t] = sum_j combine_w[t,j] * sum_p Y_p[e_j, s_j] (dropped
  * picks contribute 0).  Fuses fused_combine's local ESP sum

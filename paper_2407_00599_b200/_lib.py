@@ -71,7 +71,7 @@ SIGNATURES = {
     "parm_gate_slots_workspace": (_size, [_c_int, _c_int]),
     "parm_gate_slots": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _size, _vp]),
     "parm_dispatch_rows": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
-                                    _c_ll, _c_ll, _vp]),
+                                    _c_ll, _c_ll, _vp, _vp]),
     "parm_combine_fwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_ll,
                                   _vp]),
     "parm_combine_bwd": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
@@ -91,7 +91,7 @@ SIGNATURES = {
     "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _vp]),
 }
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 class ParmError(RuntimeError):
@@ -128,7 +128,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
 
 
 # Kernel launches each entry point issues on success (bench.py's gpu_launches).
-LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2, "parm_gate_slots": 2, "parm_dispatch_rows_peer": 2}
+LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2, "parm_gate_slots": 2}
 launch_count = 0
 
 

@@ -24,7 +24,7 @@ int gate_slots(const int*, int, int, int, int, int*, int*, int*, int*, size_t, c
 size_t gate_wgrad_workspace(int, int, int);
 int gate_wgrad(const void*, long long, const float*, int, int, int, float*, size_t, float*, int, cudaStream_t);
 int dispatch_rows(const void*, long long, const int*, const float*, int, int, int, int, int, int, void*, long long,
-                  long long, cudaStream_t);
+                  long long, const int*, cudaStream_t);
 int combine_fwd(const SlotView&, const int*, const int*, const float*, int, int, int, void*, long long, cudaStream_t);
 int combine_bwd(const void*, long long, const SlotView&, const int*, const int*, const float*, int, int, int, int,
                 float*, cudaStream_t);
@@ -82,9 +82,9 @@ int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* sl
 
 int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
                        int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
-                       long long out_stride_s, void* stream) {
+                       long long out_stride_s, const int* fill, void* stream) {
     return parm::dispatch_rows(x, ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, out, out_stride_e,
-                               out_stride_s, S(stream));
+                               out_stride_s, fill, S(stream));
 }
 
 int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,

@@ -54,7 +54,7 @@ template <bool PEER>
 __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
     const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
     int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
-    long long out_stride_s, const __grid_constant__ SlotView dstv) {
+    long long out_stride_s, const __grid_constant__ SlotView dstv, const int* __restrict__ fill) {
     constexpr int R = 4;
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
@@ -73,6 +73,11 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
                 const int e = (int)(r / slots_out);
                 const int sp = (int)(r - (long long)e * slots_out);
                 const int s = slot_lo + sp;
+                if (fill != nullptr) {   // rows past the segment's last 128-row GEMM tile are never read
+                    int sf = __ldg(fill + e) - slot_lo;
+                    sf = sf < 0 ? 0 : (sf > slots_out ? slots_out : sf);
+                    if (sp >= ((sf + 127) & ~127)) continue;
+                }
                 src[q] = (s < cap) ? __ldg(slot_src + (long long)e * cap + s) : -1;
                 if (PEER) {
                     int ep;
@@ -422,7 +427,7 @@ static int check_view(const SlotView& v, int M, const char* what) {
 
 int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
                   int slot_lo, int slots_out, int M, void* out, long long out_stride_e, long long out_stride_s,
-                  cudaStream_t s) {
+                  const int* fill, cudaStream_t s) {
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && out_stride_s % 8 == 0 && out_stride_e % 8 == 0,
                    "dispatch_rows: rows must be 16-byte aligned (M=%d)", M);
     const long long rows = (long long)E * slots_out;
@@ -430,7 +435,7 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
     SlotView none{};
     dispatch_rows_kernel<false><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
         reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
-        reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none);
+        reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none, fill);
     PARM_CHECK_LAUNCH("dispatch_rows");
     return 0;
 }
@@ -457,7 +462,7 @@ int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const 
     if (rows > 0) {
         dispatch_rows_kernel<true><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
             reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
-            dst);
+            dst, fill);
         PARM_CHECK_LAUNCH("dispatch_rows_peer");
     }
     if (fill != nullptr && fill_dst != nullptr) {

@@ -113,15 +113,16 @@ def gate_slots(expert_idx: torch.Tensor, E: int, cap: int, slot_idx: torch.Tenso
 
 
 def dispatch_rows(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, out: torch.Tensor,
-                  scale: torch.Tensor | None = None) -> None:
-    """out: (E, S_out, M) view (any strides with unit inner stride)."""
+                  scale: torch.Tensor | None = None, fill: torch.Tensor | None = None) -> None:
+    """out: (E, S_out, M) view (any strides with unit inner stride).  With ``fill`` (per-expert
+    counts) rows past the segment's last 128-row GEMM tile are not written."""
     _need(x, torch.bfloat16, "rows source")
     _need(out, torch.bfloat16, "dispatch out")
     E, S, M = out.shape
     if out.stride(2) != 1 or x.stride(1) != 1:
         raise ValueError("dispatch rows need unit inner stride")
     _lib.call("parm_dispatch_rows", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
-              slot_lo, S, M, out.data_ptr(), out.stride(0), out.stride(1), _stream())
+              slot_lo, S, M, out.data_ptr(), out.stride(0), out.stride(1), _ptr(fill), _stream())
 
 
 def combine_fwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,
@@ -168,6 +169,8 @@ def dispatch_rows_peer(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int
     _lib.call("parm_dispatch_rows_peer", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
               slot_lo, slots_out, x.shape[1], ctypes.byref(v), _ptr(fill), None if ff is None else ctypes.byref(ff),
               _stream())
+    if ff is not None and fill is not None:
+        _lib.launch_count += 1            # the fill-count fan-out kernel
 
 
 def combine_fwd_fan(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,

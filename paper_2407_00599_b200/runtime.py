@@ -452,7 +452,7 @@ class MoELayer:
             b["xin"] = x
             rt = b["route"]
             rt.run(x, s.gate64, d.k)
-            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["send"])
+            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["send"], fill=rt.fill)
             self._ffn_fwd(s, b)
             K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
             outs[r] = b["out"][:, :d.M]
@@ -468,7 +468,7 @@ class MoELayer:
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
             K.combine_bwd(dout, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
+            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w, fill=rt.fill)
             self._ffn_bwd(s, b)
             K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                            b["dx"])
@@ -530,7 +530,7 @@ class MoELayer:
             rt = b["route"]
             K.combine_bwd(ds, self._peer_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows_peer(ds, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "dyrecv", r),
-                                 scale=rt.combine_w)
+                                 scale=rt.combine_w, fill=rt.fill)
         self.world.peer_barrier()
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
@@ -561,7 +561,7 @@ class MoELayer:
             b["xslice"] = xs_
             rt = b["route"]
             rt.run(xs_, s.gate64, d.k)
-            K.dispatch_rows(xs_, rt.slot_src, d.k, rt.cap, 0, b["send"])
+            K.dispatch_rows(xs_, rt.slot_src, d.k, rt.cap, 0, b["send"], fill=rt.fill)
         self.world.exchange(self._fused_msgs("s1", "send", "recv", with_fill=True))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
@@ -590,7 +590,7 @@ class MoELayer:
             ds = dout[m * sl:(m + 1) * sl]          # adjoint of AG_mp: own slice
             rt = b["route"]
             K.combine_bwd(ds, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(ds, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w)
+            K.dispatch_rows(ds, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w, fill=rt.fill)
         self.world.exchange(self._fused_msgs("s1", "dsend", "dyrecv", with_fill=False))  # adjoint of ESP sum + A2A
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
@@ -707,7 +707,7 @@ class MoELayer:
             rt = b["route"]
             K.combine_bwd(dout, self._shard_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows_peer(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
-                                 self._peer_view(b, "dyrecv", r), scale=rt.combine_w)
+                                 self._peer_view(b, "dyrecv", r), scale=rt.combine_w, fill=rt.fill)
         self.world.peer_barrier()
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
@@ -730,7 +730,7 @@ class MoELayer:
             b["xin"] = x
             rt = b["route"]
             rt.run(x, s.gate64, d.k)
-            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"])
+            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"], fill=rt.fill)
             # fill of this rank's slot shard [m*q, (m+1)*q): clamp(fill - m*q, 0, q) per expert
             if "shard_fill" not in b:
                 b["shard_fill"] = torch.zeros(d.E, dtype=torch.int32, device=self.dev)
@@ -757,7 +757,8 @@ class MoELayer:
             rt = b["route"]
             K.combine_bwd(dout, self._gath_view(b, "gath"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             # adjoint of AG_mp over slots: only this rank's slot shard
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["dsend"], scale=rt.combine_w)
+            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["dsend"],
+                            scale=rt.combine_w, fill=rt.fill)
         self.world.exchange(self._fused_msgs("s2", "dsend", "dyrecv", with_fill=False))
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
@@ -793,7 +794,7 @@ class MoELayer:
             for q in range(d.ESP):                               # re-gate every gathered block
                 rt = b["route_blk"][q]
                 rt.run(b["xg"][q], s.gate64, d.k)
-                K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][q])
+                K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][q], fill=rt.fill)
         self.world.exchange(self._ep_dispatch_msgs("disp", "recv", with_fill=True))
         ys = {}
         for r in self.ranks:
@@ -856,7 +857,7 @@ class MoELayer:
             rt = b["route"]
             K.combine_bwd(dout, self._ret_own_view(b, "ret", L.esp_pos(r)), rt.expert_idx, rt.slot_idx, rt.probs,
                           b["dlogits"])
-            K.dispatch_rows(dout, rt.slot_src, d.k, d.T, 0, b["dyown"], scale=rt.combine_w)
+            K.dispatch_rows(dout, rt.slot_src, d.k, d.T, 0, b["dyown"], scale=rt.combine_w, fill=rt.fill)
             ins[r], outs[r] = b["dyown"], b["dyg"]
         self.world.allgather("esp", ins, outs)                   # adjoint of the ESP split
         self.world.exchange(self._ep_dispatch_msgs("dyg", "dyrecv", with_fill=False))  # adjoint of return A2A

@@ -67,7 +67,7 @@ def test_argument_validation_without_a_gpu(lib):
     _expect_arg_error(lib.parm_gate_fwd, None, 8, None, 4, 8, 2, 3, None, None, None, None,
                       match=r"top_k \(3\) exceeds number of experts \(2\)")
     _expect_arg_error(lib.parm_gate_slots, None, 4, 9, 2, 4, None, None, None, None, 0, None, match="top_k must be")
-    _expect_arg_error(lib.parm_dispatch_rows, None, 10, None, None, 1, 2, 4, 0, 4, 10, None, 10, 10, None,
+    _expect_arg_error(lib.parm_dispatch_rows, None, 10, None, None, 1, 2, 4, 0, 4, 10, None, 10, 10, None, None,
                       match="16-byte aligned")
     _expect_arg_error(lib.parm_combine_fwd, None, None, None, None, 4, 1, 8, None, 8, None,
                       match="null slot view")

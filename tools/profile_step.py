@@ -20,7 +20,7 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2407_00599_b200.config import MoEConfig  # noqa: E402
 from paper_2407_00599_b200.runtime import MoELayer  # noqa: E402
-from paper_2407_00599_b200.world import LocalWorld, NcclWorld  # noqa: E402
+from paper_2407_00599_b200.world import LocalWorld, NcclWorld, PeerWorld  # noqa: E402
 
 
 def main():
@@ -52,7 +52,8 @@ def main():
         layout = ParallelLayout(mp, ep, esp, args.gpus)
     else:
         layout = bench.layout_for(args.gpus)
-    w = NcclWorld(layout, dev) if world > 1 else LocalWorld(layout, dev)
+    peer = os.environ.get("PARM_PEER", "1") != "0"
+    w = ((PeerWorld if peer else NcclWorld)(layout, dev)) if world > 1 else LocalWorld(layout, dev)
     layer = MoELayer(cfg, layout, w)
     layer.init_random(0)
     x = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, device=dev).to(torch.bfloat16)
@@ -79,7 +80,9 @@ def main():
             print(f"GPU span {(t1 - t0) / args.steps:.1f} us/step, summed kernel time {busy / args.steps:.1f} us/step")
     if world > 1:
         torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+        torch.cuda.synchronize()
+        sys.stdout.flush()
+        os._exit(0)        # symmetric-memory mappings can stall process-group teardown
 
 
 if __name__ == "__main__":
