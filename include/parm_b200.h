@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 7
+#define PARM_ABI_VERSION 8
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -146,6 +146,13 @@ int parm_combine_fwd_fan(const parm_slot_view* y, const int* expert_idx, const i
 int parm_dispatch_bwd_fan(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,
                           const void* wg_t, int n, int k, int E, int M, const parm_row_fan* dx, long long ldx,
                           void* stream);
+
+/* Return AlltoAll as a push: holder rows src[seg][i][s] (segment = source
+ * rank, s < fill[seg * e_local + i]) stored into dst->ptr[seg] + (i * rows + s) * M,
+ * the owner's receive block for this holder (fused_combine's exchange,
+ * collectives.py:286-295). */
+int parm_push_rows(const void* src, int nseg, int e_local, int rows, int M, const int* fill, const parm_row_fan* dst,
+                   void* stream);
 
 /* Device-side barrier of the n peers (one tiny kernel; graph-capturable). */
 int parm_peer_barrier(const parm_peer_signal* sig, void* stream);

@@ -89,9 +89,10 @@ SIGNATURES = {
     "parm_dispatch_bwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
                                        ctypes.POINTER(RowFanC), _c_ll, _vp]),
     "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _vp]),
+    "parm_push_rows": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, ctypes.POINTER(RowFanC), _vp]),
 }
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 
 class ParmError(RuntimeError):

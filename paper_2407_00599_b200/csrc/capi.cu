@@ -39,6 +39,7 @@ int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, 
 int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
                      const RowFan&, long long, cudaStream_t);
 int peer_barrier(const PeerSignal&, cudaStream_t);
+int push_rows(const void*, int, int, int, int, const int*, const RowFan&, cudaStream_t);
 
 template <class A, class B>
 static A abi_cast(const B* v) {
@@ -163,6 +164,15 @@ int parm_dispatch_bwd_fan(const parm_slot_view* dr, const int* expert_idx, const
     }
     return parm::dispatch_bwd_fan(to_view(dr), expert_idx, slot_idx, dlogits, wg, n, k, E, M,
                                   parm::abi_cast<parm::RowFan>(dx), ldx, S(stream));
+}
+
+int parm_push_rows(const void* src, int nseg, int e_local, int rows, int M, const int* fill, const parm_row_fan* dst,
+                   void* stream) {
+    if (!dst) {
+        parm::set_error("push_rows: null destination fan");
+        return 1;
+    }
+    return parm::push_rows(src, nseg, e_local, rows, M, fill, parm::abi_cast<parm::RowFan>(dst), S(stream));
 }
 
 int parm_peer_barrier(const parm_peer_signal* sig, void* stream) {

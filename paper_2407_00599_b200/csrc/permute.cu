@@ -472,6 +472,55 @@ int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const 
     return 0;
 }
 
+// ------------------------------------------------------------------ push (holder -> owners)
+// Segmented expert rows src[seg][i][s] (s < fill[seg][i]) stored into
+// dst.ptr[seg] + (i * rows + s) * M -- the return AlltoAll as posted NVLink
+// stores from the holder into every owner's receive block (a push moves the
+// bytes once; the owner's combine and combine-backward then read them locally).
+__global__ void __launch_bounds__(kRowThreads) push_rows_kernel(const bf16* __restrict__ src, int nseg, int el,
+                                                                int rows, int M, const int* __restrict__ fill,
+                                                                const __grid_constant__ RowFan dst) {
+    const int lane = threadIdx.x & 31;
+    const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
+    const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
+    const long long total = (long long)nseg * el * rows;
+    for (long long r = warp_global; r < total; r += num_warps) {
+        const long long per_seg = (long long)el * rows;
+        const int seg = (int)(r / per_seg);
+        const long long rem = r - seg * per_seg;
+        const int i = (int)(rem / rows);
+        const int s = (int)(rem - (long long)i * rows);
+        if (s >= __ldg(fill + seg * el + i)) continue;
+        const bf16* sp = src + r * M;
+        bf16* dp = dst.ptr[seg] + ((long long)i * rows + s) * M;
+        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
+            int4 v[kChunks];
+#pragma unroll
+            for (int u = 0; u < kChunks; ++u) {
+                const int c = g0 + lane * 8 + u * 256;
+                v[u] = c < M ? ldg16(sp + c) : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kChunks; ++u) {
+                const int c = g0 + lane * 8 + u * 256;
+                if (c < M) *reinterpret_cast<int4*>(dp + c) = v[u];
+            }
+        }
+    }
+}
+
+int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fill, const RowFan& dst, cudaStream_t s) {
+    PARM_CHECK_ARG(nseg >= 1 && nseg <= kMaxPeers && dst.n == nseg, "push_rows: %d segments for %d destinations",
+                   nseg, dst.n);
+    PARM_CHECK_ARG(M % 8 == 0 && fill != nullptr, "push_rows: M=%d must be a multiple of 8, fill required", M);
+    const long long total = (long long)nseg * el * rows;
+    if (total == 0) return 0;
+    push_rows_kernel<<<row_grid(total), kRowThreads, 0, s>>>(reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
+                                                             fill, dst);
+    PARM_CHECK_LAUNCH("push_rows");
+    return 0;
+}
+
 // ------------------------------------------------------------------ peer barrier
 // Every rank stores the next epoch into slot [rank] of every peer's signal pad
 // (release, system scope, after a system fence that publishes this rank's

@@ -194,6 +194,14 @@ def dispatch_bwd_fan(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.T
               _ptr(wg), n, k, E, M, ctypes.byref(f), ldx, _stream())
 
 
+def push_rows(src: torch.Tensor, fill: torch.Tensor, dst_ptrs: list) -> None:
+    """src (nseg, 1, e_local, rows, M) holder rows; rows s < fill[seg, i] go to dst_ptrs[seg] + (i*rows+s)*M."""
+    _need(src, torch.bfloat16, "push source")
+    nseg, _, el, rows, M = src.shape
+    f = _fan(dst_ptrs)
+    _lib.call("parm_push_rows", src.data_ptr(), nseg, el, rows, M, fill.data_ptr(), ctypes.byref(f), _stream())
+
+
 def peer_barrier(pads: list, counter: torch.Tensor, rank: int) -> None:
     """Device-side barrier of len(pads) ranks (signal-pad addresses of every rank, this rank's epoch counter)."""
     s = _lib.PeerSignalC()

@@ -164,6 +164,9 @@ class MoELayer:
         self.saa_phased = _saa_phased(layout)
         # S1/S2 over NVLink peer memory (fused dispatch/return/AllGather) when the world maps peers
         self.peer = (isinstance(self.world, PeerWorld) and d.P > 1 and os.environ.get("PARM_PEER", "1") != "0")
+        # S1's return path: holders push expert outputs into the owners' receive blocks ("push", one
+        # NVLink pass reused by combine and combine-backward) or owners gather them ("pull")
+        self.peer_push = os.environ.get("PARM_PEER_RETURN", "push") == "push"
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -293,7 +296,9 @@ class MoELayer:
             b["y"] = torch.zeros(*shape, d.Mp, **bf)
             b["dr"] = torch.zeros(*shape, d.Mp, **bf)
         if peer:
-            pass
+            if schedule == "s1" and self.peer_push:     # owners' receive blocks [holder][i][slot]
+                b["ret"], b["ret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
+                b["dret"], b["dret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
         elif schedule == "baseline":
             b["ret"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # owner side [holder j][block][i][slot]
             b["dd"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
@@ -487,6 +492,12 @@ class MoELayer:
         return K.SlotView(None, e_local=el, n_p=d.ESP, stride_i=q * d.Mp, stride_slo=d.Mp,
                           peers=tuple(a + off for a in b[key + "_peers"]), peer_ep=pe, peer_p=pp)
 
+    def _push_fan(self, b: dict, key: str, h: int) -> list[int]:
+        """Holder h's block in every owner's (P, e_local, q, M) receive buffer `key` (segment = owner)."""
+        d = self.d
+        off = 2 * h * d.e_local * b["q"] * d.Mp
+        return [a + off for a in b[key + "_peers"]]
+
     def _mp_fan(self, b: dict, key: str, r: int) -> list[int]:
         """Row r-slice of every MP peer's (n, M) buffer `key` (the fused MP AllGather)."""
         d, L = self.d, self.layout
@@ -508,13 +519,16 @@ class MoELayer:
                                  fill=rt.fill, fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
         self.world.peer_barrier()                                     # receive buffers complete
         for r in self.ranks:
-            self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
-        self.world.peer_barrier()                                     # expert outputs complete
+            b = self.st[r].bufs["s1"]
+            self._ffn_fwd(self.st[r], b)
+            if self.peer_push:
+                K.push_rows(b["y"], b["fill_in"], self._push_fan(b, "ret", r))
+        self.world.peer_barrier()                                     # expert outputs complete / delivered
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
             rt = b["route"]
-            K.combine_fwd_fan(self._peer_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.combine_w,
-                              self._mp_fan(b, "out", r), sl, d.Mp, d.Mp)
+            yv = self._ret_view(b, "ret") if self.peer_push else self._peer_view(b, "y", r)
+            K.combine_fwd_fan(yv, rt.expert_idx, rt.slot_idx, rt.combine_w, self._mp_fan(b, "out", r), sl, d.Mp, d.Mp)
         self.world.peer_barrier()                                     # every MP slice gathered
         self._last = "s1"
         return {r: self.st[r].bufs["s1"]["out"][:, :d.M] for r in self.ranks}
@@ -528,18 +542,23 @@ class MoELayer:
             m = L.mp_pos(r)
             ds = dout[m * sl:(m + 1) * sl]
             rt = b["route"]
-            K.combine_bwd(ds, self._peer_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            yv = self._ret_view(b, "ret") if self.peer_push else self._peer_view(b, "y", r)
+            K.combine_bwd(ds, yv, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows_peer(ds, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "dyrecv", r),
                                  scale=rt.combine_w, fill=rt.fill)
         self.world.peer_barrier()
         for r in self.ranks:
-            self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
+            b = self.st[r].bufs["s1"]
+            self._ffn_bwd(self.st[r], b)
+            if self.peer_push:
+                K.push_rows(b["dr"], b["fill_in"], self._push_fan(b, "dret", r))
         self.world.peer_barrier()
         gins = {}
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s1"]
             rt = b["route"]
-            K.dispatch_bwd_fan(self._peer_view(b, "dr", r), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
+            dv = self._ret_view(b, "dret") if self.peer_push else self._peer_view(b, "dr", r)
+            K.dispatch_bwd_fan(dv, rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                                self._mp_fan(b, "dx", r), sl, d.Mp, d.Mp)
             K.gate_wgrad(b["xslice"], b["dlogits"], s.dgate, self._ws_gate)
             gins[r] = s.dgate
