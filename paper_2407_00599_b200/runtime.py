@@ -167,6 +167,9 @@ class MoELayer:
         # S1's return path: holders push expert outputs into the owners' receive blocks ("push", one
         # NVLink pass reused by combine and combine-backward) or owners gather them ("pull")
         self.peer_push = os.environ.get("PARM_PEER_RETURN", "push") == "push"
+        # S2 pushes MP copies of every row (its AllGather), measured no faster than the owners'
+        # gathers through the slot-shard view (N=4: 0.85 vs 0.84 ms), so S2 pulls by default
+        self.peer_push_s2 = os.environ.get("PARM_PEER_RETURN_S2", "pull") == "push"
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -299,6 +302,9 @@ class MoELayer:
             if schedule == "s1" and self.peer_push:     # owners' receive blocks [holder][i][slot]
                 b["ret"], b["ret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
                 b["dret"], b["dret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
+            if schedule == "s2" and self.peer_push_s2:  # owners' gathered slots [holder][MP shard][i][slot]
+                b["gath"], b["gath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp))
+                b["dgath"], b["dgath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp))
         elif schedule == "baseline":
             b["ret"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # owner side [holder j][block][i][slot]
             b["dd"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
@@ -694,6 +700,25 @@ class MoELayer:
                           stride_slo=d.Mp, peers=tuple(a + 2 * r0 * seg for a in b[key + "_peers"]),
                           peer_ep=pe, peer_p=pp)
 
+    def _push_s2(self, b: dict, src_key: str, dst_key: str, h: int) -> None:
+        """S2's return + MP AllGather as pushes: holder h stores segment src's rows into the
+        [h][mp_pos(src)] block of every member of src's MP group (one launch per member index)."""
+        d = self.d
+        blk = d.e_local * b["q"] * d.Mp
+        for j in range(d.MP):
+            fan = [b[dst_key + "_peers"][(src // d.MP) * d.MP + j] + 2 * (h * d.MP + src % d.MP) * blk
+                   for src in range(d.P)]
+            K.push_rows(b[src_key], b["fill_in"], fan)
+
+    def _gath_push_view(self, b: dict, key: str) -> K.SlotView:
+        """Owner-side pushed slots: row (e, s, p) = buf[rank_of(ep_e, p)][s // q][i_e][s % q]."""
+        d, L = self.d, self.layout
+        q, el = b["q"], d.e_local
+        blk = d.MP * el * q * d.Mp
+        a, c = (d.ESP, 1) if L.esp_contiguous else (1, d.EP)
+        return K.SlotView(b[key], e_local=el, n_p=d.ESP, slot_div=q, stride_ep=a * blk, stride_i=q * d.Mp,
+                          stride_p=c * blk, stride_shi=el * q * d.Mp, stride_slo=d.Mp)
+
     def _fwd_s2_peer(self, xs: dict) -> dict:
         d, L = self.d, self.layout
         el = d.e_local
@@ -709,12 +734,16 @@ class MoELayer:
                                  fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
         self.world.peer_barrier()
         for r in self.ranks:
-            self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
+            b = self.st[r].bufs["s2"]
+            self._ffn_fwd(self.st[r], b)
+            if self.peer_push_s2:
+                self._push_s2(b, "y", "gath", r)
         self.world.peer_barrier()
         for r in self.ranks:      # return A2A + ESP sum + MP AllGather of the slots, fused into the combine
             b = self.st[r].bufs["s2"]
             rt = b["route"]
-            K.combine_fwd(self._shard_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
+            yv = self._gath_push_view(b, "gath") if self.peer_push_s2 else self._shard_view(b, "y", r)
+            K.combine_fwd(yv, rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
         self._last = "s2"
         return {r: self.st[r].bufs["s2"]["out"][:, :d.M] for r in self.ranks}
 
@@ -724,18 +753,22 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["s2"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            K.combine_bwd(dout, self._shard_view(b, "y", r), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
+            yv = self._gath_push_view(b, "gath") if self.peer_push_s2 else self._shard_view(b, "y", r)
+            K.combine_bwd(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             K.dispatch_rows_peer(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
                                  self._peer_view(b, "dyrecv", r), scale=rt.combine_w, fill=rt.fill)
         self.world.peer_barrier()
         for r in self.ranks:
-            self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
+            b = self.st[r].bufs["s2"]
+            self._ffn_bwd(self.st[r], b)
+            if self.peer_push_s2:
+                self._push_s2(b, "dr", "dgath", r)
         self.world.peer_barrier()
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s2"]
             rt = b["route"]
-            K.dispatch_bwd(self._shard_view(b, "dr", r), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
-                           b["dx"])
+            dv = self._gath_push_view(b, "dgath") if self.peer_push_s2 else self._shard_view(b, "dr", r)
+            K.dispatch_bwd(dv, rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E, b["dx"])
             K.gate_wgrad(b["xin"], b["dlogits"], s.dgate, self._ws_gate)
         return {r: self.st[r].bufs["s2"]["dx"][:, :d.M] for r in self.ranks}
 
