@@ -285,10 +285,17 @@ def h2d_bandwidth(host, dev) -> float:
 def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_graph=True):
     """Public-API step with host buffers: H2D of the step's tokens and upstream
     gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
-    and a D2H read of the step's routing metric (per-expert fill)."""
+    and a D2H read of the step's routing metric (per-expert fill).  S1 splits
+    the MP group's tokens (paper §IV-C): a rank gates, dispatches and
+    back-propagates only its slice, so only the slice's rows cross PCIe."""
     import torch
 
     r = layer.ranks[0]
+    lo, hi = 0, host_x.shape[0]
+    if schedule == "s1" and layer.d.MP > 1:
+        sl = layer.d.n // layer.d.MP
+        lo = layer.layout.mp_pos(r) * sl
+        hi = lo + sl
     comp = torch.cuda.current_stream()
     cps = torch.cuda.Stream()
     dx = [torch.empty(host_x.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
@@ -307,8 +314,8 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
             cps.wait_event(free[slot])
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(cps)
-            dx[slot].copy_(host_x, non_blocking=True)
-            dd[slot].copy_(host_d, non_blocking=True)
+            dx[slot][lo:hi].copy_(host_x[lo:hi], non_blocking=True)
+            dd[slot][lo:hi].copy_(host_d[lo:hi], non_blocking=True)
             c1.record(cps)
             copy_ev.append((c0, c1))
             ready[slot].record(cps)
@@ -342,7 +349,7 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    h2d = 2 * host_x.numel() * 2
+    h2d = 2 * host_x[lo:hi].numel() * 2
     d2h = layer.d.E * 4
     return ms, h2d, d2h
 
@@ -445,7 +452,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         tps = tokens_per_step(cfg, layout)
         e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream)",
+               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream; "
+                      "S1 copies each rank's MP token slice)",
                "h2d_gbs_measured": h2d_gbs, "host_numa_cpus": numa, "h2d_ms_per_step_in_loop": h2d_ms,
                "repetitions_ms": [r[0] for r in reps]}
     if rank != 0:
