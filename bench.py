@@ -282,6 +282,39 @@ def h2d_bandwidth(host, dev) -> float:
     return 5 * host.numel() * host.element_size() / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
+def peaks_hbm() -> float:
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0                           # B200_PROFILING.md fallback
+
+
+NVLINK_GBS = 770.0        # measured peer copy per direction per GPU (B200_PROFILING.md)
+
+
+def layer_roofline(cfg, layout, schedule: str, ms: float, tc_peak: float, hbm_gbs: float) -> dict:
+    """serialized-sum roofline of the whole layer step on one GPU,
+    t_roof = FLOP_alg / tensor peak + wire bytes / NVLink + token-side HBM bytes / HBM,
+    frac = t_roof / t_measured (Parm has no intra-layer pipelining)."""
+    from paper_2407_00599_b200.trace import schedule_trace
+
+    P, MP, ESP, k = layout.world_size, layout.mp_size, layout.esp_size, cfg.top_k
+    n, M, H = cfg.tokens_per_rank, cfg.embed_dim, cfg.hidden_dim
+    flops = (P // MP) * n * k * 12 * M * H / P                     # useful assignments, fwd 4MH + bwd 8MH
+    wire = 0.0
+    if P > 1:
+        wire = 2 * 2 * sum(r.wire_per_rank for r in schedule_trace(schedule, cfg, layout).records)  # bf16, fwd+bwd
+    ng = n // MP if schedule == "s1" else n                         # tokens this rank gates / combines
+    row = M * 2
+    hbm = ng * row * (1 + 2 * k + (k * ESP + 1) + (1 + k * ESP) + 2 * k + (k * ESP + 1) + 1)
+    t_tc, t_nvl, t_hbm = flops / (tc_peak * 1e12), wire / (NVLINK_GBS * 1e9), hbm / (hbm_gbs * 1e9)
+    t_roof = t_tc + t_nvl + t_hbm
+    return {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "tensor_ms": t_tc * 1e3, "nvlink_ms": t_nvl * 1e3,
+            "hbm_ms": t_hbm * 1e3, "flop_alg": flops, "wire_bytes": wire, "hbm_bytes": hbm,
+            "peaks": {"tensor_tflops": tc_peak, "nvlink_gbs": NVLINK_GBS, "hbm_gbs": hbm_gbs},
+            "note": "HBM bytes = token-side kernels (gate, dispatch x2, combine, combine-bwd, dispatch-bwd, gate wgrad)"}
+
+
 def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_graph=True):
     """Public-API step with host buffers: H2D of the step's tokens and upstream
     gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
@@ -478,6 +511,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
                 "executed_tflops": roof["padded_flops_per_launch"] / (roof["avg_launch_ms"] / 1e3) / 1e12,
                 "gemm_share_of_step": roof["gemm_ms_per_step"] / ms,
                 "units": "alg FLOPs = 2 * kept assignment rows * M * (H/N_ESP) per GEMM; 6 GEMMs per step"}
+    roofline["layer"] = layer_roofline(cfg, layout, schedule, ms, peak, peaks_hbm())
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         rate, dt, cores = oracle_step_rate(cfg, layout, CPU_SAMPLE_TOKENS, 3)
