@@ -67,4 +67,8 @@ def __getattr__(name):
         from .runtime import MoELayer
 
         return MoELayer
+    if name in ("ParmMoE",):
+        from .module import ParmMoE
+
+        return ParmMoE
     raise AttributeError(name)
