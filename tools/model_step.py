@@ -1,9 +1,14 @@
-"""BERT-large-shaped MoE model training step on one B200 (BASELINE config 4).
+"""MoE transformer training steps around the hot path (BASELINE configs 4-5).
 
-    python tools/model_step.py [--layers 24] [--moe parm|torch] [--steps 10]
+    python tools/model_step.py [--model bert|gpt2] [--moe parm|torch] [--steps 10]
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/model_step.py \
+        --model gpt2 --gpus 4          # E=16, MP=2 ESP=2 (EP=2), NVLink peer transport
 
 24 pre-LN transformer blocks, hidden 1024, 16 heads, FFN 4096; every other FFN is an MoE
-layer with E=8 experts, top-2, f=1.2 (the paper's model-level setting).
+layer, top-2, f=1.2 (the paper's model-level setting): bert = bidirectional
+attention, E=8; gpt2 = causal attention, E=16.  Multi-GPU (torchrun): the MoE layers run the
+Parm schedule over the (MP, EP, ESP) layout; the dense blocks are replicated inside an MP group
+(the paper's replicated-MP convention) and data-parallel across groups (gradient all-reduce).
 Synthetic token embeddings (B=16, L=512 -> 8192 tokens), MSE loss, AdamW, bf16 autocast for the
 dense parts.  ``--moe parm`` uses ParmMoE (the sm_100a hot path); ``--moe torch`` an eager
 PyTorch MoE with the same routing rule (softmax top-2, capacity drop, scatter/gather + bmm
@@ -60,8 +65,9 @@ class TorchMoE(nn.Module):
 
 
 class Block(nn.Module):
-    def __init__(self, M, heads, H, moe: nn.Module | None):
+    def __init__(self, M, heads, H, moe: nn.Module | None, causal: bool = False):
         super().__init__()
+        self.causal = causal
         self.ln1, self.ln2 = nn.LayerNorm(M), nn.LayerNorm(M)
         self.qkv, self.proj = nn.Linear(M, 3 * M), nn.Linear(M, M)
         self.heads = heads
@@ -72,7 +78,7 @@ class Block(nn.Module):
     def forward(self, x, B, L):
         M = x.shape[-1]
         q, k, v = self.qkv(self.ln1(x)).view(B, L, 3, self.heads, M // self.heads).permute(2, 0, 3, 1, 4)
-        a = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B * L, M)
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=self.causal).transpose(1, 2).reshape(B * L, M)
         x = x + self.proj(a)
         h = self.ln2(x)
         if self.moe is None:
@@ -81,26 +87,57 @@ class Block(nn.Module):
 
 
 def main() -> int:
+    import os
+
     ap = argparse.ArgumentParser()
+    ap.add_argument("--model", choices=("bert", "gpt2"), default="bert")
     ap.add_argument("--layers", type=int, default=24)
     ap.add_argument("--moe", choices=("parm", "torch"), default="parm")
+    ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     args = ap.parse_args()
-    dev = torch.device("cuda", 0)
-    torch.manual_seed(0)
-    B, L, M, heads, H, E, k, f = 16, 512, 1024, 16, 4096, 8, 2, 1.2
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    E = 8 if args.model == "bert" else 16
+    B, L = (16, 512) if args.model == "bert" else (8, 1024)
+    M, heads, H, k, f = 1024, 16, 4096, 2, 1.2
     n = B * L
     cfg = MoEConfig(B, L, M, H, E, k, f)
-    layout = ParallelLayout(1, 1, 1, 1)
+    layout = {1: ParallelLayout(1, 1, 1, 1), 2: ParallelLayout(2, 1, 2, 2), 4: ParallelLayout(2, 2, 2, 4),
+              8: ParallelLayout(2, 4, 2, 8)}[world]
+    if world > 1 and args.moe != "parm":
+        raise SystemExit("the eager comparison MoE is single-GPU")
+    torch.manual_seed(1234 + rank // layout.mp_size)    # MP ranks hold identical dense replicas and tokens
+    mk_world = None
+    if world > 1:
+        from paper_2407_00599_b200.world import PeerWorld
+
+        mk_world = PeerWorld(layout, dev)
     blocks = []
     for i in range(args.layers):
         moe = None
         if i % 2 == 1:
-            moe = (ParmMoE(cfg, layout, LocalWorld(layout, dev), schedule="s1", seed=i) if args.moe == "parm"
-                   else TorchMoE(M, H, E, k, f, n).to(dev))
-        blocks.append(Block(M, heads, H, moe).to(dev))
+            if args.moe == "parm":
+                moe = ParmMoE(cfg, layout, mk_world if world > 1 else LocalWorld(layout, dev), schedule="s1", seed=i)
+            else:
+                moe = TorchMoE(M, H, E, k, f, n).to(dev)
+        blocks.append(Block(M, heads, H, moe, causal=args.model == "gpt2").to(dev))
     model = nn.ModuleList(blocks)
+    if world > 1:   # identical dense init on every rank
+        for p_ in model.parameters():
+            if not any(p_ is q_ for blk in blocks if blk.moe is not None for q_ in (blk.moe.w1, blk.moe.w2)):
+                dist.broadcast(p_.data, 0)
+    dense = [p_ for p_ in model.parameters()
+             if not any(p_ is q_ for blk in blocks if blk.moe is not None for q_ in (blk.moe.w1, blk.moe.w2))]
     opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
     x0 = torch.randn(n, M, device=dev)
     target = torch.randn(n, M, device=dev)
@@ -113,12 +150,18 @@ def main() -> int:
                 x = blk(x, B, L)
             loss = F.mse_loss(x.float(), target)
         loss.backward()
+        if world > 1:       # data-parallel dense (and gate) gradients; expert shards are unique per rank
+            for p_ in dense:
+                if p_.grad is not None:
+                    dist.all_reduce(p_.grad, op=dist.ReduceOp.AVG)
         opt.step()
         return loss
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
@@ -127,10 +170,24 @@ def main() -> int:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    print(json.dumps({"model": f"BERT-large-MoE ({args.layers} blocks, MoE every other FFN, E=8 top-2 f=1.2)",
-                      "moe_impl": args.moe, "tokens_per_step": n, "ms_per_step": ms, "tokens_per_s": n / ms * 1e3,
-                      "wall_ms_per_step": (time.perf_counter() - t0) / args.steps * 1e3, "loss": float(loss),
-                      "data": "synthetic embeddings, MSE loss, AdamW, bf16 autocast (dense), fp32 masters"}))
+    if dist is not None:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    toks = (world // layout.mp_size) * n
+    if rank == 0:
+        name = {"bert": "BERT-large-MoE", "gpt2": "GPT-2-MoE"}[args.model]
+        print(json.dumps({"model": f"{name} ({args.layers} blocks, MoE every other FFN, E={E} top-2 f=1.2)",
+                          "moe_impl": args.moe, "n_gpus": world,
+                          "layout": f"MP={layout.mp_size} EP={layout.ep_size} ESP={layout.esp_size}",
+                          "tokens_per_step": toks, "ms_per_step": ms, "tokens_per_s": toks / ms * 1e3,
+                          "wall_ms_per_step": (time.perf_counter() - t0) / args.steps * 1e3, "loss": float(loss),
+                          "data": "synthetic embeddings, MSE loss, AdamW, bf16 autocast (dense), fp32 masters"}),
+              flush=True)
+    if dist is not None:
+        dist.barrier()
+        sys.stdout.flush()
+        os._exit(0)
     return 0
 
 
