@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 8
+#define PARM_ABI_VERSION 9
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -153,6 +153,10 @@ int parm_dispatch_bwd_fan(const parm_slot_view* dr, const int* expert_idx, const
  * collectives.py:286-295). */
 int parm_push_rows(const void* src, int nseg, int e_local, int rows, int M, const int* fill, const parm_row_fan* dst,
                    void* stream);
+
+/* `bytes` of src replicated into dst->ptr[0..n) (16-byte aligned): small payloads sent to
+ * every MP peer, e.g. S1's gate-weight gradient partials (replaces its MP all-reduce). */
+int parm_fan_copy(const void* src, long long bytes, const parm_row_fan* dst, void* stream);
 
 /* Device-side barrier of the n peers (one tiny kernel; graph-capturable). */
 int parm_peer_barrier(const parm_peer_signal* sig, void* stream);

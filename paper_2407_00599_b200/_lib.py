@@ -90,9 +90,10 @@ SIGNATURES = {
                                        ctypes.POINTER(RowFanC), _c_ll, _vp]),
     "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _vp]),
     "parm_push_rows": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, ctypes.POINTER(RowFanC), _vp]),
+    "parm_fan_copy": (_c_int, [_vp, _c_ll, ctypes.POINTER(RowFanC), _vp]),
 }
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 
 class ParmError(RuntimeError):

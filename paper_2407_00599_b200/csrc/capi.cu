@@ -40,6 +40,7 @@ int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, cons
                      const RowFan&, long long, cudaStream_t);
 int peer_barrier(const PeerSignal&, cudaStream_t);
 int push_rows(const void*, int, int, int, int, const int*, const RowFan&, cudaStream_t);
+int fan_copy(const void*, long long, const RowFan&, cudaStream_t);
 
 template <class A, class B>
 static A abi_cast(const B* v) {
@@ -173,6 +174,14 @@ int parm_push_rows(const void* src, int nseg, int e_local, int rows, int M, cons
         return 1;
     }
     return parm::push_rows(src, nseg, e_local, rows, M, fill, parm::abi_cast<parm::RowFan>(dst), S(stream));
+}
+
+int parm_fan_copy(const void* src, long long bytes, const parm_row_fan* dst, void* stream) {
+    if (!dst) {
+        parm::set_error("fan_copy: null destination fan");
+        return 1;
+    }
+    return parm::fan_copy(src, bytes, parm::abi_cast<parm::RowFan>(dst), S(stream));
 }
 
 int parm_peer_barrier(const parm_peer_signal* sig, void* stream) {

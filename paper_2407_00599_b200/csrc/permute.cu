@@ -521,6 +521,29 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
     return 0;
 }
 
+// ------------------------------------------------------------------ fan copy
+// `bytes` of src stored into each dst.ptr[i] (16-byte vectors): small payloads
+// replicated to every MP peer (the gate-gradient exchange of S1).
+__global__ void fan_copy_kernel(const int4* __restrict__ src, long long vecs, const __grid_constant__ RowFan dst) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < vecs; i += (long long)gridDim.x * blockDim.x) {
+        const int4 v = __ldg(src + i);
+        for (int f = 0; f < dst.n; ++f) reinterpret_cast<int4*>(dst.ptr[f])[i] = v;
+    }
+}
+
+int fan_copy(const void* src, long long bytes, const RowFan& dst, cudaStream_t s) {
+    PARM_CHECK_ARG(bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0,
+                   "fan_copy: %lld bytes must be 16-byte aligned and sized", bytes);
+    PARM_CHECK_ARG(dst.n >= 1 && dst.n <= kMaxPeers, "fan_copy: %d destinations", dst.n);
+    const long long vecs = bytes / 16;
+    if (vecs == 0) return 0;
+    long long blocks = (vecs + 255) / 256;
+    if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
+    fan_copy_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const int4*>(src), vecs, dst);
+    PARM_CHECK_LAUNCH("fan_copy");
+    return 0;
+}
+
 // ------------------------------------------------------------------ peer barrier
 // Every rank stores the next epoch into slot [rank] of every peer's signal pad
 // (release, system scope, after a system fence that publishes this rank's

@@ -202,6 +202,14 @@ def push_rows(src: torch.Tensor, fill: torch.Tensor, dst_ptrs: list) -> None:
     _lib.call("parm_push_rows", src.data_ptr(), nseg, el, rows, M, fill.data_ptr(), ctypes.byref(f), _stream())
 
 
+def fan_copy(src: torch.Tensor, dst_ptrs: list) -> None:
+    """Replicate the bytes of contiguous ``src`` into every address of ``dst_ptrs``."""
+    if not src.is_contiguous():
+        raise ValueError("fan_copy needs a contiguous source")
+    f = _fan(dst_ptrs)
+    _lib.call("parm_fan_copy", src.data_ptr(), src.numel() * src.element_size(), ctypes.byref(f), _stream())
+
+
 def peer_barrier(pads: list, counter: torch.Tensor, rank: int) -> None:
     """Device-side barrier of len(pads) ranks (signal-pad addresses of every rank, this rank's epoch counter)."""
     s = _lib.PeerSignalC()

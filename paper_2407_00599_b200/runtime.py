@@ -299,6 +299,8 @@ class MoELayer:
             b["y"] = torch.zeros(*shape, d.Mp, **bf)
             b["dr"] = torch.zeros(*shape, d.Mp, **bf)
         if peer:
+            if schedule == "s1" and d.MP > 1:           # MP members' gate-gradient partials [mp_pos][E][M]
+                b["gsum"], b["gsum_peers"] = W.sym((d.MP, d.E, d.Mp), torch.float32)
             if schedule == "s1" and self.peer_push:     # owners' receive blocks [holder][i][slot]
                 b["ret"], b["ret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
                 b["dret"], b["dret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
@@ -559,7 +561,6 @@ class MoELayer:
             if self.peer_push:
                 K.push_rows(b["dr"], b["fill_in"], self._push_fan(b, "dret", r))
         self.world.peer_barrier()
-        gins = {}
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s1"]
             rt = b["route"]
@@ -567,9 +568,14 @@ class MoELayer:
             K.dispatch_bwd_fan(dv, rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                                self._mp_fan(b, "dx", r), sl, d.Mp, d.Mp)
             K.gate_wgrad(b["xslice"], b["dlogits"], s.dgate, self._ws_gate)
-            gins[r] = s.dgate
-        self.world.allreduce("mp", gins)                                 # slices gate different tokens
-        self.world.peer_barrier()                                        # every MP slice of dx gathered
+            if d.MP > 1:      # slices gate different tokens: replicate the partial to every MP peer
+                off = 4 * L.mp_pos(r) * d.E * d.Mp
+                K.fan_copy(s.dgate, [b["gsum_peers"][m] + off for m in group_members(L, "mp", r)])
+        self.world.peer_barrier()                                        # dx slices and dWg partials landed
+        if d.MP > 1:
+            for r in self.ranks:                                         # fixed-order sum: identical on the group
+                s, b = self.st[r], self.st[r].bufs["s1"]
+                torch.sum(b["gsum"], dim=0, out=s.dgate)
         return {r: self.st[r].bufs["s1"]["dx"][:, :d.M] for r in self.ranks}
 
     # ------------------------------------------------------------ S1
