@@ -441,7 +441,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         if os.environ.get("PARM_PEER", "1") != "0":
             try:
                 w = PeerWorld(layout, dev)
-                transport = "nvlink-peer (S1, S2) + nccl (baseline, dWg all-reduce)"
+                transport = "nvlink-peer (S1, S2) + nccl (baseline)"
             except Exception as exc:   # symmetric memory unavailable: NCCL for every exchange
                 print(f"peer memory unavailable ({exc}); using NCCL", file=sys.stderr)
         if w is None:
