@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 9
+#define PARM_ABI_VERSION 10
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -209,6 +209,13 @@ typedef struct parm_gemm_desc {
 } parm_gemm_desc;
 
 int parm_gemm(const parm_gemm_desc* desc, void* stream);
+
+/* ROW GEMM whose output rows of segment (hi, lo) go straight to seg_dst->ptr[hi * nlo + lo]
+ * + g * dst_g_stride + r * dst_ld (elements; bf16 epilogues): with peer addresses the
+ * expert output is stored into every owner's receive block from the epilogue -- the
+ * return AlltoAll (collectives.py:286-295) fused into the GEMM, tile by tile. */
+int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,7 @@ int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const vo
                  long long, cudaStream_t);
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
 int moe_gemm(const parm_gemm_desc&, cudaStream_t);
+int moe_gemm_peer(const parm_gemm_desc&, const RowFan*, long long, long long, cudaStream_t);
 int dispatch_rows_peer(const void*, long long, const int*, const float*, int, int, int, int, int, int,
                        const SlotView&, const int*, const IntFan*, cudaStream_t);
 int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, int, int, const RowFan&, long long,
@@ -198,6 +199,16 @@ int parm_gemm(const parm_gemm_desc* desc, void* stream) {
         return 1;
     }
     return parm::moe_gemm(*desc, S(stream));
+}
+
+int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld,
+                   void* stream) {
+    if (!desc || !seg_dst) {
+        parm::set_error("gemm_peer: null descriptor or destination fan");
+        return 1;
+    }
+    const parm::RowFan fan = parm::abi_cast<parm::RowFan>(seg_dst);
+    return parm::moe_gemm_peer(*desc, &fan, dst_g_stride, dst_ld, S(stream));
 }
 
 }  // extern "C"

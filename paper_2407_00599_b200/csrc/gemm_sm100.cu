@@ -55,6 +55,15 @@ struct Params {
     int pairs;                 // CTA-pair kernel: max 256-row pair tiles per group
     int debug;                 // PARM_GEMM_DEBUG bits (perf experiments only): 1 = no epilogue stores, 2 = no TMA,
                                // 4 = no MMA (pair kernel)
+    int seg_peer;              // ROW: rows of segment (hi, lo) stored into seg_dst[hi * nlo + lo] (peer buffers)
+    bf16* seg_dst[kMaxPeers];  //   + g * sd_g + r * sd_ld + n -- the return AlltoAll fused into the epilogue
+    long long sd_g, sd_ld;
+};
+
+// Per-segment 3-D store maps (N, rows, G) over peer destinations: the TMA-store
+// epilogue writes each output tile straight into its owner's receive block.
+struct SegMaps {
+    CUtensorMap m[kMaxPeers];
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -230,7 +239,7 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const int* sfil
 // processed, so its global-load latency is exposed once per tile, not per chunk.
 template <int BN, int EPI>
 __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long long drow, long long xrow,
-                                           bool row_ok, int n0, bool empty) {
+                                           bool row_ok, int n0, bool empty, void* dbase) {
     constexpr int NC = BN / 32;
     int4 ax_next[4];
     if (EPI == kEpiDReluBF16 && row_ok) {
@@ -260,7 +269,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long
         if (!row_ok || (p.debug & 1)) continue;
         const int col = n0 + c * 32;
         if (EPI == kEpiF32 || EPI == kEpiF32Acc) {
-            float* dst = reinterpret_cast<float*>(p.D) + drow + col;
+            float* dst = reinterpret_cast<float*>(dbase) + drow + col;
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
                 float4 o = make_float4(p.alpha * __uint_as_float(r[4 * v]), p.alpha * __uint_as_float(r[4 * v + 1]),
@@ -276,7 +285,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long
                 reinterpret_cast<float4*>(dst)[v] = o;
             }
         } else {
-            bf16* dst = reinterpret_cast<bf16*>(p.D) + drow + col;
+            bf16* dst = reinterpret_cast<bf16*>(dbase) + drow + col;
             float f[32];
 #pragma unroll
             for (int v = 0; v < 32; ++v) f[v] = p.alpha * __uint_as_float(r[v]);
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
-            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
+            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty, p.D);
             tc_fence_before();
             mbar_arrive(&tempty_bar[as]);
         }
@@ -671,7 +680,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 template <int BN, int KIND, int EPI>
 __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMap* tmap_d, uint32_t taddr, int lane,
                                                int row0, int g, int lo, int hi, int n0, bool row_ok, long long xrow,
-                                               bool empty, uint8_t* stage, int& buf) {
+                                               bool empty, uint8_t* stage, int& buf,
+                                               const CUtensorMap* seg_map = nullptr) {
     constexpr bool F32 = (EPI == kEpiF32 || EPI == kEpiF32Acc);
     constexpr int COLS = F32 ? 32 : 64;          // output columns per 128-byte chunk
     constexpr int NCH = BN / COLS;
@@ -738,7 +748,9 @@ __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMa
         __syncwarp();
         if (lane == 0) {
             const int col = n0 + ch * COLS;
-            if (KIND == kRow)
+            if (KIND == kRow && seg_map != nullptr)
+                tma_store_3d(seg_map, sbuf, col, row0, g);
+            else if (KIND == kRow)
                 tma_store_5d(tmap_d, sbuf, col, row0, g, lo, hi);
             else if (EPI == kEpiF32Acc)
                 tma_reduce_add_3d(tmap_d, sbuf, col, row0, g);
@@ -766,7 +778,8 @@ struct CfgPair {
 template <int BN, int KIND, int MB, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                         const __grid_constant__ CUtensorMap tmap_d, const Params p) {
+                         const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ Params p,
+                         const __grid_constant__ SegMaps segmaps) {
     using C = CfgPair<BN, KIND, MB, EPI>;
     constexpr int STAGES = C::kStages;
     constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
@@ -946,8 +959,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
             (void)drow;
-            if (p.debug & 1) {
-                drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty);
+            if (KIND == kRow && p.seg_peer == 2) {   // TMA stores straight into the owner's receive block
+                drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
+                                              xrow, empty, my_stage, ebuf, &segmaps.m[t.hi * p.nlo + t.lo]);
+            } else if (KIND == kRow && p.seg_peer) {   // per-thread stores into the owner's receive block
+                const long long prow = (long long)t.g * p.sd_g + (long long)row * p.sd_ld;
+                drain_tile<BN, EPI>(p, taddr, prow, xrow, row_ok, t.n0, empty, p.seg_dst[t.hi * p.nlo + t.lo]);
+            } else if (p.debug & 1) {
+                drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty, p.D);
             } else {
                 drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
                                               xrow, empty, my_stage, ebuf);
@@ -1029,6 +1048,8 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
     return 0;
 }
 
+static SegMaps g_segmaps;   // per-call store maps of moe_gemm_peer (host calls are stream-ordered, one thread)
+
 template <int BN, int KIND, int MB, int EPI>
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const Params& p,
                        cudaStream_t stream) {
@@ -1041,7 +1062,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
     }
     int grid = 2 * (p.num_tiles < kNumSMs / 2 ? p.num_tiles : kNumSMs / 2);   // clusters of 2 CTAs
     if (grid < 2) grid = 2;
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, td, p);
+    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, td, p, g_segmaps);
     PARM_CHECK_LAUNCH("moe_gemm_pair");
     return 0;
 }
@@ -1070,7 +1091,12 @@ static bool pair_mode() {
 
 }  // namespace gemm
 
-int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
+int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g, long long sd_ld, cudaStream_t stream);
+
+int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) { return moe_gemm_peer(q, nullptr, 0, 0, stream); }
+
+int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g, long long sd_ld,
+                  cudaStream_t stream) {
     using namespace gemm;
     PARM_CHECK_ARG(q.kind == kRow || q.kind == kWgt, "gemm: bad kind %d", q.kind);
     PARM_CHECK_ARG(q.groups > 0 && q.nhi > 0 && q.nlo > 0 && q.seg_len > 0, "gemm: empty row space");
@@ -1095,6 +1121,31 @@ int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) {
             dbg = e ? atoi(e) : 0;
         }
         p.debug = dbg;
+    }
+    p.seg_peer = 0;
+    p.sd_g = p.sd_ld = 0;
+    for (int i = 0; i < kMaxPeers; ++i) p.seg_dst[i] = nullptr;
+    if (seg_dst != nullptr) {
+        PARM_CHECK_ARG(q.kind == kRow && (q.epi == kEpiBF16 || q.epi == kEpiReluBF16),
+                       "gemm: peer segment outputs need a ROW GEMM with a bf16 epilogue");
+        PARM_CHECK_ARG(seg_dst->n == q.nhi * q.nlo, "gemm: %d peer outputs for %d segments", seg_dst->n,
+                       q.nhi * q.nlo);
+        PARM_CHECK_ARG(pair_mode(), "gemm: peer segment outputs need the CTA-pair kernel");
+        PARM_CHECK_ARG(sd_ld % 8 == 0 && sd_g % 8 == 0, "gemm: peer output rows must be 16-byte aligned");
+        static int mode = -1;     // PARM_GEMM_PEER_STORES=thread: per-thread stores instead of TMA stores
+        if (mode < 0) {
+            const char* e = getenv("PARM_GEMM_PEER_STORES");
+            mode = (e && e[0] == 't') ? 1 : 2;
+        }
+        p.seg_peer = mode;
+        for (int i = 0; i < seg_dst->n; ++i) {
+            p.seg_dst[i] = seg_dst->ptr[i];
+            const long long dd[3] = {q.N, q.seg_len, q.groups};
+            const long long ds[2] = {sd_ld, sd_g};
+            if (int rc = make_tmap(&g_segmaps.m[i], seg_dst->ptr[i], 3, dd, ds, 32, 2, 64)) return rc;
+        }
+        p.sd_g = sd_g;
+        p.sd_ld = sd_ld;
     }
     p.D = const_cast<void*>(q.d.ptr);
     p.d_ld = q.d.ld;

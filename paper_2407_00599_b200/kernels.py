@@ -273,23 +273,35 @@ def _rows(t: torch.Tensor | None) -> _lib.RowsC:
     raise ValueError(f"GEMM operand must be 3-D or 5-D, got {t.dim()}-D")
 
 
-def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill, flops) -> None:
+def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill, flops, peer=None) -> None:
     desc = _lib.GemmDescC(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, float(alpha), 0, _rows(a), _rows(b),
                           _rows(d), _rows(aux), _ptr(fill))
+
+    def launch():
+        if peer is None:
+            _lib.call("parm_gemm", ctypes.byref(desc), _stream())
+        else:
+            ptrs, g_stride, ld = peer
+            f = _fan(ptrs)
+            _lib.call("parm_gemm_peer", ctypes.byref(desc), ctypes.byref(f), g_stride, ld, _stream())
+
     if gemm_timer is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.call("parm_gemm", ctypes.byref(desc), _stream())
+        launch()
         e1.record()
         gemm_timer.pairs.append((e0, e1, flops))
         return
-    _lib.call("parm_gemm", ctypes.byref(desc), _stream())
+    launch()
 
 
 def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, epi: int,
-              aux: torch.Tensor | None = None, fill: torch.Tensor | None = None, alpha: float = 1.0) -> None:
-    """ROW GEMM: D[hi][lo][g][r][n] = alpha * A[hi][lo][g][r][:] . B[g][n][:] (5-D A/D, 3-D weights B)."""
+              aux: torch.Tensor | None = None, fill: torch.Tensor | None = None, alpha: float = 1.0,
+              peer: tuple | None = None) -> None:
+    """ROW GEMM: D[hi][lo][g][r][n] = alpha * A[hi][lo][g][r][:] . B[g][n][:] (5-D A/D, 3-D weights B).
+    ``peer=(addresses, g_stride, ld)``: rows of segment hi*nlo+lo go to addresses[seg] + g*g_stride + r*ld
+    instead of D (the epilogue stores into the owners' receive blocks over NVLink)."""
     _need(a, torch.bfloat16, "A")
     _need(b, torch.bfloat16, "B")
     _need(d, torch.bfloat16, "D")
@@ -300,7 +312,7 @@ def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, e
     if aux is not None and tuple(aux.shape) != tuple(d.shape):
         raise ValueError("aux must be shaped like D")
     _gemm(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill,
-          2 * nhi * nlo * G * L * N * Kd)
+          2 * nhi * nlo * G * L * N * Kd, peer)
 
 
 def gemm_wgrad(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epi: int = EPI_F32,

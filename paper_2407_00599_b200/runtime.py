@@ -170,6 +170,8 @@ class MoELayer:
         # S2 pushes MP copies of every row (its AllGather), measured no faster than the owners'
         # gathers through the slot-shard view (N=4: 0.85 vs 0.84 ms), so S2 pulls by default
         self.peer_push_s2 = os.environ.get("PARM_PEER_RETURN_S2", "pull") == "push"
+        # S1 push from the GEMM epilogue itself (tile by tile, overlapping the math) instead of a copy kernel
+        self.peer_epilogue = os.environ.get("PARM_PEER_EPILOGUE", "1") != "0"
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -343,16 +345,16 @@ class MoELayer:
         return b[key]
 
     # ------------------------------------------------------------ FFN
-    def _ffn_fwd(self, s: RankState, b: dict) -> None:
+    def _ffn_fwd(self, s: RankState, b: dict, y_peer: tuple | None = None) -> None:
         K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU, fill=b["fill_in"])
-        K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"])
+        K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"], peer=y_peer)
 
-    def _ffn_bwd(self, s: RankState, b: dict, wscale: float = 1.0) -> None:
+    def _ffn_bwd(self, s: RankState, b: dict, wscale: float = 1.0, dr_peer: tuple | None = None) -> None:
         f = b["fill_in"]
         K.gemm_rows(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DRELU, aux=b["h"], fill=f)
         K.gemm_wgrad(b["dyrecv"], b["h"], s.dw2t, K.EPI_F32, fill=f, alpha=wscale)
         K.gemm_wgrad(b["dh"], b["recv"], s.dw1t, K.EPI_F32, fill=f, alpha=wscale)
-        K.gemm_rows(b["dh"], s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16, fill=f)
+        K.gemm_rows(b["dh"], s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16, fill=f, peer=dr_peer)
 
     # ------------------------------------------------------------ message plans
     def _owned(self, *ranks) -> bool:
@@ -500,6 +502,11 @@ class MoELayer:
         return K.SlotView(None, e_local=el, n_p=d.ESP, stride_i=q * d.Mp, stride_slo=d.Mp,
                           peers=tuple(a + off for a in b[key + "_peers"]), peer_ep=pe, peer_p=pp)
 
+    def _epi_peer(self, b: dict, key: str, h: int) -> tuple:
+        """GEMM-epilogue destinations: segment src of holder h's output -> owner src's block [h]."""
+        d = self.d
+        return (self._push_fan(b, key, h), b["q"] * d.Mp, d.Mp)
+
     def _push_fan(self, b: dict, key: str, h: int) -> list[int]:
         """Holder h's block in every owner's (P, e_local, q, M) receive buffer `key` (segment = owner)."""
         d = self.d
@@ -528,9 +535,12 @@ class MoELayer:
         self.world.peer_barrier()                                     # receive buffers complete
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
-            self._ffn_fwd(self.st[r], b)
-            if self.peer_push:
-                K.push_rows(b["y"], b["fill_in"], self._push_fan(b, "ret", r))
+            if self.peer_push and self.peer_epilogue:      # the second GEMM stores into the owners directly
+                self._ffn_fwd(self.st[r], b, y_peer=self._epi_peer(b, "ret", r))
+            else:
+                self._ffn_fwd(self.st[r], b)
+                if self.peer_push:
+                    K.push_rows(b["y"], b["fill_in"], self._push_fan(b, "ret", r))
         self.world.peer_barrier()                                     # expert outputs complete / delivered
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
@@ -557,9 +567,12 @@ class MoELayer:
         self.world.peer_barrier()
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
-            self._ffn_bwd(self.st[r], b)
-            if self.peer_push:
-                K.push_rows(b["dr"], b["fill_in"], self._push_fan(b, "dret", r))
+            if self.peer_push and self.peer_epilogue:
+                self._ffn_bwd(self.st[r], b, dr_peer=self._epi_peer(b, "dret", r))
+            else:
+                self._ffn_bwd(self.st[r], b)
+                if self.peer_push:
+                    K.push_rows(b["dr"], b["fill_in"], self._push_fan(b, "dret", r))
         self.world.peer_barrier()
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["s1"]
