@@ -599,14 +599,24 @@ struct PairTile {
 };
 
 __device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfill, int tile, int kind, int bn,
-                                               uint32_t rank) {
+                                               uint32_t rank, const int* sprefix) {
     PairTile t;
-    const int per_g = p.pairs * p.n_blocks;     // pairs = max 256-row pair tiles per group
-    t.g = tile / per_g;
-    const int rem = tile - t.g * per_g;
-    const int pj = rem / p.n_blocks;
-    t.n0 = (rem % p.n_blocks) * bn;
+    int pj;
     t.hi = t.lo = 0;
+    if (kind == kRow) {   // tile = live pair-tile index: groups' live row pairs, compacted (sprefix)
+        const int pu = tile / p.n_blocks;
+        t.n0 = (tile - pu * p.n_blocks) * bn;
+        int g = 0;
+        while (sprefix[g + 1] <= pu) ++g;
+        t.g = g;
+        pj = pu - sprefix[g];
+    } else {
+        const int per_g = p.pairs * p.n_blocks;
+        t.g = tile / per_g;
+        const int rem = tile - t.g * per_g;
+        pj = rem / p.n_blocks;
+        t.n0 = (rem % p.n_blocks) * bn;
+    }
     if (kind == kRow) {
         int h0, l0, m00;
         t.live = nth_live_row_tile(p, sfill, t.g, 2 * pj, h0, l0, m00);
@@ -802,6 +812,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
     if (p.fill)
         for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
+    // ROW: work list = live 256-row pair tiles only (groups' live row pairs, prefix-summed), so the
+    // static round-robin over the 74 pairs balances the real work instead of an index space with
+    // unfilled capacity holes (max 5 vs the ideal 4 tiles per pair measured on the second GEMM).
+    int* sprefix = sfill + p.G * p.nhi * p.nlo;
+    if (KIND == kRow) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            sprefix[0] = 0;
+            for (int g = 0; g < p.G; ++g) {
+                int lt = 0;
+                for (int seg = 0; seg < p.nhi * p.nlo; ++seg) {
+                    const int h = seg / p.nlo, l = seg - h * p.nlo;
+                    int live = (seg_fill(p, sfill, g, h, l) + BM - 1) / BM;
+                    lt += live > p.m_tiles ? p.m_tiles : live;
+                }
+                acc += (lt + 1) / 2;
+                sprefix[g + 1] = acc;
+            }
+        }
+    }
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x >> 1;
@@ -831,14 +862,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int ntiles = (KIND == kRow) ? sprefix[p.G] * p.n_blocks : p.num_tiles;
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
-                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+            for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
+                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
                 if (!t.live) continue;
                 for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -895,8 +927,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it_tile = 0;
-            for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
-                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+            for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
+                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
                 if (!t.live) continue;
                 const int as = it_tile & 1;
                 const uint32_t aphase = (it_tile >> 1) & 1;
@@ -932,8 +964,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int it_tile = 0;
         int ebuf = 0;
         uint8_t* my_stage = smem_epi + ew * kEpiBufs * kEpiStageBytes;
-        for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
-            const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank);
+        for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
+            const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
             if (!t.live) continue;
             const int as = it_tile & 1;
             const uint32_t aphase = (it_tile >> 1) & 1;
@@ -1103,7 +1135,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     PARM_CHECK_ARG(q.N > 0 && q.N % 64 == 0, "gemm: N=%d must be a positive multiple of 64", q.N);
     PARM_CHECK_ARG(q.epi >= 0 && q.epi <= 4, "gemm: bad epilogue %d", q.epi);
     PARM_CHECK_ARG(q.epi != kEpiDReluBF16 || q.aux.ptr != nullptr, "gemm: relu-mask epilogue needs aux");
-    PARM_CHECK_ARG(q.fill == nullptr || q.groups * q.nhi * q.nlo <= kMaxFill, "gemm: fill table too large");
+    PARM_CHECK_ARG(q.groups * q.nhi * q.nlo + q.groups + 1 <= kMaxFill, "gemm: fill table too large");
     Params p;
     p.G = q.groups;
     p.nhi = q.nhi;
