@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 10
+#define PARM_ABI_VERSION 11
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -182,7 +182,9 @@ typedef struct parm_rows {
  * (every row tensor is the AlltoAll receive layout [src_hi][src_lo][expert][r < seg_len][col]).
  * kind 0 (ROW):  D[hi][lo][g][r][n] = alpha * sum_k A[hi][lo][g][r][k] * B[g][n][k]
  *                b_major 0: B stored [g][n][k]; 1: B stored [g][k][n].  K, N % 64 == 0.
- *                epi 0 bf16, 1 relu -> bf16, 2 keep where aux > 0 -> bf16 (aux shaped like D).
+ *                epi 0 bf16, 1 relu -> bf16, 2 keep where aux > 0 -> bf16 (aux shaped like D),
+ *                5 relu -> bf16 and aux (u32 rows of N/32 words) <- bit mask of the stored
+ *                values > 0, 6 keep where that bit mask is set -> bf16.
  * kind 1 (WGT):  D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n]
  *                M % 128 == 0, N % 64 == 0; epi 3 f32, 4 f32 accumulate.
  * fill (nullable, int32 [hi][lo][g]): rows >= fill of a segment are skipped

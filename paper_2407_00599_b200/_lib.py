@@ -94,7 +94,7 @@ SIGNATURES = {
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 
 class ParmError(RuntimeError):

@@ -35,7 +35,21 @@ namespace gemm {
 
 enum Major : int { kKMajor = 0, kMNMajor = 1 };
 enum Kind : int { kRow = 0, kWgt = 1 };
-enum Epi : int { kEpiBF16 = 0, kEpiReluBF16 = 1, kEpiDReluBF16 = 2, kEpiF32 = 3, kEpiF32Acc = 4 };
+enum Epi : int {
+    kEpiBF16 = 0,
+    kEpiReluBF16 = 1,
+    kEpiDReluBF16 = 2,      // keep where aux (bf16, shaped like D) > 0
+    kEpiF32 = 3,
+    kEpiF32Acc = 4,
+    kEpiReluMaskBF16 = 5,   // relu, and aux (u32 [rows][N/32]) receives the bit mask of the stored value > 0
+    kEpiDMaskBF16 = 6,      // keep where the aux bit mask is set (1/16 of kEpiDReluBF16's aux bytes)
+};
+
+__device__ __forceinline__ uint32_t bf16_pos_bits(uint32_t packed) {   // bit0: low half > 0, bit1: high half > 0
+    const uint32_t lo = packed & 0xFFFFu, hi = packed >> 16;
+    return (uint32_t)((lo & 0x8000u) == 0 && (lo & 0x7FFFu) != 0) |
+           ((uint32_t)((hi & 0x8000u) == 0 && (hi & 0x7FFFu) != 0) << 1);
+}
 
 constexpr int BM = 128;
 constexpr int BK = 64;
@@ -241,6 +255,7 @@ template <int BN, int EPI>
 __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long long drow, long long xrow,
                                            bool row_ok, int n0, bool empty, void* dbase) {
     constexpr int NC = BN / 32;
+    uint32_t* mrow = reinterpret_cast<uint32_t*>(const_cast<bf16*>(p.aux)) + xrow + n0 / 32;   // mask epilogues
     int4 ax_next[4];
     if (EPI == kEpiDReluBF16 && row_ok) {
         const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0);
@@ -304,8 +319,27 @@ __device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long
                     for (int u = 0; u < 8; ++u) f[8 * v + u] = a[u] > 0.0f ? f[8 * v + u] : 0.0f;
                 }
             }
+            if (EPI == kEpiDMaskBF16) {
+                const uint32_t m = __ldg(mrow + c);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) st_vec8(dst + 8 * v, f32_to_vec8(f + 8 * v));
+                for (int v = 0; v < 32; ++v) f[v] = ((m >> v) & 1u) ? f[v] : 0.0f;
+            }
+            if (EPI == kEpiReluMaskBF16) {
+#pragma unroll
+                for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
+            }
+            uint32_t bits = 0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const Vec8 o8 = f32_to_vec8(f + 8 * v);
+                st_vec8(dst + 8 * v, o8);
+                if (EPI == kEpiReluMaskBF16) {
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(&o8);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) bits |= bf16_pos_bits(w[u]) << (8 * v + 2 * u);
+                }
+            }
+            if (EPI == kEpiReluMaskBF16) mrow[c] = bits;
         }
     }
 }
@@ -695,6 +729,9 @@ __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMa
     constexpr bool F32 = (EPI == kEpiF32 || EPI == kEpiF32Acc);
     constexpr int COLS = F32 ? 32 : 64;          // output columns per 128-byte chunk
     constexpr int NCH = BN / COLS;
+    uint2* mrow = reinterpret_cast<uint2*>(reinterpret_cast<uint32_t*>(const_cast<bf16*>(p.aux)) + xrow + n0 / 32);
+    uint2 mk_next = make_uint2(0u, 0u);
+    if (EPI == kEpiDMaskBF16 && row_ok) mk_next = __ldg(mrow);
     int4 ax_next[8];
     if (EPI == kEpiDReluBF16 && row_ok) {
         const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0);
@@ -721,6 +758,8 @@ __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMa
                     for (int v = 0; v < 8; ++v) ax_next[v] = __ldg(src + v);
                 }
             }
+            uint2 mk = mk_next;
+            if (EPI == kEpiDMaskBF16 && row_ok && ch + 1 < NCH) mk_next = __ldg(mrow + ch + 1);
             uint32_t r0[32], r1[32];
             PARM_TMEM_LD32(taddr + ch * 64, r0);
             PARM_TMEM_LD32(taddr + ch * 64 + 32, r1);
@@ -739,7 +778,25 @@ __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMa
                     a = ma > 0.0f ? a : 0.0f;
                     b = mb > 0.0f ? b : 0.0f;
                 }
+                if (EPI == kEpiDMaskBF16) {
+                    const uint32_t w = v < 16 ? mk.x : mk.y;
+                    const int bit = (2 * v) & 31;
+                    a = ((w >> bit) & 1u) ? a : 0.0f;
+                    b = ((w >> (bit + 1)) & 1u) ? b : 0.0f;
+                }
+                if (EPI == kEpiReluMaskBF16) {
+                    a = fmaxf(a, 0.0f);
+                    b = fmaxf(b, 0.0f);
+                }
                 pk[v] = pack_bf16x2(a, b);
+            }
+            if (EPI == kEpiReluMaskBF16 && row_ok) {   // bit per stored value > 0, two words per chunk
+                uint32_t w0 = 0u, w1 = 0u;
+#pragma unroll
+                for (int v = 0; v < 16; ++v) w0 |= bf16_pos_bits(pk[v]) << (2 * v);
+#pragma unroll
+                for (int v = 0; v < 16; ++v) w1 |= bf16_pos_bits(pk[16 + v]) << (2 * v);
+                mrow[ch] = make_uint2(w0, w1);
             }
         }
         uint8_t* sbuf = stage + buf * kEpiStageBytes;
@@ -1133,8 +1190,12 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     PARM_CHECK_ARG(q.kind == kRow || q.kind == kWgt, "gemm: bad kind %d", q.kind);
     PARM_CHECK_ARG(q.groups > 0 && q.nhi > 0 && q.nlo > 0 && q.seg_len > 0, "gemm: empty row space");
     PARM_CHECK_ARG(q.N > 0 && q.N % 64 == 0, "gemm: N=%d must be a positive multiple of 64", q.N);
-    PARM_CHECK_ARG(q.epi >= 0 && q.epi <= 4, "gemm: bad epilogue %d", q.epi);
-    PARM_CHECK_ARG(q.epi != kEpiDReluBF16 || q.aux.ptr != nullptr, "gemm: relu-mask epilogue needs aux");
+    PARM_CHECK_ARG(q.epi >= 0 && q.epi <= 6, "gemm: bad epilogue %d", q.epi);
+    PARM_CHECK_ARG((q.epi != kEpiDReluBF16 && q.epi != kEpiReluMaskBF16 && q.epi != kEpiDMaskBF16) ||
+                       q.aux.ptr != nullptr, "gemm: relu-mask epilogue needs aux");
+    PARM_CHECK_ARG((q.epi != kEpiReluMaskBF16 && q.epi != kEpiDMaskBF16) ||
+                       ((reinterpret_cast<uintptr_t>(q.aux.ptr) & 7) == 0 && q.N % 64 == 0 && q.aux.ld % 2 == 0),
+                   "gemm: bit-mask aux must be 8-byte aligned with N %% 64 == 0");
     PARM_CHECK_ARG(q.groups * q.nhi * q.nlo + q.groups + 1 <= kMaxFill, "gemm: fill table too large");
     Params p;
     p.G = q.groups;
@@ -1205,7 +1266,8 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     }
     if (q.kind == kRow) {
         PARM_CHECK_ARG(q.K > 0 && q.K % BK == 0, "gemm: K=%d must be a positive multiple of %d", q.K, BK);
-        PARM_CHECK_ARG(q.epi <= kEpiDReluBF16, "gemm: row GEMMs produce bf16");
+        PARM_CHECK_ARG(q.epi <= kEpiDReluBF16 || q.epi == kEpiReluMaskBF16 || q.epi == kEpiDMaskBF16,
+                       "gemm: row GEMMs produce bf16");
         p.m_tiles = (q.seg_len + BM - 1) / BM;
         p.pairs = (p.nhi * p.nlo * p.m_tiles + 1) / 2;
         p.num_tiles = pair ? p.G * p.pairs * p.n_blocks : p.G * p.nhi * p.nlo * p.m_tiles * p.n_blocks;
@@ -1227,9 +1289,12 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
         const int combo = q.b_major;
         if (combo == kKMajor) {
             if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiReluMaskBF16)
+                return dispatch_bn<kRow, kKMajor, kEpiReluMaskBF16>(pair, bn, ta, tb, td, p, stream);
             if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
         } else {
             if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiDMaskBF16) return dispatch_bn<kRow, kMNMajor, kEpiDMaskBF16>(pair, bn, ta, tb, td, p, stream);
             if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
         }
     } else {

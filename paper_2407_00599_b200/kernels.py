@@ -14,7 +14,7 @@ import torch
 from . import _lib
 
 KMAJOR, MNMAJOR = 0, 1
-EPI_BF16, EPI_RELU, EPI_DRELU, EPI_F32, EPI_F32_ACC = 0, 1, 2, 3, 4
+EPI_BF16, EPI_RELU, EPI_DRELU, EPI_F32, EPI_F32_ACC, EPI_RELU_MASK, EPI_DMASK = 0, 1, 2, 3, 4, 5, 6
 
 
 def _stream(stream: torch.cuda.Stream | None = None) -> int:
@@ -309,7 +309,10 @@ def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, e
     N = b.shape[1] if b_major == KMAJOR else b.shape[2]
     if tuple(d.shape) != (nhi, nlo, G, L, N) or b.shape[0] != G:
         raise ValueError(f"gemm_rows shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
-    if aux is not None and tuple(aux.shape) != tuple(d.shape):
+    if epi in (EPI_RELU_MASK, EPI_DMASK):
+        if aux is None or aux.dtype != torch.int32 or tuple(aux.shape) != (nhi, nlo, G, L, N // 32):
+            raise ValueError("bit-mask epilogues need an int32 aux of shape D[..., N/32]")
+    elif aux is not None and tuple(aux.shape) != tuple(d.shape):
         raise ValueError("aux must be shaped like D")
     _gemm(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill,
           2 * nhi * nlo * G * L * N * Kd, peer)

@@ -293,6 +293,7 @@ class MoELayer:
             b["dg"] = torch.zeros(d.ESP, d.n, d.Mp, **bf)
             shape = (d.EP, d.ESP, el, d.T)
         b["h"] = torch.zeros(*shape, d.Hsp, **bf)
+        b["hmask"] = torch.zeros(*shape, d.Hsp // 32, dtype=torch.int32, device=dev)   # H > 0, one bit each
         b["dh"] = torch.zeros(*shape, d.Hsp, **bf)
         if peer:             # expert outputs, gathered by the owners' combine / dispatch-backward kernels
             b["y"], b["y_peers"] = W.sym((*shape, d.Mp))
@@ -346,12 +347,13 @@ class MoELayer:
 
     # ------------------------------------------------------------ FFN
     def _ffn_fwd(self, s: RankState, b: dict, y_peer: tuple | None = None) -> None:
-        K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU, fill=b["fill_in"])
+        K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=b["fill_in"])
         K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"], peer=y_peer)
 
     def _ffn_bwd(self, s: RankState, b: dict, wscale: float = 1.0, dr_peer: tuple | None = None) -> None:
         f = b["fill_in"]
-        K.gemm_rows(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DRELU, aux=b["h"], fill=f)
+        # ReLU' from the bit mask the forward GEMM wrote (1/16 of re-reading H)
+        K.gemm_rows(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DMASK, aux=b["hmask"], fill=f)
         K.gemm_wgrad(b["dyrecv"], b["h"], s.dw2t, K.EPI_F32, fill=f, alpha=wscale)
         K.gemm_wgrad(b["dh"], b["recv"], s.dw1t, K.EPI_F32, fill=f, alpha=wscale)
         K.gemm_rows(b["dh"], s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16, fill=f, peer=dr_peer)

@@ -32,7 +32,32 @@ def check(G, M, N, Kd, ma, mb, epi):
     print(f"G={G} M={M} N={N} K={Kd} ma={ma} mb={mb} epi={epi}: rel_err={err:.3e} {'OK' if ok else 'FAIL'}", flush=True)
     return ok
 
+def check_mask(G, M, N, Kd):
+    """ReLU bit-mask epilogues: fwd writes relu(x w) + bits, bwd keeps dy w^T where the bit is set."""
+    u = lambda t: t.unsqueeze(0).unsqueeze(0)
+    x = torch.randn(G, M, Kd, device=dev).bfloat16(); w = torch.randn(G, N, Kd, device=dev).bfloat16()
+    h = torch.empty(G, M, N, device=dev, dtype=torch.bfloat16)
+    mask = torch.zeros(G, M, N // 32, device=dev, dtype=torch.int32)
+    K.gemm_rows(u(x), w, K.KMAJOR, u(h), K.EPI_RELU_MASK, aux=u(mask))
+    wb = torch.randn(G, N, Kd, device=dev).bfloat16()          # MN-major B for the masked GEMM: (G, K=Kd?, N)
+    dy = torch.randn(G, M, Kd, device=dev).bfloat16()
+    bm = torch.randn(G, Kd, N, device=dev).bfloat16()
+    dh = torch.empty(G, M, N, device=dev, dtype=torch.bfloat16)
+    K.gemm_rows(u(dy), bm, K.MNMAJOR, u(dh), K.EPI_DMASK, aux=u(mask))
+    torch.cuda.synchronize()
+    ref_h = torch.bmm(x.float(), w.float().transpose(1, 2)).clamp_min(0)
+    bits = ((mask.unsqueeze(-1) >> torch.arange(32, device=dev)) & 1).reshape(G, M, N).bool()
+    ok1 = torch.equal(bits, h.float() > 0)
+    ref_dh = torch.where(h.float() > 0, torch.bmm(dy.float(), bm.float()), torch.zeros_like(ref_h))
+    e1 = (h.float() - ref_h).abs().max().item() / max(1.0, ref_h.abs().max().item())
+    e2 = (dh.float() - ref_dh).abs().max().item() / max(1.0, ref_dh.abs().max().item())
+    ok = ok1 and e1 < 1e-2 and e2 < 1e-2
+    print(f"mask G={G} M={M} N={N} K={Kd}: bits_exact={ok1} fwd={e1:.3e} bwd={e2:.3e} {'OK' if ok else 'FAIL'}", flush=True)
+    return ok
+
 allok = True
+for (G, M, N, Kd) in [(1,128,64,64),(2,256,128,128),(3,512,512,320)]:
+    allok &= check_mask(G, M, N, Kd)
 for (ma, mb, epi) in [(0,0,1),(0,0,0),(0,1,2),(0,1,0),(1,1,3),(1,1,4)]:
     for (G, M, N, Kd) in [(1,128,64,64),(2,256,128,128),(2,384,256,192),(3,512,512,320)]:
         allok &= check(G, M, N, Kd, ma, mb, epi)
