@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
                                                                  int k, int* __restrict__ expert_idx,
                                                                  float* __restrict__ combine_w,
                                                                  float* __restrict__ probs) {
+    pdl_entry();
     constexpr int TPW = 32 / EMAX;
     const int lane = threadIdx.x & 31;
     const int warp_global = (blockIdx.x * kGateThreads + threadIdx.x) >> 5;
@@ -225,6 +226,7 @@ template <int NT>   // n-tiles of 8 experts (E <= 8 NT)
 __global__ void __launch_bounds__(kDmmaWarps * 32) gate_fwd_dmma_kernel(
     const bf16* __restrict__ x, long long ldx, const double* __restrict__ wgT, int n, int M, int E, int k,
     int* __restrict__ expert_idx, float* __restrict__ combine_w, float* __restrict__ probs) {
+    pdl_entry();
     __shared__ double red[kDmmaWarps][NT][64];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
@@ -310,6 +312,7 @@ template <int NT>
 __global__ void __launch_bounds__(kGateSmemWarps * 32) gate_fwd_dmma_smem_kernel(
     const bf16* __restrict__ x, long long ldx, const double* __restrict__ wgT, int n, int M, int E, int k,
     int* __restrict__ expert_idx, float* __restrict__ combine_w, float* __restrict__ probs) {
+    pdl_entry();
     extern __shared__ double sw[];
     const int Q = M / 4;
     const long long stride = gate_smem_stride(M);
@@ -408,6 +411,7 @@ template <int EMAX>
 __global__ void __launch_bounds__(kSlotChunk) slot_count_kernel(const int* __restrict__ expert_idx, int n, int k,
                                                                  int E, int cap, int* __restrict__ chunk_cnt,
                                                                  int* __restrict__ slot_src) {
+    pdl_entry();
     __shared__ int wc[kSlotWarps][EMAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long tot = (long long)E * cap;
@@ -434,6 +438,7 @@ __global__ void __launch_bounds__(kSlotChunk) slot_assign_kernel(const int* __re
                                                                   int E, int cap, const int* __restrict__ chunk_cnt,
                                                                   int* __restrict__ slot_idx,
                                                                   int* __restrict__ slot_src, int* __restrict__ fill) {
+    pdl_entry();
     __shared__ int base[EMAX];
     __shared__ int wc[kSlotWarps][EMAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -501,6 +506,7 @@ template <int EMAX>
 __global__ void __launch_bounds__(kWgCols / 8 * kWgSub) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
                                                                   const float* __restrict__ dlogits, int n, int M,
                                                                   int E, int chunk, float* __restrict__ part) {
+    pdl_entry();
     __shared__ float red[8][kWgCols / 8][8 + 1];     // one 8-expert block of one sub-group at a time
     const int col_lane = threadIdx.x % (kWgCols / 8);
     const int sub = threadIdx.x / (kWgCols / 8);
@@ -568,6 +574,7 @@ __global__ void __launch_bounds__(kWgCols / 8 * kWgSub) gate_wgrad_partial_kerne
 // are added in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restrict__ part, int chunks, long long len,
                                                            float* __restrict__ out, int accumulate) {
+    pdl_entry();
     __shared__ float ws[8][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long i = (long long)blockIdx.x * 32 + lane;
@@ -603,7 +610,7 @@ static void launch_gate_fwd(const bf16* x, long long ldx, const double* wgT, int
     const int max_blocks = kNumSMs * 16;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    gate_fwd_kernel<EMAX><<<blocks, kGateThreads, 0, s>>>(x, ldx, wgT, n, M, E, k, ei, cw, probs);
+    launch_k(gate_fwd_kernel<EMAX>, blocks, kGateThreads, 0, s, x, ldx, wgT, n, M, E, k, ei, cw, probs);
 }
 
 // PARM_GATE_DMMA=0 selects the FP64-FMA gate kernel (A/B comparisons).
@@ -632,24 +639,24 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
         if (nt_need == 1) {
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
-            gate_fwd_dmma_smem_kernel<1><<<blocks, kGateSmemWarps * 32, smem_bytes, s>>>(X, ldx, W, n, M, E, k,
+            launch_k(gate_fwd_dmma_smem_kernel<1>, blocks, kGateSmemWarps * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
                                                                                         expert_idx, combine_w, probs);
         } else {
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
-            gate_fwd_dmma_smem_kernel<2><<<blocks, kGateSmemWarps * 32, smem_bytes, s>>>(X, ldx, W, n, M, E, k,
+            launch_k(gate_fwd_dmma_smem_kernel<2>, blocks, kGateSmemWarps * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
                                                                                         expert_idx, combine_w, probs);
         }
     } else if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
         const int blocks = (int)std::min<long long>((n + 7) / 8, (long long)kNumSMs * 64);
         if (E <= 8)
-            gate_fwd_dmma_kernel<1><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+            launch_k(gate_fwd_dmma_kernel<1>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
                                                                        probs);
         else if (E <= 16)
-            gate_fwd_dmma_kernel<2><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+            launch_k(gate_fwd_dmma_kernel<2>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
                                                                        probs);
         else
-            gate_fwd_dmma_kernel<4><<<blocks, kDmmaWarps * 32, 0, s>>>(X, ldx, W, n, M, E, k, expert_idx, combine_w,
+            launch_k(gate_fwd_dmma_kernel<4>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
                                                                        probs);
     } else if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
@@ -677,11 +684,11 @@ int gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_id
     PARM_CHECK_ARG(ws_bytes >= gate_slots_workspace(n, E), "gate_slots: workspace too small");
     const int chunks = n > 0 ? (n + kSlotChunk - 1) / kSlotChunk : 1;
     if (E <= 8) {
-        slot_count_kernel<8><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_src);
-        slot_assign_kernel<8><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
+        launch_k(slot_count_kernel<8>, chunks, kSlotChunk, 0, s, expert_idx, n, k, E, cap, ws, slot_src);
+        launch_k(slot_assign_kernel<8>, chunks, kSlotChunk, 0, s, expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
     } else {
-        slot_count_kernel<32><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_src);
-        slot_assign_kernel<32><<<chunks, kSlotChunk, 0, s>>>(expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
+        launch_k(slot_count_kernel<32>, chunks, kSlotChunk, 0, s, expert_idx, n, k, E, cap, ws, slot_src);
+        launch_k(slot_assign_kernel<32>, chunks, kSlotChunk, 0, s, expert_idx, n, k, E, cap, ws, slot_idx, slot_src, fill);
     }
     PARM_CHECK_LAUNCH("gate_slots");
     return 0;
@@ -700,14 +707,14 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     dim3 grid((M + kWgCols - 1) / kWgCols, kWgChunks);
     auto X = reinterpret_cast<const bf16*>(x);
     if (E <= 8)
-        gate_wgrad_partial_kernel<8><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        launch_k(gate_wgrad_partial_kernel<8>, grid, kWgThreads, 0, s, X, ldx, dlogits, n, M, E, chunk, ws);
     else if (E <= 16)
-        gate_wgrad_partial_kernel<16><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        launch_k(gate_wgrad_partial_kernel<16>, grid, kWgThreads, 0, s, X, ldx, dlogits, n, M, E, chunk, ws);
     else
-        gate_wgrad_partial_kernel<32><<<grid, kWgThreads, 0, s>>>(X, ldx, dlogits, n, M, E, chunk, ws);
+        launch_k(gate_wgrad_partial_kernel<32>, grid, kWgThreads, 0, s, X, ldx, dlogits, n, M, E, chunk, ws);
     PARM_CHECK_LAUNCH("gate_wgrad_partial");
     const long long len = (long long)M * E;
-    sum_partials_kernel<<<(int)((len + 31) / 32), 256, 0, s>>>(ws, kWgChunks, len, dwgT, accumulate);
+    launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, ws, kWgChunks, len, dwgT, accumulate);
     PARM_CHECK_LAUNCH("gate_wgrad_sum");
     return 0;
 }

@@ -68,7 +68,7 @@ struct Params {
     const int* fill;           // [hi][lo][g] valid rows, or null
     int pairs;                 // CTA-pair kernel: max 256-row pair tiles per group
     int debug;                 // PARM_GEMM_DEBUG bits (perf experiments only): 1 = no epilogue stores, 2 = no TMA,
-                               // 4 = no MMA (pair kernel)
+                               // 4 = no MMA (pair kernel), 8 = per-thread stores instead of TMA stores
     int seg_peer;              // ROW: rows of segment (hi, lo) stored into seg_dst[hi * nlo + lo] (peer buffers)
     bf16* seg_dst[kMaxPeers];  //   + g * sd_g + r * sd_ld + n -- the return AlltoAll fused into the epilogue
     long long sd_g, sd_ld;
@@ -360,6 +360,7 @@ template <int BN, int KIND, int MB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                     const Params p) {
+    pdl_entry();
     using C = Cfg<BN, KIND, MB, EPI>;
     constexpr int STAGES = C::kStages;
     constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
@@ -867,29 +868,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    if (p.fill)
-        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
-    // ROW: work list = live 256-row pair tiles only (groups' live row pairs, prefix-summed), so the
-    // static round-robin over the 74 pairs balances the real work instead of an index space with
-    // unfilled capacity holes (max 5 vs the ideal 4 tiles per pair measured on the second GEMM).
-    int* sprefix = sfill + p.G * p.nhi * p.nlo;
-    if (KIND == kRow) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            sprefix[0] = 0;
-            for (int g = 0; g < p.G; ++g) {
-                int lt = 0;
-                for (int seg = 0; seg < p.nhi * p.nlo; ++seg) {
-                    const int h = seg / p.nlo, l = seg - h * p.nlo;
-                    int live = (seg_fill(p, sfill, g, h, l) + BM - 1) / BM;
-                    lt += live > p.m_tiles ? p.m_tiles : live;
-                }
-                acc += (lt + 1) / 2;
-                sprefix[g + 1] = acc;
-            }
-        }
-    }
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x >> 1;
@@ -914,6 +892,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      "r"((uint32_t)C::kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    // everything above is independent of the previous kernel (PDL prologue); fill counts and operands are not
+    pdl_entry();
+    if (p.fill)
+        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
+    // ROW: work list = live 256-row pair tiles only (groups' live row pairs, prefix-summed), so the
+    // static round-robin over the 74 pairs balances the real work instead of an index space with
+    // unfilled capacity holes (max 5 vs the ideal 4 tiles per pair measured on the second GEMM).
+    int* sprefix = sfill + p.G * p.nhi * p.nlo;
+    if (KIND == kRow) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            sprefix[0] = 0;
+            for (int g = 0; g < p.G; ++g) {
+                int lt = 0;
+                for (int seg = 0; seg < p.nhi * p.nlo; ++seg) {
+                    const int h = seg / p.nlo, l = seg - h * p.nlo;
+                    int live = (seg_fill(p, sfill, g, h, l) + BM - 1) / BM;
+                    lt += live > p.m_tiles ? p.m_tiles : live;
+                }
+                acc += (lt + 1) / 2;
+                sprefix[g + 1] = acc;
+            }
+        }
     }
     tc_fence_before();
     cluster_sync_all();
@@ -1054,7 +1057,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else if (KIND == kRow && p.seg_peer) {   // per-thread stores into the owner's receive block
                 const long long prow = (long long)t.g * p.sd_g + (long long)row * p.sd_ld;
                 drain_tile<BN, EPI>(p, taddr, prow, xrow, row_ok, t.n0, empty, p.seg_dst[t.hi * p.nlo + t.lo]);
-            } else if (p.debug & 1) {
+            } else if (p.debug & 9) {   // 8: per-thread global stores instead of the TMA-store staging
                 drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty, p.D);
             } else {
                 drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
@@ -1132,7 +1135,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
     }
     int grid = p.num_tiles < kNumSMs ? p.num_tiles : kNumSMs;
     if (grid < 1) grid = 1;
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, ta, tb, p);
     PARM_CHECK_LAUNCH("moe_gemm");
     return 0;
 }
@@ -1151,7 +1154,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
     }
     int grid = 2 * (p.num_tiles < kNumSMs / 2 ? p.num_tiles : kNumSMs / 2);   // clusters of 2 CTAs
     if (grid < 2) grid = 2;
-    kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, td, p, g_segmaps);
+    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, ta, tb, td, p, g_segmaps);
     PARM_CHECK_LAUNCH("moe_gemm_pair");
     return 0;
 }

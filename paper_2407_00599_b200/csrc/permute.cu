@@ -17,7 +17,9 @@
 // All are HBM-streaming gathers: one warp per token/row, 16-byte vectors, and
 // every row load of a 1024-column group is issued before any is consumed
 // (KT picks x 4 chunks in flight per lane) — the memory-level parallelism
-// these kernels live on.  Accumulation is f32.
+// these kernels live on.  Accumulation is f32.  dispatch, combine_fwd and
+// dispatch_bwd run as bulk-copy rings (gather_ring.cuh) whenever their views
+// are local and 16-byte aligned (PARM_RING=0: the register kernels below).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
     const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
     int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
     long long out_stride_s, const __grid_constant__ SlotView dstv, const int* __restrict__ fill) {
+    pdl_entry();
     constexpr int R = 4;
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
@@ -182,6 +185,9 @@ __device__ __forceinline__ void fma_bf16x8(float* acc, float w, const int4& v) {
     for (int u = 0; u < 8; ++u) acc[u] = fmaf(w, f[u], acc[u]);
 }
 
+#include "gather_ring.cuh"
+
+
 // 256 threads, <= 128 registers, a resident grid of two CTAs per SM looping over
 // tokens; the per-group accumulators are the only long-lived state.
 template <int KT>
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_fwd_kernel(const __gri
                                                                       const float* __restrict__ combine_w, int n, int k,
                                                                       int M, const __grid_constant__ RowFan out,
                                                                       long long ldo) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -230,6 +237,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
                                                                       const int* __restrict__ slot_idx,
                                                                       const float* __restrict__ probs, int n, int k,
                                                                       int E, int M, float* __restrict__ dlogits) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
                                                                        int E, int M,
                                                                        const __grid_constant__ RowFan dx,
                                                                        long long ldx) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -380,6 +389,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
 __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const __grid_constant__ SlotView y, int E, int slots,
                                                                   int M,
                                                                   bf16* __restrict__ out) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -435,7 +445,18 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
     const long long rows = (long long)E * slots_out;
     if (rows == 0) return 0;
     SlotView none{};
-    dispatch_rows_kernel<false><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
+    if (ring::enabled() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        constexpr int S = 6;
+        static int per_sm = 0;
+        const int smem = ring::ring_smem(S, 1, 0);
+        auto kern = ring::dispatch_rows_ring<false, S>;
+        launch_k(kern, ring::grid_for(kern, smem, rows, per_sm), kRowThreads, smem, s, 
+            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
+            reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none, fill);
+        PARM_CHECK_LAUNCH("dispatch_rows");
+        return 0;
+    }
+    launch_k(dispatch_rows_kernel<false>, row_grid((rows + 3) / 4), kRowThreads, 0, s, 
         reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
         reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none, fill);
     PARM_CHECK_LAUNCH("dispatch_rows");
@@ -445,6 +466,7 @@ int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float
 // Per-segment fill counts of this source's slot range, stored into every holder's table.
 __global__ void fan_fill_kernel(const int* __restrict__ fill, int E, int slot_lo, int slots_out,
                                 const __grid_constant__ SlotView dstv, const __grid_constant__ IntFan fan) {
+    pdl_entry();
     const int e = threadIdx.x;
     if (e >= E) return;
     int c = __ldg(fill + e) - slot_lo;
@@ -461,14 +483,23 @@ int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const 
                    "dispatch_rows_peer: rows must be 16-byte aligned (M=%d)", M);
     PARM_CHECK_ARG(E <= 1024, "dispatch_rows_peer: too many experts");
     const long long rows = (long long)E * slots_out;
-    if (rows > 0) {
-        dispatch_rows_kernel<true><<<row_grid((rows + 3) / 4), kRowThreads, 0, s>>>(
+    if (rows > 0 && ring::enabled() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && dst.stride_shi % 8 == 0) {
+        constexpr int S = 6;
+        static int per_sm = 0;
+        const int smem = ring::ring_smem(S, 1, 0);
+        auto kern = ring::dispatch_rows_ring<true, S>;
+        launch_k(kern, ring::grid_for(kern, smem, rows, per_sm), kRowThreads, smem, s, 
+            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
+            dst, fill);
+        PARM_CHECK_LAUNCH("dispatch_rows_peer");
+    } else if (rows > 0) {
+        launch_k(dispatch_rows_kernel<true>, row_grid((rows + 3) / 4), kRowThreads, 0, s, 
             reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
             dst, fill);
         PARM_CHECK_LAUNCH("dispatch_rows_peer");
     }
     if (fill != nullptr && fill_dst != nullptr) {
-        fan_fill_kernel<<<1, ((E + 31) / 32) * 32, 0, s>>>(fill, E, slot_lo, slots_out, dst, *fill_dst);
+        launch_k(fan_fill_kernel, 1, ((E + 31) / 32) * 32, 0, s, fill, E, slot_lo, slots_out, dst, *fill_dst);
         PARM_CHECK_LAUNCH("dispatch_rows_peer(fill)");
     }
     return 0;
@@ -482,6 +513,7 @@ int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const 
 __global__ void __launch_bounds__(kRowThreads) push_rows_kernel(const bf16* __restrict__ src, int nseg, int el,
                                                                 int rows, int M, const int* __restrict__ fill,
                                                                 const __grid_constant__ RowFan dst) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -517,7 +549,7 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
     PARM_CHECK_ARG(M % 8 == 0 && fill != nullptr, "push_rows: M=%d must be a multiple of 8, fill required", M);
     const long long total = (long long)nseg * el * rows;
     if (total == 0) return 0;
-    push_rows_kernel<<<row_grid(total), kRowThreads, 0, s>>>(reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
+    launch_k(push_rows_kernel, row_grid(total), kRowThreads, 0, s, reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
                                                              fill, dst);
     PARM_CHECK_LAUNCH("push_rows");
     return 0;
@@ -527,6 +559,7 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
 // `bytes` of src stored into each dst.ptr[i] (16-byte vectors): small payloads
 // replicated to every MP peer (the gate-gradient exchange of S1).
 __global__ void fan_copy_kernel(const int4* __restrict__ src, long long vecs, const __grid_constant__ RowFan dst) {
+    pdl_entry();
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < vecs; i += (long long)gridDim.x * blockDim.x) {
         const int4 v = __ldg(src + i);
         for (int f = 0; f < dst.n; ++f) reinterpret_cast<int4*>(dst.ptr[f])[i] = v;
@@ -541,7 +574,7 @@ int fan_copy(const void* src, long long bytes, const RowFan& dst, cudaStream_t s
     if (vecs == 0) return 0;
     long long blocks = (vecs + 255) / 256;
     if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
-    fan_copy_kernel<<<(int)blocks, 256, 0, s>>>(reinterpret_cast<const int4*>(src), vecs, dst);
+    launch_k(fan_copy_kernel, (int)blocks, 256, 0, s, reinterpret_cast<const int4*>(src), vecs, dst);
     PARM_CHECK_LAUNCH("fan_copy");
     return 0;
 }
@@ -553,6 +586,7 @@ int fan_copy(const void* src, long long bytes, const RowFan& dst, cudaStream_t s
 // own pad.  The epoch lives in device memory, so a replayed CUDA graph
 // advances it like an eager launch.  A watchdog traps instead of hanging.
 __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
+    pdl_entry();
     __shared__ unsigned epoch;
     if (threadIdx.x == 0) {
         unsigned* cnt = reinterpret_cast<unsigned*>(sig.counter);
@@ -581,7 +615,7 @@ int peer_barrier(const PeerSignal& sig, cudaStream_t s) {
     PARM_CHECK_ARG(sig.n >= 1 && sig.n <= kMaxPeers && sig.rank >= 0 && sig.rank < sig.n,
                    "peer_barrier: bad rank %d of %d", sig.rank, sig.n);
     PARM_CHECK_ARG(sig.counter != nullptr, "peer_barrier: null epoch counter");
-    peer_barrier_kernel<<<1, 32, 0, s>>>(sig);
+    launch_k(peer_barrier_kernel, 1, 32, 0, s, sig);
     PARM_CHECK_LAUNCH("peer_barrier");
     return 0;
 }
@@ -610,10 +644,26 @@ int combine_fwd_fan(const SlotView& y, const int* expert_idx, const int* slot_id
     PARM_CHECK_ARG(k >= 1 && k <= 8, "combine_fwd: top_k must be in [1, 8]");
     PARM_CHECK_ARG(O.n >= 1 && O.n <= kMaxPeers, "combine_fwd: output fan of %d buffers", O.n);
     if (n == 0) return 0;
+    if (ring::enabled() && k <= 2 && y.n_p <= 2 && ring::view_aligned(y) && ring::fan_aligned(O, ldo)) {
+        constexpr int S = 4;
+        static int per_sm1 = 0, per_sm2 = 0;
+        const int smem = ring::ring_smem(S, 2 * y.n_p, 0);
+        if (y.n_p == 1) {
+            auto kern = ring::combine_fwd_ring<1, S>;
+            launch_k(kern, ring::grid_for(kern, smem, n, per_sm1), kRowThreads, smem, s, y, expert_idx, slot_idx, combine_w,
+                                                                                 n, k, M, O, ldo);
+        } else {
+            auto kern = ring::combine_fwd_ring<2, S>;
+            launch_k(kern, ring::grid_for(kern, smem, n, per_sm2), kRowThreads, smem, s, y, expert_idx, slot_idx, combine_w,
+                                                                                 n, k, M, O, ldo);
+        }
+        PARM_CHECK_LAUNCH("combine_fwd");
+        return 0;
+    }
     if (k <= 2)
-        combine_fwd_kernel<2><<<resident_grid(n, 2), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        launch_k(combine_fwd_kernel<2>, resident_grid(n, 2), kRowThreads, 0, s, y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     else
-        combine_fwd_kernel<8><<<resident_grid(n, 2), kRowThreads, 0, s>>>(y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
+        launch_k(combine_fwd_kernel<8>, resident_grid(n, 2), kRowThreads, 0, s, y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     PARM_CHECK_LAUNCH("combine_fwd");
     return 0;
 }
@@ -625,10 +675,10 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     if (n == 0) return 0;
     auto D = reinterpret_cast<const bf16*>(dout);
     if (k <= 2)
-        combine_bwd_kernel<2><<<resident_grid(n, 2), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        launch_k(combine_bwd_kernel<2>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     else
-        combine_bwd_kernel<8><<<resident_grid(n, 2), kRowThreads, 0, s>>>(D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
+        launch_k(combine_bwd_kernel<8>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
                                                                   dlogits);
     PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
@@ -649,16 +699,33 @@ int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_
     if (n == 0) return 0;
     auto W = reinterpret_cast<const bf16*>(wg);
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "dispatch_bwd: rows must be 16-byte aligned (M=%d)", M);
+    if (ring::enabled() && k <= 2 && dr.n_p <= 2 && ring::view_aligned(dr) && ring::fan_aligned(DX, ldx) &&
+        (dlogits == nullptr || (E % 4 == 0 && (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0))) {
+        constexpr int S = 4;
+        static int per_sm1 = 0, per_sm2 = 0;
+        const int smem = ring::ring_smem(S, 2 * dr.n_p, 128);
+        if (dr.n_p == 1) {
+            auto kern = ring::dispatch_bwd_ring<1, S>;
+            launch_k(kern, ring::grid_for(kern, smem, n, per_sm1), kRowThreads, smem, s, dr, expert_idx, slot_idx, dlogits,
+                                                                                 W, n, k, E, M, DX, ldx);
+        } else {
+            auto kern = ring::dispatch_bwd_ring<2, S>;
+            launch_k(kern, ring::grid_for(kern, smem, n, per_sm2), kRowThreads, smem, s, dr, expert_idx, slot_idx, dlogits,
+                                                                                 W, n, k, E, M, DX, ldx);
+        }
+        PARM_CHECK_LAUNCH("dispatch_bwd");
+        return 0;
+    }
     // (the E <= 8 variant that keeps the logit gradients in registers spills at 128 registers and
     // measured 39 us against 30 us for loading them per use; kept for E <= 8 experiments only)
     if (k <= 2 && E <= 8 && getenv("PARM_DBWD_REGS"))
-        dispatch_bwd_kernel<2, 4, 8><<<row_grid((n + 3) / 4), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits,
+        launch_k(dispatch_bwd_kernel<2, 4, 8>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
                                                                                       W, n, k, E, M, DX, ldx);
     else if (k <= 2)
-        dispatch_bwd_kernel<2, 4, 0><<<row_grid((n + 3) / 4), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits,
+        launch_k(dispatch_bwd_kernel<2, 4, 0>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
                                                                                       W, n, k, E, M, DX, ldx);
     else
-        dispatch_bwd_kernel<8, 1, 0><<<row_grid(n), kRowThreads, 0, s>>>(dr, expert_idx, slot_idx, dlogits, W, n, k,
+        launch_k(dispatch_bwd_kernel<8, 1, 0>, row_grid(n), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits, W, n, k,
                                                                             E, M, DX, ldx);
     PARM_CHECK_LAUNCH("dispatch_bwd");
     return 0;
@@ -669,7 +736,7 @@ int esp_sum(const SlotView& y, int E, int slots, int M, void* out, cudaStream_t 
     PARM_CHECK_ARG(y.n_peer == 0, "esp_sum: local views only");
     const long long rows = (long long)E * slots;
     if (rows == 0) return 0;
-    esp_sum_kernel<<<row_grid(rows), kRowThreads, 0, s>>>(y, E, slots, M, reinterpret_cast<bf16*>(out));
+    launch_k(esp_sum_kernel, row_grid(rows), kRowThreads, 0, s, y, E, slots, M, reinterpret_cast<bf16*>(out));
     PARM_CHECK_LAUNCH("esp_sum");
     return 0;
 }
