@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 11
+#define PARM_ABI_VERSION 12
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -111,6 +111,21 @@ int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* 
 int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
                      const int* slot_idx, const float* probs, int n, int k, int E, int M, float* dlogits,
                      void* stream);
+
+/* Combine backward fused with the backward dispatch of dOut (ABI v12): the
+ * dlogits of parm_combine_bwd, and in the same pass over dOut the slot rows
+ * parm_dispatch_rows(dOut, scale = combine_w, fill) writes -- row (e, s - slot_lo)
+ * <- combine_w[t, j] * dOut[t] for each kept pick with s in [slot_lo, slot_lo +
+ * slots_out), zero rows up to each expert's last 128-row GEMM tile.  Rows go to
+ * out (+ e * out_stride_e + s * out_stride_s) or, when dst is non-null, to the
+ * N_ESP holders through the peer view (the EP&ESP AlltoAll fused, as in
+ * parm_dispatch_rows_peer).  Replaces combine_bwd + dispatch_rows (one read of
+ * dOut instead of two, one launch instead of two). */
+int parm_combine_bwd_dispatch(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
+                              const int* slot_idx, const float* probs, const float* combine_w, int n, int k, int E,
+                              int M, float* dlogits, int slot_lo, int slots_out, const int* fill, void* out,
+                              long long out_stride_e, long long out_stride_s, const parm_slot_view* dst,
+                              void* stream);
 
 /* Dispatch backward: dx[t] = sum_j sum_p dR_p[e_j, s_j] + dlogits[t] . Wg^T
  * (dlogits nullable; wg_t is the (E, M) bf16 gate weights, transposed).

@@ -76,6 +76,9 @@ SIGNATURES = {
                                   _vp]),
     "parm_combine_bwd": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
                                   _c_int, _vp, _vp]),
+    "parm_combine_bwd_dispatch": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int,
+                                           _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll,
+                                           ctypes.POINTER(SlotViewC), _vp]),
     "parm_dispatch_bwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
                                    _vp, _c_ll, _vp]),
     "parm_esp_sum": (_c_int, [ctypes.POINTER(SlotViewC), _c_int, _c_int, _c_int, _vp, _vp]),
@@ -94,7 +97,7 @@ SIGNATURES = {
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 
 class ParmError(RuntimeError):

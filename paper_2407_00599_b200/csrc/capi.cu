@@ -30,6 +30,9 @@ int combine_bwd(const void*, long long, const SlotView&, const int*, const int*,
                 float*, cudaStream_t);
 int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int, void*,
                  long long, cudaStream_t);
+int combine_bwd_dispatch(const void*, long long, const SlotView&, const int*, const int*, const float*, const float*,
+                         int, int, int, int, float*, int, int, const int*, void*, long long, long long, const SlotView*,
+                         cudaStream_t);
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
 int moe_gemm(const parm_gemm_desc&, cudaStream_t);
 int moe_gemm_peer(const parm_gemm_desc&, const RowFan*, long long, long long, cudaStream_t);
@@ -107,6 +110,22 @@ int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* 
         return 1;
     }
     return parm::combine_bwd(dout, ld_dout, to_view(y), expert_idx, slot_idx, probs, n, k, E, M, dlogits, S(stream));
+}
+
+int parm_combine_bwd_dispatch(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
+                              const int* slot_idx, const float* probs, const float* combine_w, int n, int k, int E,
+                              int M, float* dlogits, int slot_lo, int slots_out, const int* fill, void* out,
+                              long long out_stride_e, long long out_stride_s, const parm_slot_view* dst,
+                              void* stream) {
+    if (!y) {
+        parm::set_error("combine_bwd_dispatch: null slot view");
+        return 1;
+    }
+    parm::SlotView dv{};
+    if (dst) dv = to_view(dst);
+    return parm::combine_bwd_dispatch(dout, ld_dout, to_view(y), expert_idx, slot_idx, probs, combine_w, n, k, E, M,
+                                      dlogits, slot_lo, slots_out, fill, out, out_stride_e, out_stride_s,
+                                      dst ? &dv : nullptr, S(stream));
 }
 
 int parm_dispatch_bwd(const parm_slot_view* dr, const int* expert_idx, const int* slot_idx, const float* dlogits,

@@ -231,21 +231,49 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_fwd_kernel(const __gri
     }
 }
 
-template <int KT>
+// Scatter target of the fused combine-backward + dy dispatch (SC = 1 local, 2 peer view):
+// row (e, s - slot_lo) <- w_j * dOut[t] for every kept pick with s in the slot range,
+// zero rows up to each segment's last 128-row GEMM tile -- what dispatch_rows(dOut,
+// scale = combine weights, fill) writes, without reading dOut a second time.
+struct DyScatter {
+    const float* combine_w;
+    int slot_lo, slots_out;
+    const int* fill;
+    bf16* out;
+    long long stride_e, stride_s;
+};
+
+template <int SC>
+__device__ __forceinline__ void scatter_row(const SlotView& dstv, const DyScatter& sc, int e, int sp, int c,
+                                            const int4& v) {
+    if (SC == 1) {
+        *reinterpret_cast<int4*>(sc.out + (long long)e * sc.stride_e + (long long)sp * sc.stride_s + c) = v;
+    } else {
+        int ep;
+        const long long off = slot_inbuf(dstv, e, sp, ep);
+        for (int pp = 0; pp < dstv.n_p; ++pp)
+            *reinterpret_cast<int4*>(const_cast<bf16*>(slot_base(dstv, ep, pp)) + off + c) = v;
+    }
+}
+
+template <int KT, int SC>
 __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16* __restrict__ dout, long long ldd,
                                                                       const __grid_constant__ SlotView y, const int* __restrict__ expert_idx,
                                                                       const int* __restrict__ slot_idx,
                                                                       const float* __restrict__ probs, int n, int k,
-                                                                      int E, int M, float* __restrict__ dlogits) {
+                                                                      int E, int M, float* __restrict__ dlogits,
+                                                                      const __grid_constant__ DyScatter sc,
+                                                                      const __grid_constant__ SlotView dstv) {
     pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
     Picks<KT> nx;
-    if (warp_global < n) nx.load(warp_global, k, slot_idx, expert_idx, nullptr, y);
+    const float* cw = SC ? sc.combine_w : nullptr;
+    if (warp_global < n) nx.load(warp_global, k, slot_idx, expert_idx, cw, y);
     for (long long t = warp_global; t < n; t += num_warps) {
         const Picks<KT> pk = nx;
-        if (t + num_warps < n) nx.load(t + num_warps, k, slot_idx, expert_idx, nullptr, y);
+        if (t + num_warps < n) nx.load(t + num_warps, k, slot_idx, expert_idx, cw, y);
         float dw[KT];
 #pragma unroll
         for (int j = 0; j < KT; ++j) dw[j] = 0.0f;
@@ -276,6 +304,26 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
                     }
                 }
             }
+            if (SC) {   // the dy dispatch: w_j * dOut[t] into the pick's slot row
+#pragma unroll
+                for (int j = 0; j < KT; ++j) {
+                    const int sp = pk.sl[j] - sc.slot_lo;
+                    if (pk.sl[j] < 0 || sp < 0 || sp >= sc.slots_out) continue;
+#pragma unroll
+                    for (int i = 0; i < kChunks; ++i) {
+                        const int c = g0 + lane * 8 + i * 256;
+                        if (c >= M) continue;
+                        Vec8 g8;
+                        *reinterpret_cast<int4*>(&g8) = gv[i];
+                        float f[8];
+                        vec8_to_f32(g8, f);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) f[u] *= pk.w[j];
+                        const Vec8 r8 = f32_to_vec8(f);
+                        scatter_row<SC>(dstv, sc, pk.ex[j], sp, c, *reinterpret_cast<const int4*>(&r8));
+                    }
+                }
+            }
         }
 #pragma unroll
         for (int j = 0; j < KT; ++j)
@@ -292,6 +340,16 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
                 if (pk.ex[j] == lane) dse = dw[j];
             }
             dlogits[t * E + lane] = pe * (dse - dot);
+        }
+    }
+    if (SC) {   // unfilled slot rows inside each segment's last GEMM tile: zeros
+        for (long long it = warp_global; it < (long long)E * 128; it += num_warps) {
+            const int e = (int)(it >> 7), r = (int)(it & 127);
+            int sf = __ldg(sc.fill + e) - sc.slot_lo;
+            sf = sf < 0 ? 0 : (sf > sc.slots_out ? sc.slots_out : sf);
+            const int end = min((sf + 127) & ~127, sc.slots_out);
+            if (sf + r >= end) continue;
+            for (int c = lane * 8; c < M; c += 256) scatter_row<SC>(dstv, sc, e, sf + r, c, make_int4(0, 0, 0, 0));
         }
     }
 }
@@ -674,13 +732,57 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     PARM_CHECK_ARG(k <= 8 && E <= 32, "combine_bwd: k<=8 and E<=32 required");
     if (n == 0) return 0;
     auto D = reinterpret_cast<const bf16*>(dout);
+    const DyScatter none{};
+    const SlotView nov{};
     if (k <= 2)
-        launch_k(combine_bwd_kernel<2>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
-                                                                  dlogits);
+        launch_k(combine_bwd_kernel<2, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
+                 probs, n, k, E, M, dlogits, none, nov);
     else
-        launch_k(combine_bwd_kernel<8>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E, M,
-                                                                  dlogits);
+        launch_k(combine_bwd_kernel<8, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
+                 probs, n, k, E, M, dlogits, none, nov);
     PARM_CHECK_LAUNCH("combine_bwd");
+    return 0;
+}
+
+int combine_bwd_dispatch(const void* dout, long long ldd, const SlotView& y, const int* expert_idx,
+                         const int* slot_idx, const float* probs, const float* combine_w, int n, int k, int E, int M,
+                         float* dlogits, int slot_lo, int slots_out, const int* fill, void* out, long long stride_e,
+                         long long stride_s, const SlotView* dst, cudaStream_t s) {
+    if (int rc = check_view(y, M, "combine_bwd_dispatch")) return rc;
+    PARM_CHECK_ARG(k <= 8 && E <= 32, "combine_bwd_dispatch: k<=8 and E<=32 required");
+    PARM_CHECK_ARG(combine_w != nullptr && fill != nullptr, "combine_bwd_dispatch: combine weights and fill required");
+    PARM_CHECK_ARG(ldd % 8 == 0 && (reinterpret_cast<uintptr_t>(dout) & 15) == 0,
+                   "combine_bwd_dispatch: dOut rows must be 16-byte aligned");
+    if (dst != nullptr) {
+        PARM_CHECK_ARG(dst->n_peer >= 1 && dst->n_peer <= kMaxPeers, "combine_bwd_dispatch: destination must be a peer view");
+        PARM_CHECK_ARG(dst->stride_i % 8 == 0 && dst->stride_slo % 8 == 0 && dst->stride_shi % 8 == 0,
+                       "combine_bwd_dispatch: destination rows must be 16-byte aligned");
+    } else {
+        PARM_CHECK_ARG(out != nullptr && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && stride_e % 8 == 0 &&
+                           stride_s % 8 == 0,
+                       "combine_bwd_dispatch: output rows must be 16-byte aligned");
+    }
+    if (n == 0 && slots_out == 0) return 0;
+    auto D = reinterpret_cast<const bf16*>(dout);
+    DyScatter sc{combine_w, slot_lo, slots_out, fill, reinterpret_cast<bf16*>(out), stride_e, stride_s};
+    const SlotView nov{};
+    const int grid = resident_grid(n > E * 128 ? n : E * 128, 2);
+    if (dst != nullptr) {
+        if (k <= 2)
+            launch_k(combine_bwd_kernel<2, 2>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
+                     M, dlogits, sc, *dst);
+        else
+            launch_k(combine_bwd_kernel<8, 2>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
+                     M, dlogits, sc, *dst);
+    } else {
+        if (k <= 2)
+            launch_k(combine_bwd_kernel<2, 1>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
+                     M, dlogits, sc, nov);
+        else
+            launch_k(combine_bwd_kernel<8, 1>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
+                     M, dlogits, sc, nov);
+    }
+    PARM_CHECK_LAUNCH("combine_bwd_dispatch");
     return 0;
 }
 

@@ -144,6 +144,34 @@ def combine_bwd(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, sl
               slot_idx.data_ptr(), probs.data_ptr(), n, k, E, M, dlogits.data_ptr(), _stream())
 
 
+def combine_bwd_dispatch(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor,
+                         probs: torch.Tensor, combine_w: torch.Tensor, dlogits: torch.Tensor, slot_lo: int,
+                         fill: torch.Tensor, out: torch.Tensor | None = None, dst: SlotView | None = None,
+                         slots_out: int | None = None) -> None:
+    """combine_bwd + dispatch_rows(dout, scale=combine_w, fill) in one pass over dOut: the slot rows
+    go to ``out`` (E, S_out, M) or, with ``dst``, to the holders through the peer view."""
+    _need(dout, torch.bfloat16, "dOut")
+    n, M = dout.shape
+    k = expert_idx.shape[1]
+    E = probs.shape[1]
+    v = view.c()
+    if dst is not None:
+        if slots_out is None:
+            raise ValueError("combine_bwd_dispatch: slots_out required with a peer destination")
+        dv = dst.c()
+        _lib.call("parm_combine_bwd_dispatch", dout.data_ptr(), dout.stride(0), ctypes.byref(v),
+                  expert_idx.data_ptr(), slot_idx.data_ptr(), probs.data_ptr(), combine_w.data_ptr(), n, k, E, M,
+                  dlogits.data_ptr(), slot_lo, slots_out, fill.data_ptr(), None, 0, 0, ctypes.byref(dv), _stream())
+    else:
+        _need(out, torch.bfloat16, "dispatch out")
+        if out.stride(2) != 1:
+            raise ValueError("dispatch rows need unit inner stride")
+        _lib.call("parm_combine_bwd_dispatch", dout.data_ptr(), dout.stride(0), ctypes.byref(v),
+                  expert_idx.data_ptr(), slot_idx.data_ptr(), probs.data_ptr(), combine_w.data_ptr(), n, k, E, M,
+                  dlogits.data_ptr(), slot_lo, out.shape[1], fill.data_ptr(), out.data_ptr(), out.stride(0),
+                  out.stride(1), None, _stream())
+
+
 def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, dlogits: torch.Tensor | None,
                  wg: torch.Tensor | None, E: int, dx: torch.Tensor) -> None:
     """wg: the transposed (E, M) bf16 gate weights (or None with dlogits None)."""

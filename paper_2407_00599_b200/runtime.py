@@ -172,6 +172,8 @@ class MoELayer:
         self.peer_push_s2 = os.environ.get("PARM_PEER_RETURN_S2", "pull") == "push"
         # S1 push from the GEMM epilogue itself (tile by tile, overlapping the math) instead of a copy kernel
         self.peer_epilogue = os.environ.get("PARM_PEER_EPILOGUE", "1") != "0"
+        # combine backward and the dOut dispatch fused into one pass over dOut
+        self.fused_dy = os.environ.get("PARM_FUSED_DY", "1") != "0"
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -346,6 +348,22 @@ class MoELayer:
         return b[key]
 
     # ------------------------------------------------------------ FFN
+    def _combine_bwd_dy(self, dout, yv, rt, dlogits, slot_lo: int, cap: int, out=None, dst=None,
+                        slots_out=None) -> None:
+        """Combine backward (dlogits) and the dispatch of combine_w * dOut into the slot rows the
+        dH GEMM reads (``out``, or the holders' buffers through the peer view ``dst``) -- one
+        fused pass over dOut (PARM_FUSED_DY=0: the two separate kernels)."""
+        if self.fused_dy:
+            K.combine_bwd_dispatch(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, rt.combine_w, dlogits, slot_lo,
+                                   rt.fill, out=out, dst=dst, slots_out=slots_out)
+            return
+        K.combine_bwd(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, dlogits)
+        if dst is None:
+            K.dispatch_rows(dout, rt.slot_src, self.d.k, cap, slot_lo, out, scale=rt.combine_w, fill=rt.fill)
+        else:
+            K.dispatch_rows_peer(dout, rt.slot_src, self.d.k, cap, slot_lo, slots_out, dst, scale=rt.combine_w,
+                                 fill=rt.fill)
+
     def _ffn_fwd(self, s: RankState, b: dict, y_peer: tuple | None = None) -> None:
         K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=b["fill_in"])
         K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"], peer=y_peer)
@@ -484,8 +502,7 @@ class MoELayer:
             b = s.bufs["_local"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            K.combine_bwd(dout, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(dout, self._ret_view(b, "ret"), rt, b["dlogits"], 0, rt.cap, out=b["dsend"])
             self._ffn_bwd(s, b)
             K.dispatch_bwd(self._ret_view(b, "dret"), rt.expert_idx, rt.slot_idx, b["dlogits"], s.gate, d.E,
                            b["dx"])
@@ -563,9 +580,8 @@ class MoELayer:
             ds = dout[m * sl:(m + 1) * sl]
             rt = b["route"]
             yv = self._ret_view(b, "ret") if self.peer_push else self._peer_view(b, "y", r)
-            K.combine_bwd(ds, yv, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows_peer(ds, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "dyrecv", r),
-                                 scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(ds, yv, rt, b["dlogits"], 0, rt.cap, dst=self._peer_view(b, "dyrecv", r),
+                                 slots_out=b["q"])
         self.world.peer_barrier()
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
@@ -635,8 +651,7 @@ class MoELayer:
             m = L.mp_pos(r)
             ds = dout[m * sl:(m + 1) * sl]          # adjoint of AG_mp: own slice
             rt = b["route"]
-            K.combine_bwd(ds, self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows(ds, rt.slot_src, d.k, rt.cap, 0, b["dsend"], scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(ds, self._ret_view(b, "ret"), rt, b["dlogits"], 0, rt.cap, out=b["dsend"])
         self.world.exchange(self._fused_msgs("s1", "dsend", "dyrecv", with_fill=False))  # adjoint of ESP sum + A2A
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s1"])
@@ -775,9 +790,8 @@ class MoELayer:
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
             yv = self._gath_push_view(b, "gath") if self.peer_push_s2 else self._shard_view(b, "y", r)
-            K.combine_bwd(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
-            K.dispatch_rows_peer(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
-                                 self._peer_view(b, "dyrecv", r), scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(dout, yv, rt, b["dlogits"], L.mp_pos(r) * b["q"], rt.cap,
+                                 dst=self._peer_view(b, "dyrecv", r), slots_out=b["q"])
         self.world.peer_barrier()
         for r in self.ranks:
             b = self.st[r].bufs["s2"]
@@ -828,10 +842,9 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["s2"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            K.combine_bwd(dout, self._gath_view(b, "gath"), rt.expert_idx, rt.slot_idx, rt.probs, b["dlogits"])
             # adjoint of AG_mp over slots: only this rank's slot shard
-            K.dispatch_rows(dout, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["dsend"],
-                            scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(dout, self._gath_view(b, "gath"), rt, b["dlogits"], L.mp_pos(r) * b["q"], rt.cap,
+                                 out=b["dsend"])
         self.world.exchange(self._fused_msgs("s2", "dsend", "dyrecv", with_fill=False))
         for r in self.ranks:
             self._ffn_bwd(self.st[r], self.st[r].bufs["s2"])
@@ -928,9 +941,8 @@ class MoELayer:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             dout = self._input(b, douts[r], "dout")
             rt = b["route"]
-            K.combine_bwd(dout, self._ret_own_view(b, "ret", L.esp_pos(r)), rt.expert_idx, rt.slot_idx, rt.probs,
-                          b["dlogits"])
-            K.dispatch_rows(dout, rt.slot_src, d.k, d.T, 0, b["dyown"], scale=rt.combine_w, fill=rt.fill)
+            self._combine_bwd_dy(dout, self._ret_own_view(b, "ret", L.esp_pos(r)), rt, b["dlogits"], 0, d.T,
+                                 out=b["dyown"])
             ins[r], outs[r] = b["dyown"], b["dyg"]
         self.world.allgather("esp", ins, outs)                   # adjoint of the ESP split
         self.world.exchange(self._ep_dispatch_msgs("dyg", "dyrecv", with_fill=False))  # adjoint of return A2A

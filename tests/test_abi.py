@@ -34,7 +34,7 @@ def test_header_lists_the_boundary():
                      "parm_combine_bwd", "parm_dispatch_bwd", "parm_esp_sum", "parm_gate_wgrad",
                      "parm_gemm", "parm_last_error", "parm_abi_version", "parm_dispatch_rows_peer",
                      "parm_combine_fwd_fan", "parm_dispatch_bwd_fan", "parm_peer_barrier", "parm_push_rows",
-                     "parm_fan_copy", "parm_gemm_peer"):
+                     "parm_fan_copy", "parm_gemm_peer", "parm_combine_bwd_dispatch"):
         assert required in fns
 
 

@@ -77,6 +77,46 @@ def test_gate_routing_bit_exact(cuda_lib, n, M, E, k, cap):
         assert (ssh[e, counts[e]:] == -1).all()
 
 
+@pytest.mark.parametrize("n,M,E,k,cap,slot_lo,slots_out", [
+    (4096, 1024, 8, 2, 1229, 0, 1229),     # S1 slice, whole slot range
+    (1000, 256, 4, 2, 300, 150, 150),      # S2 slot shard (second MP rank)
+    (777, 128, 16, 1, 40, 0, 48),          # k=1, heavy overflow, padded shard past cap
+    (300, 64, 8, 4, 90, 0, 90),            # k=4 (KT=8 kernel)
+])
+def test_combine_bwd_dispatch_matches_separate_kernels(cuda_lib, n, M, E, k, cap, slot_lo, slots_out):
+    """The fused combine-backward + dOut dispatch writes exactly what combine_bwd and
+    dispatch_rows(scale = combine weights, fill) write (bit-identical dlogits and slot rows)."""
+    from paper_2407_00599_b200 import kernels as K
+
+    rng = np.random.default_rng(n + k)
+    x = _t(O.round_bf16(rng.normal(size=(n, M))))
+    wg = _t(O.round_bf16(rng.normal(size=(M, E))).T).double()
+    ei = torch.empty(n, k, dtype=torch.int32, device="cuda")
+    cw = torch.empty(n, k, dtype=torch.float32, device="cuda")
+    pr = torch.empty(n, E, dtype=torch.float32, device="cuda")
+    si = torch.empty(n, k, dtype=torch.int32, device="cuda")
+    ss = torch.empty(E, cap, dtype=torch.int32, device="cuda")
+    fill = torch.empty(E, dtype=torch.int32, device="cuda")
+    K.gate_fwd(x, wg, k, ei, cw, pr)
+    K.gate_slots(ei, E, cap, si, ss, fill)
+    y = _t(O.round_bf16(rng.normal(size=(E, cap, M))))
+    view = K.SlotView(y, e_local=E, stride_i=cap * M, stride_slo=M)
+    dout = _t(O.round_bf16(rng.normal(size=(n, M))))
+    poison = float("nan")
+    dl_a = torch.full((n, E), poison, device="cuda")
+    dl_b = torch.full((n, E), poison, device="cuda")
+    rows_a = torch.full((E, slots_out, M), poison, device="cuda", dtype=torch.bfloat16)
+    rows_b = rows_a.clone()
+    K.combine_bwd(dout, view, ei, si, pr, dl_a)
+    K.dispatch_rows(dout, ss, k, cap, slot_lo, rows_a, scale=cw, fill=fill)
+    K.combine_bwd_dispatch(dout, view, ei, si, pr, cw, dl_b, slot_lo, fill, out=rows_b)
+    torch.cuda.synchronize()
+    assert torch.equal(dl_a, dl_b)
+    # rows the GEMM reads (up to each expert's last 128-row tile) are identical, NaN poison included
+    assert torch.equal(rows_a.isnan(), rows_b.isnan())
+    assert torch.equal(torch.nan_to_num(rows_a.float()), torch.nan_to_num(rows_b.float()))
+
+
 def test_gate_ties_go_to_lower_expert(cuda_lib):
     from paper_2407_00599_b200 import api
 
