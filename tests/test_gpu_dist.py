@@ -30,8 +30,15 @@ def _free_port() -> int:
 def test_nccl_parity(world):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs (have {torch.cuda.device_count()})")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "tools" / "dist_parity.py")]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ))
+    # one retry on a fresh port: the rendezvous port from _free_port can be taken before torchrun
+    # binds it (a parity mismatch is deterministic and fails both attempts)
+    for attempt in range(2):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               str(ROOT / "tools" / "dist_parity.py")]
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ))
+        if res.returncode == 0:
+            break
+        print(f"attempt {attempt}: rc={res.returncode}\n{res.stdout[-2000:]}\n{res.stderr[-2000:]}")
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert f"DIST PARITY OK (P={world}" in res.stdout
