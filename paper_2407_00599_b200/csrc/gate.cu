@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(kGateSmemWarps * 32) gate_fwd_dmma_smem_kernel
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) wrow[nt] = sw + (nt * 8 + g) * stride + (long long)q * (Q + 8);
     const int tiles = (n + 7) / 8;
-    for (int tile = blockIdx.x * kGateSmemWarps + warp; tile < tiles; tile += gridDim.x * kGateSmemWarps) {
+    const int wpc = blockDim.x >> 5;   // warps per CTA (host-chosen so the CTAs cover the SMs evenly)
+    for (int tile = blockIdx.x * wpc + warp; tile < tiles; tile += gridDim.x * wpc) {
         const int t = tile * 8 + g;
         const bool tok = t < n;
         const bf16* xr = x + (long long)(tok ? t : 0) * ldx + (long long)q * Q;
@@ -635,16 +636,28 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     const size_t smem_bytes = (size_t)(nt_need <= 2 ? nt_need : 4) * 8 * gate_smem_stride(M) * sizeof(double);
     if (M % 64 == 0 && nt_need <= 2 && smem_bytes <= 200 * 1024 && gate_dmma_enabled()) {
         const int tiles = (n + 7) / 8;
-        const int blocks = (int)std::min<long long>((tiles + kGateSmemWarps - 1) / kGateSmemWarps, kNumSMs * 2);
+        // warps per CTA (one 8-token tile each): the fewest tiles on the busiest SM, e.g. 7 warps x 147
+        // CTAs for 8192 tokens instead of 8 x 128 (20 SMs idle); one CTA per SM holds the Wg^T copy
+        int wpc = kGateSmemWarps;
+        long long best = -1;
+        for (int w = kGateSmemWarps; w >= 4; --w) {
+            const long long ctas = (tiles + w - 1) / w;
+            const long long load = (ctas + kNumSMs - 1) / kNumSMs * w;
+            if (best < 0 || load < best) {
+                best = load;
+                wpc = w;
+            }
+        }
+        const int blocks = (int)std::min<long long>((tiles + wpc - 1) / wpc, kNumSMs * 2);
         if (nt_need == 1) {
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
-            launch_k(gate_fwd_dmma_smem_kernel<1>, blocks, kGateSmemWarps * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
+            launch_k(gate_fwd_dmma_smem_kernel<1>, blocks, wpc * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
                                                                                         expert_idx, combine_w, probs);
         } else {
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
-            launch_k(gate_fwd_dmma_smem_kernel<2>, blocks, kGateSmemWarps * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
+            launch_k(gate_fwd_dmma_smem_kernel<2>, blocks, wpc * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
                                                                                         expert_idx, combine_w, probs);
         }
     } else if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
