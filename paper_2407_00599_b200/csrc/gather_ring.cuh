@@ -258,7 +258,6 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
             const int cols = min(kCols, M - c0);
             const uint32_t qs = phase_base + q, st = qs % S;
             const PickB<KT> b = bcast(mine, i);
-            // the gate term's weights do not depend on the stage: load them before waiting
             bar_wait(bar0 + 8 * st, (qs / S) & 1);
             const bf16* sb = ring + st * STAGE;
             float acc[2][8];
