@@ -653,24 +653,24 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
             launch_k(gate_fwd_dmma_smem_kernel<1>, blocks, wpc * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
-                                                                                        expert_idx, combine_w, probs);
+                expert_idx, combine_w, probs);
         } else {
             cudaFuncSetAttribute(gate_fwd_dmma_smem_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes);
             launch_k(gate_fwd_dmma_smem_kernel<2>, blocks, wpc * 32, smem_bytes, s, X, ldx, W, n, M, E, k,
-                                                                                        expert_idx, combine_w, probs);
+                expert_idx, combine_w, probs);
         }
     } else if (M % (16 * kDmmaWarps * 2) == 0 && gate_dmma_enabled()) {   // span per lane a multiple of 8
         const int blocks = (int)std::min<long long>((n + 7) / 8, (long long)kNumSMs * 64);
         if (E <= 8)
             launch_k(gate_fwd_dmma_kernel<1>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
-                                                                       probs);
+                probs);
         else if (E <= 16)
             launch_k(gate_fwd_dmma_kernel<2>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
-                                                                       probs);
+                probs);
         else
             launch_k(gate_fwd_dmma_kernel<4>, blocks, kDmmaWarps * 32, 0, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
-                                                                       probs);
+                probs);
     } else if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 4)

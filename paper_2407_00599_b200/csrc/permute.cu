@@ -608,7 +608,7 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
     const long long total = (long long)nseg * el * rows;
     if (total == 0) return 0;
     launch_k(push_rows_kernel, row_grid(total), kRowThreads, 0, s, reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
-                                                             fill, dst);
+        fill, dst);
     PARM_CHECK_LAUNCH("push_rows");
     return 0;
 }
@@ -709,11 +709,11 @@ int combine_fwd_fan(const SlotView& y, const int* expert_idx, const int* slot_id
         if (y.n_p == 1) {
             auto kern = ring::combine_fwd_ring<1, S>;
             launch_k(kern, ring::grid_for(kern, smem, n, per_sm1), kRowThreads, smem, s, y, expert_idx, slot_idx, combine_w,
-                                                                                 n, k, M, O, ldo);
+                n, k, M, O, ldo);
         } else {
             auto kern = ring::combine_fwd_ring<2, S>;
             launch_k(kern, ring::grid_for(kern, smem, n, per_sm2), kRowThreads, smem, s, y, expert_idx, slot_idx, combine_w,
-                                                                                 n, k, M, O, ldo);
+                n, k, M, O, ldo);
         }
         PARM_CHECK_LAUNCH("combine_fwd");
         return 0;
@@ -736,10 +736,10 @@ int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* e
     const SlotView nov{};
     if (k <= 2)
         launch_k(combine_bwd_kernel<2, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
-                 probs, n, k, E, M, dlogits, none, nov);
+            probs, n, k, E, M, dlogits, none, nov);
     else
         launch_k(combine_bwd_kernel<8, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
-                 probs, n, k, E, M, dlogits, none, nov);
+            probs, n, k, E, M, dlogits, none, nov);
     PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
 }
@@ -770,17 +770,17 @@ int combine_bwd_dispatch(const void* dout, long long ldd, const SlotView& y, con
     if (dst != nullptr) {
         if (k <= 2)
             launch_k(combine_bwd_kernel<2, 2>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
-                     M, dlogits, sc, *dst);
+                M, dlogits, sc, *dst);
         else
             launch_k(combine_bwd_kernel<8, 2>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
-                     M, dlogits, sc, *dst);
+                M, dlogits, sc, *dst);
     } else {
         if (k <= 2)
             launch_k(combine_bwd_kernel<2, 1>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
-                     M, dlogits, sc, nov);
+                M, dlogits, sc, nov);
         else
             launch_k(combine_bwd_kernel<8, 1>, grid, kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx, probs, n, k, E,
-                     M, dlogits, sc, nov);
+                M, dlogits, sc, nov);
     }
     PARM_CHECK_LAUNCH("combine_bwd_dispatch");
     return 0;
@@ -809,11 +809,11 @@ int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_
         if (dr.n_p == 1) {
             auto kern = ring::dispatch_bwd_ring<1, S>;
             launch_k(kern, ring::grid_for(kern, smem, n, per_sm1), kRowThreads, smem, s, dr, expert_idx, slot_idx, dlogits,
-                                                                                 W, n, k, E, M, DX, ldx);
+                W, n, k, E, M, DX, ldx);
         } else {
             auto kern = ring::dispatch_bwd_ring<2, S>;
             launch_k(kern, ring::grid_for(kern, smem, n, per_sm2), kRowThreads, smem, s, dr, expert_idx, slot_idx, dlogits,
-                                                                                 W, n, k, E, M, DX, ldx);
+                W, n, k, E, M, DX, ldx);
         }
         PARM_CHECK_LAUNCH("dispatch_bwd");
         return 0;
@@ -822,13 +822,13 @@ int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_
     // measured 39 us against 30 us for loading them per use; kept for E <= 8 experiments only)
     if (k <= 2 && E <= 8 && getenv("PARM_DBWD_REGS"))
         launch_k(dispatch_bwd_kernel<2, 4, 8>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
-                                                                                      W, n, k, E, M, DX, ldx);
+            W, n, k, E, M, DX, ldx);
     else if (k <= 2)
         launch_k(dispatch_bwd_kernel<2, 4, 0>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
-                                                                                      W, n, k, E, M, DX, ldx);
+            W, n, k, E, M, DX, ldx);
     else
         launch_k(dispatch_bwd_kernel<8, 1, 0>, row_grid(n), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits, W, n, k,
-                                                                            E, M, DX, ldx);
+            E, M, DX, ldx);
     PARM_CHECK_LAUNCH("dispatch_bwd");
     return 0;
 }
