@@ -607,7 +607,12 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
     PARM_CHECK_ARG(M % 8 == 0 && fill != nullptr, "push_rows: M=%d must be a multiple of 8, fill required", M);
     const long long total = (long long)nseg * el * rows;
     if (total == 0) return 0;
-    launch_k(push_rows_kernel, row_grid(total), kRowThreads, 0, s, reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
+    int grid = row_grid(total);
+    if (const char* e = getenv("PARM_PUSH_MAX_CTAS")) {   // probe knob: NVLink store rate vs issuing SMs
+        const int cap = atoi(e);
+        if (cap > 0 && cap < grid) grid = cap;
+    }
+    launch_k(push_rows_kernel, grid, kRowThreads, 0, s, reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
         fill, dst);
     PARM_CHECK_LAUNCH("push_rows");
     return 0;
