@@ -72,6 +72,12 @@ def test_argument_validation_without_a_gpu(lib):
                       match="16-byte aligned")
     _expect_arg_error(lib.parm_combine_fwd, None, None, None, None, 4, 1, 8, None, 8, None,
                       match="null slot view")
+    _expect_arg_error(lib.parm_combine_bwd_dispatch, None, 8, None, None, None, None, None, 4, 2, 4, 8, None, 0, 4,
+                      None, None, 8, 8, None, None, match="null slot view")
+    y = _lib.SlotViewC()
+    y.ptr, y.e_local, y.n_p, y.slot_div = 4096, 4, 1, 1 << 30
+    _expect_arg_error(lib.parm_combine_bwd_dispatch, None, 8, ctypes.byref(y), None, None, None, None, 4, 2, 4, 8,
+                      None, 0, 4, None, None, 8, 8, None, None, match="combine weights and fill required")
     desc = _lib.GemmDescC()
     desc.kind = 7
     _expect_arg_error(lib.parm_gemm, ctypes.byref(desc), None, match="bad kind")
