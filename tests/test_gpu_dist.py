@@ -42,3 +42,21 @@ def test_nccl_parity(world):
         print(f"attempt {attempt}: rc={res.returncode}\n{res.stdout[-2000:]}\n{res.stderr[-2000:]}")
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert f"DIST PARITY OK (P={world}" in res.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fullsize_peer_equals_nccl(world):
+    """Bench-size S1 step (tools/dist_fullsize.py): slice routing bit-exact against the oracle gate,
+    and the fused NVLink transport bit-identical to the NCCL transport."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs (have {torch.cuda.device_count()})")
+    for attempt in range(2):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               str(ROOT / "tools" / "dist_fullsize.py")]
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=dict(os.environ))
+        if res.returncode == 0:
+            break
+        print(f"attempt {attempt}: rc={res.returncode}\n{res.stdout[-2000:]}\n{res.stderr[-2000:]}")
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert f"FULLSIZE OK (P={world}" in res.stdout
