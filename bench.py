@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="time only the headline schedule")
     ap.add_argument("--eager", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--transport", choices=("peer", "nccl"), default="peer",
+                    help="N>1: S1/S2 over NVLink peer memory (fused kernels; default) or NCCL collectives")
+    ap.add_argument("--no-api-e2e", action="store_true", help="skip the api.run_schedule (NumPy) e2e leg")
     return ap.parse_args()
 
 
@@ -212,17 +215,20 @@ def pick_schedule(cfg, layout, requested: str):
 
 
 def make_step(layer, schedule, xs, ds, use_graph: bool):
-    """One fwd+bwd step: a replayed CUDA graph (default) or eager launches."""
+    """One fwd+bwd step: a replayed CUDA graph (default) or eager launches.
+    Returns (step, outs, dxs): the layer's output / input-gradient buffers the step writes."""
     if use_graph:
         g = layer.capture_step(schedule, xs, ds)
-        return g.replay
-    return lambda: (layer.forward(schedule, xs), layer.backward(ds))
+        return g.replay, g.outs, g.dxs
+    outs = layer.forward(schedule, xs)
+    dxs = layer.backward(ds)
+    return (lambda: (layer.forward(schedule, xs), layer.backward(ds))), outs, dxs
 
 
 def time_steps(layer, schedule, xs, ds, steps, warmup, dist, dev, use_graph=True):
     import torch
 
-    step = make_step(layer, schedule, xs, ds, use_graph)
+    step = make_step(layer, schedule, xs, ds, use_graph)[0]
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
@@ -316,11 +322,15 @@ def layer_roofline(cfg, layout, schedule: str, ms: float, tc_peak: float, hbm_gb
 
 
 def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_graph=True):
-    """Public-API step with host buffers: H2D of the step's tokens and upstream
-    gradient from pinned memory (double-buffered on a copy stream), fwd+bwd,
-    and a D2H read of the step's routing metric (per-expert fill).  S1 splits
-    the MP group's tokens (paper §IV-C): a rank gates, dispatches and
-    back-propagates only its slice, so only the slice's rows cross PCIe."""
+    """The step as a user runs it, a full round trip every step: the step's tokens and upstream
+    gradient copied H2D from pinned host memory, forward + backward through the layer API,
+    and the step's results -- the layer output and the input gradient -- copied back D2H into
+    pinned host memory.  Copies are double-buffered on two copy streams (H2D of step i+1 and
+    D2H of step i-1 overlap step i); each step's results are first snapshotted on the device
+    (two D2D copies inside the timed region) so the next step may overwrite the layer's
+    buffers.  S1 splits the MP group's tokens (paper §IV-C): a rank gates, dispatches and
+    back-propagates only its slice, so only the slice's rows cross PCIe (the MP group as a
+    whole moves every token once)."""
     import torch
 
     r = layer.ranks[0]
@@ -329,40 +339,55 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
         sl = layer.d.n // layer.d.MP
         lo = layer.layout.mp_pos(r) * sl
         hi = lo + sl
+    M = host_x.shape[1]
     comp = torch.cuda.current_stream()
-    cps = torch.cuda.Stream()
-    dx = [torch.empty(host_x.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
-    dd = [torch.empty(host_d.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    bx = [torch.empty(host_x.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    bd = [torch.empty(host_d.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    so = [torch.empty(hi - lo, M, dtype=torch.bfloat16, device=dev) for _ in range(2)]     # result snapshots
+    sd = [torch.empty(hi - lo, M, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    ho = [torch.empty(hi - lo, M, dtype=torch.bfloat16).pin_memory() for _ in range(2)]   # host results
+    hdx = [torch.empty(hi - lo, M, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]
-    metric = torch.empty(layer.d.E, dtype=torch.int32).pin_memory()
-    for f in free:
-        f.record(comp)
-    steps_fn = [make_step(layer, schedule, {r: dx[sl]}, {r: dd[sl]}, use_graph) for sl in range(2)]
-
+    done = [torch.cuda.Event() for _ in range(2)]
+    back = [torch.cuda.Event() for _ in range(2)]
+    for e in free + back:
+        e.record(comp)
+    fns = [make_step(layer, schedule, {r: bx[k]}, {r: bd[k]}, use_graph) for k in range(2)]
     copy_ev = []
 
-    def prefetch(slot):
-        with torch.cuda.stream(cps):
-            cps.wait_event(free[slot])
+    def prefetch(k):
+        with torch.cuda.stream(h2d_s):
+            h2d_s.wait_event(free[k])
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(cps)
-            dx[slot][lo:hi].copy_(host_x[lo:hi], non_blocking=True)
-            dd[slot][lo:hi].copy_(host_d[lo:hi], non_blocking=True)
-            c1.record(cps)
+            c0.record(h2d_s)
+            bx[k][lo:hi].copy_(host_x[lo:hi], non_blocking=True)
+            bd[k][lo:hi].copy_(host_d[lo:hi], non_blocking=True)
+            c1.record(h2d_s)
             copy_ev.append((c0, c1))
-            ready[slot].record(cps)
+            ready[k].record(h2d_s)
 
     def run(total):
         prefetch(0)
         for i in range(total):
-            s = i % 2
+            k = i % 2
             if i + 1 < total:
                 prefetch((i + 1) % 2)
-            comp.wait_event(ready[s])
-            steps_fn[s]()
-            metric.copy_(layer.routing(r).fill, non_blocking=True)
-            free[s].record(comp)
+            comp.wait_event(ready[k])
+            fn, outs, dxs = fns[k]
+            fn()
+            free[k].record(comp)
+            comp.wait_event(back[k])                  # snapshot k's previous contents are on the host
+            so[k].copy_(outs[r][lo:hi])
+            sd[k].copy_(dxs[r][lo:hi])
+            done[k].record(comp)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(done[k])
+                ho[k].copy_(so[k], non_blocking=True)
+                hdx[k].copy_(sd[k], non_blocking=True)
+                back[k].record(d2h_s)
+        comp.wait_stream(d2h_s)
 
     run(warmup)
     torch.cuda.synchronize()
@@ -371,20 +396,57 @@ def time_e2e(layer, schedule, host_x, host_d, steps, warmup, dist, dev, use_grap
     copy_ev.clear()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
-    cps.wait_event(e0)
+    h2d_s.wait_event(e0)
     run(steps)
-    e1.record(comp)
+    e1.record(comp)                                   # after the last step's results reached the host
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     time_e2e.h2d_ms = statistics.median(a.elapsed_time(b) for a, b in copy_ev)   # copy engine time per step
+    time_e2e.result_check = (torch.equal(ho[(steps - 1) % 2], so[(steps - 1) % 2].cpu()) and
+                             torch.equal(hdx[(steps - 1) % 2], sd[(steps - 1) % 2].cpu()))
     if dist is not None:
         dist.barrier()
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    h2d = 2 * host_x[lo:hi].numel() * 2
-    d2h = layer.d.E * 4
+    h2d = 2 * (hi - lo) * M * 2
+    d2h = 2 * (hi - lo) * M * 2
     return ms, h2d, d2h
+
+
+def time_api_e2e(cfg, layout, rank, dist, calls: int = 3) -> dict:
+    """The reference's own entry point: api.run_schedule (moesched dataplane.py:183), NumPy f64
+    inputs (P/MP, B*L, M) in, NumPy f64 outputs (P, B*L, M) + trace + drop set out -- forward
+    only, like the reference.  Wall clock per call (host API, synchronous), max over ranks."""
+    import numpy as np
+    import torch
+
+    from paper_2407_00599_b200 import api
+    from paper_2407_00599_b200.config import ClusterSpec
+
+    w = api.ExpertWeights.generate(cfg, seed=0)
+    inputs = np.random.default_rng(1).normal(size=(layout.world_size // layout.mp_size, cfg.tokens_per_rank,
+                                                   cfg.embed_dim))
+    cluster = ClusterSpec(1, layout.world_size, 4e-10, 4e-9)
+    api.run_schedule("s1", cfg, layout, cluster, w, inputs)          # weights uploaded, buffers built
+    samples = []
+    for _ in range(calls):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = api.run_schedule("s1", cfg, layout, cluster, w, inputs)
+        samples.append(time.perf_counter() - t0)
+    s = statistics.median(samples)
+    if dist is not None:
+        t = torch.tensor([s], device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = float(t.item())
+    tokens = layout.world_size // layout.mp_size * cfg.tokens_per_rank
+    return {"value": tokens / s, "unit": "tokens/s (forward only)", "ms_per_call": s * 1e3,
+            "h2d_bytes_per_call": int(inputs.nbytes), "d2h_bytes_per_call": int(res.outputs.nbytes),
+            "api": "api.run_schedule('s1', ...) -- the reference's NumPy float64 boundary (dataplane.py:183), "
+                   "forward only as in the reference; every rank returns all ranks' outputs"}
 
 
 def gemm_roofline(layer, schedule, xs, ds, steps, dist, dev):
@@ -438,7 +500,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         transport = "nccl"
         w = None
-        if os.environ.get("PARM_PEER", "1") != "0":
+        if args.transport == "peer":
             try:
                 w = PeerWorld(layout, dev)
                 transport = "nvlink-peer (S1, S2) + nccl (baseline)"
@@ -450,6 +512,11 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         w = LocalWorld(layout, dev)
     layer = MoELayer(cfg, layout, w)
     layer.init_random(seed=0)
+    # like-for-like: the same schedules over NCCL collectives (same world, same communicators)
+    layer_nccl = None
+    if world > 1 and layer.peer and not args.no_compare:
+        layer_nccl = MoELayer(cfg, layout, w, peer=False)
+        layer_nccl.init_random(seed=0)
     g = torch.Generator(device=dev).manual_seed(1000 + rank // layout.mp_size)
     x = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, generator=g, device=dev).to(torch.bfloat16)
     dout = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, generator=g, device=dev).to(torch.bfloat16)
@@ -466,11 +533,19 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     layer.backward(ds)
     launches = (_lib.launch_count - n0) * args.steps          # our kernels per step x timed steps
     ms = time_steps(layer, schedule, xs, ds, args.steps, args.warmup, dist, dev, use_graph)
-    clk = clocks.stop() if clocks else None
     sched_ms[schedule] = ms
     for s in others:
         sched_ms[s] = time_steps(layer, s, xs, ds, args.steps, args.warmup, dist, dev, use_graph)
+    # the dominant kernel's roofline, inside the same clock record as the timed steps
     roof = gemm_roofline(layer, schedule, xs, ds, max(3, min(args.steps, 10)), dist, dev)
+    clk = clocks.stop() if clocks else None
+    sched_ms_nccl = {}
+    if layer_nccl is not None:
+        for s in ("baseline", "s1", "s2"):
+            sched_ms_nccl[s] = time_steps(layer_nccl, s, xs, ds, args.steps, args.warmup, dist, dev, use_graph)
+    api_e2e = None
+    if not args.no_api_e2e:
+        api_e2e = time_api_e2e(cfg, layout, rank, dist)
     e2e = None
     if not args.no_e2e:
         aff = os.sched_getaffinity(0)
@@ -488,26 +563,40 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         tps = tokens_per_step(cfg, layout)
         e2e = {"value": tps / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "api": "MoELayer.forward/backward with pinned-host inputs (H2D double-buffered on a copy stream; "
-                      "S1 copies each rank's MP token slice)",
+               "api": "MoELayer.forward/backward; every step: tokens + upstream gradient H2D from pinned host "
+                      "memory, layer output + input gradient D2H into pinned host memory (double-buffered on "
+                      "copy streams; S1: each rank moves its MP token slice)",
+               "results_on_host_verified": bool(time_e2e.result_check),
                "h2d_gbs_measured": h2d_gbs, "host_numa_cpus": numa, "h2d_ms_per_step_in_loop": h2d_ms,
                "repetitions_ms": [r[0] for r in reps]}
+        if api_e2e is not None:
+            e2e["run_schedule"] = api_e2e
     if rank != 0:
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
         return
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("bf16_tflops_sustained")
-    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
-    if peak is None:
-        peak, peak_src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    burst = peaks.get("bf16_tflops")
+    sustained = peaks.get("bf16_tflops_sustained")
+    if burst is None or sustained is None:
+        burst, sustained = 1590.0, 1590.0
+        src = "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    # the burst figure applies when the clock record shows the SMs at (or within 3% of) max clock
+    # during the timed steps and the GEMM timing; the sustained one when they ran clocked down
+    at_max = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"])
+    if burst != sustained:
+        peak = burst if at_max else sustained
+        src = ("MEASURED_PEAKS.json bf16_tflops (burst): median SM clock at max during the measurement"
+               if at_max else "MEASURED_PEAKS.json bf16_tflops_sustained: SM clock below max during the measurement")
+    peak_src = src
     achieved = roof["alg_flops_per_launch"] / (roof["avg_launch_ms"] / 1e3) / 1e12
     traffic = None
     tfile = ROOT / "profiles" / "gemm_traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "frac_burst": achieved / burst, "frac_sustained": achieved / sustained,
                 "traffic": traffic, "peak_source": peak_src, "kernel": roof["kernel"],
                 "avg_launch_ms": roof["avg_launch_ms"], "launches_sampled": roof["launches"],
                 "alg_flops_per_launch": roof["alg_flops_per_launch"],
@@ -530,6 +619,14 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         "schedules_ms": sched_ms,
         "speedup_vs_baseline_schedule": (sched_ms["baseline"] / ms) if "baseline" in sched_ms and
                                         schedule != "baseline" else None,
+        "schedules_ms_nccl": sched_ms_nccl or None,
+        "speedup_vs_baseline_schedule_same_transport": (
+            sched_ms_nccl["baseline"] / sched_ms_nccl[schedule]) if sched_ms_nccl and schedule != "baseline" else (
+            sched_ms["baseline"] / ms if "baseline" in sched_ms and not layer.peer and schedule != "baseline"
+            else None),
+        "speedup_note": ("speedup_vs_baseline_schedule: the selected schedule on this run's transport vs the "
+                         "baseline (DeepSpeed-MoE order, always on NCCL collectives); _same_transport: both on "
+                         "NCCL collectives" if world > 1 else None),
         "selector": sel,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "launch_mode": "eager" if args.eager else "cuda_graph (one replay per step; NCCL calls captured)",

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 12
+#define PARM_ABI_VERSION 13
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -66,6 +66,8 @@ typedef struct parm_peer_signal {
     void* counter;             /* uint32 on this device: epoch, advanced by every barrier */
     int rank;
     int n;
+    long long timeout_ns;      /* a waiting rank traps after this long without every peer (<= 0: 300 s);
+                                  host-side skew between ranks (checkpoints, eval) must stay inside it */
 } parm_peer_signal;
 
 int parm_abi_version(void);

@@ -49,7 +49,7 @@ class IntFanC(ctypes.Structure):
 
 
 class PeerSignalC(ctypes.Structure):
-    _fields_ = [("pad", _vp * MAX_PEERS), ("counter", _vp), ("rank", _c_int), ("n", _c_int)]
+    _fields_ = [("pad", _vp * MAX_PEERS), ("counter", _vp), ("rank", _c_int), ("n", _c_int), ("timeout_ns", _c_ll)]
 
 
 class RowsC(ctypes.Structure):
@@ -97,7 +97,7 @@ SIGNATURES = {
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 
 class ParmError(RuntimeError):

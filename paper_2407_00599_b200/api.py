@@ -156,14 +156,27 @@ def expert_shard_forward(rows, w1_shard, w2_shard) -> np.ndarray:
 _LAYER_CACHE: dict = {}
 
 
+def _dist_key() -> tuple:
+    """Which world make_world would build right now (process group size and rank, or local)."""
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return ("dist", dist.get_world_size(), dist.get_rank())
+    except ImportError:  # pragma: no cover
+        pass
+    return ("local",)
+
+
 def _layer(cfg: MoEConfig, layout: ParallelLayout, weights) -> MoELayer:
-    world = make_world(layout)
-    key = (cfg, layout, type(world).__name__)
+    # The world (and, under torchrun, its NCCL sub-communicators) is built only on a cache miss
+    # and lives with the cached layer: a hit creates no process groups.
+    key = (cfg, layout, _dist_key())
     lay = _LAYER_CACHE.get(key)
     if lay is None:
         if len(_LAYER_CACHE) > 8:
             _LAYER_CACHE.clear()
-        lay = MoELayer(cfg, layout, world)
+        lay = MoELayer(cfg, layout, make_world(layout))
         _LAYER_CACHE[key] = lay
     if getattr(lay, "_weights_id", None) is not weights:
         lay.load_weights(weights)

@@ -13,7 +13,7 @@ reference convention: gathered length for allgather, per-rank buffer length
 otherwise.  The overlap key is fitted like the reference's acceptance suite
 (test_acceptance.py:285-294): t(A2A(ep&esp, x) with AG(mp, x*MP/ESP)) - t(AG(mp, x*MP/ESP)),
 the pair executed exactly as S2's return runs it (MoELayer._saa: sequential unless
-PARM_SAA=phased), so the selector prices the overlap this hardware actually delivers.
+the layer runs with saa="phased"; --saa here), so the selector prices the overlap this hardware actually delivers.
 """
 
 from __future__ import annotations
@@ -27,7 +27,6 @@ import torch
 import torch.distributed as dist
 
 from .config import ParallelLayout, group_members
-from .runtime import _saa_phased
 from .selector import FIT_HEADER, fit_profile, write_profile_csv
 from .world import Msg, NcclWorld
 
@@ -82,7 +81,7 @@ def _a2a_msgs(world: NcclWorld, kind: str, send: torch.Tensor, recv: torch.Tenso
     return msgs
 
 
-def measure(layout: ParallelLayout, dev) -> list[tuple[str, str, float, float]]:
+def measure(layout: ParallelLayout, dev, saa: str = "seq") -> list[tuple[str, str, float, float]]:
     world = NcclWorld(layout, dev)
     rows = []
     bf = dict(dtype=torch.bfloat16, device=dev)
@@ -125,7 +124,7 @@ def measure(layout: ParallelLayout, dev) -> list[tuple[str, str, float, float]]:
             ag_n -= ag_n % layout.ep_size
             ag_src, ag_out = torch.randn(ag_n, **bf), torch.empty(layout.ep_size, mp_g, ag_n // layout.ep_size, **bf)
             ag = lambda: world.allgather("mp", {world.rank: ag_src}, {world.rank: ag_out})  # noqa: E731
-            if _saa_phased(layout):
+            if saa == "phased" and layout.ep_size > 1:
                 src_blocks = ag_src.view(layout.ep_size, -1)
 
                 def saa():
@@ -154,6 +153,7 @@ def main(argv=None) -> int:
     ap.add_argument("--layout", default=None, help="MP,EP,ESP (default: bench layout for the world size)")
     ap.add_argument("--out", default="profiles/nvlink_profile.csv")
     ap.add_argument("--samples-out", default=None)
+    ap.add_argument("--saa", choices=("seq", "phased"), default="seq", help="S2 return execution to price (overlap key)")
     args = ap.parse_args(argv)
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -165,7 +165,7 @@ def main(argv=None) -> int:
     else:
         mp, ep, esp = {2: (2, 1, 2), 4: (2, 2, 2), 8: (2, 4, 2)}[P]
     layout = ParallelLayout(mp, ep, esp, P)
-    rows = measure(layout, dev)
+    rows = measure(layout, dev, args.saa)
     if dist.get_rank() == 0:
         lines = [",".join(FIT_HEADER)] + [f"{c},{g},{x},{t:.9g}" for c, g, x, t in rows]
         samples_path = args.samples_out or args.out.replace(".csv", "_samples.csv")

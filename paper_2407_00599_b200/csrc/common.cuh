@@ -178,6 +178,7 @@ struct PeerSignal {
     void* counter;
     int rank;
     int n;
+    long long timeout_ns;
 };
 
 }  // namespace parm

@@ -647,7 +647,14 @@ int fan_copy(const void* src, long long bytes, const RowFan& dst, cudaStream_t s
 // (release, system scope, after a system fence that publishes this rank's
 // earlier peer stores), then waits until every peer's epoch has reached its
 // own pad.  The epoch lives in device memory, so a replayed CUDA graph
-// advances it like an eager launch.  A watchdog traps instead of hanging.
+// advances it like an eager launch.  A watchdog (wall clock, %globaltimer)
+// traps after sig.timeout_ns instead of hanging the GPU on a dead peer.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
     pdl_entry();
     __shared__ unsigned epoch;
@@ -663,12 +670,12 @@ __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
         unsigned* slot = reinterpret_cast<unsigned*>(sig.pad[j]) + sig.rank;
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
         const unsigned* mine = reinterpret_cast<const unsigned*>(sig.pad[sig.rank]) + j;
-        const long long t0 = clock64();
-        while (true) {
+        const unsigned long long t0 = globaltimer_ns();
+        for (unsigned it = 0;; ++it) {
             unsigned v;
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
             if ((int)(v - epoch) >= 0) break;
-            if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");   // ~4 s: a peer never arrived
+            if ((it & 1023u) == 1023u && (long long)(globaltimer_ns() - t0) > sig.timeout_ns) asm volatile("trap;");
         }
     }
     __syncthreads();
@@ -678,7 +685,9 @@ int peer_barrier(const PeerSignal& sig, cudaStream_t s) {
     PARM_CHECK_ARG(sig.n >= 1 && sig.n <= kMaxPeers && sig.rank >= 0 && sig.rank < sig.n,
                    "peer_barrier: bad rank %d of %d", sig.rank, sig.n);
     PARM_CHECK_ARG(sig.counter != nullptr, "peer_barrier: null epoch counter");
-    launch_k(peer_barrier_kernel, 1, 32, 0, s, sig);
+    PeerSignal g = sig;
+    if (g.timeout_ns <= 0) g.timeout_ns = 300ll * 1000000000ll;
+    launch_k(peer_barrier_kernel, 1, 32, 0, s, g);
     PARM_CHECK_LAUNCH("peer_barrier");
     return 0;
 }

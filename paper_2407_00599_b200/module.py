@@ -26,17 +26,33 @@ from .world import World, make_world
 
 
 class _MoEFunction(torch.autograd.Function):
+    """The layer keeps ONE set of activation buffers (routing, received rows, H and its ReLU
+    mask) per schedule, so a backward is only valid for the most recent forward.  Each forward
+    stamps a generation number into ctx; a backward whose forward has since been overwritten
+    (microbatch loops running all forwards first, an eval forward in between) raises instead
+    of silently returning the gradients of another batch.  x is saved through
+    save_for_backward so autograd's version counter catches in-place edits of the input (the
+    gate weight gradient reads it)."""
+
     @staticmethod
     def forward(ctx, x, gate, w1, w2, mod):          # noqa: D401 - autograd signature
         mod._sync_compute_weights()
         r = mod.rank
         out = mod.layer.forward(mod.schedule, {r: x})[r]
+        mod._generation += 1
         ctx.mod = mod
+        ctx.generation = mod._generation
+        ctx.save_for_backward(x)
         return out.clone()                           # the layer reuses its output buffer next call
 
     @staticmethod
     def backward(ctx, dout):
         mod = ctx.mod
+        if ctx.generation != mod._generation:
+            raise RuntimeError("ParmMoE: backward of a forward whose activations were overwritten by a later "
+                               "forward (one outstanding forward per module; run backward before the next "
+                               "forward, or use one ParmMoE per microbatch in flight)")
+        ctx.saved_tensors                            # autograd's in-place check of x
         r = mod.rank
         dx = mod.layer.backward({r: dout.contiguous().to(torch.bfloat16)})[r].clone()
         d, s = mod.layer.d, mod.layer.st[r]
@@ -64,6 +80,7 @@ class ParmMoE(nn.Module):
         self.w1 = nn.Parameter(torch.randn(d.e_local, d.M, d.Hs, generator=gen, device=dev) / math.sqrt(d.M))
         self.w2 = nn.Parameter(torch.randn(d.e_local, d.Hs, d.M, generator=gen, device=dev) / math.sqrt(d.H))
         self._synced = None
+        self._generation = 0
 
     def _sync_compute_weights(self) -> None:
         """bf16 compute copies (transposed, padded layouts of MoELayer) from the fp32 masters."""

@@ -47,7 +47,7 @@ import torch
 
 from . import kernels as K
 from .config import MoEConfig, ParallelLayout, check_compatible, derive_capacity, group_members
-from .world import Msg, PeerWorld, World, make_world
+from .world import Msg, World, make_world
 
 SCHEDULES = ("baseline", "s1", "s2")
 
@@ -121,7 +121,7 @@ class RankState:
     dw1t: torch.Tensor            # (e_local, Hsp, Mp) f32
     dw2t: torch.Tensor            # (e_local, Mp, Hsp) f32
     bufs: dict = field(default_factory=dict)
-    gate64: torch.Tensor | None = None   # exact f64 upcast of `gate` for the f64 logits (refresh_gate())
+    gate64: torch.Tensor | None = None   # exact f64 upcast of `gate` for the f64 logits (refresh_gate(), in place)
 
 
 @dataclass
@@ -137,43 +137,57 @@ class StepGraph:
         self.graph.replay()
 
 
-def _saa_phased(layout: ParallelLayout) -> bool:
-    """Whether S2's return runs as the phased SAA (see MoELayer._saa).
-
-    Default: sequential.  On one NVSwitch box the return A2A and the MP AllGather
-    share the same NVLink ports, and the phased overlap measured 8% slower than
-    back-to-back collectives over the P=4 selector sweep (profiles/selector_sweep_p4*).
-    PARM_SAA=phased selects the paper's overlapped form (balanced rotation when
-    N_EP divides the number of MP groups)."""
-    return os.environ.get("PARM_SAA", "seq") == "phased" and layout.mp_size > 1 and layout.ep_size > 1
+S1_RETURNS = ("epilogue", "push", "pull")
+S2_RETURNS = ("pull", "push")
+SAA_MODES = ("seq", "phased")
 
 
 class MoELayer:
-    """One MoE layer under MP+EP+ESP on the ranks this process owns."""
+    """One MoE layer under MP+EP+ESP on the ranks this process owns.
 
-    def __init__(self, cfg: MoEConfig, layout: ParallelLayout, world: World | None = None, device=None):
+    Execution options (all paths are parity-tested against the oracle; the defaults are
+    the measured-fastest on B200, DESIGN.md §(e)):
+
+    ``s1_return``  peer-memory S1 only: how expert outputs (and dR) go back to the owners.
+                   ``epilogue`` -- the second GEMM's TMA epilogue stores each tile straight
+                   into the owner's receive block over NVLink (default); ``push`` -- a copy
+                   kernel pushes the filled rows after the GEMM; ``pull`` -- the owners'
+                   combine gathers from the holders through a peer slot view.
+    ``s2_return``  peer-memory S2: ``pull`` (owners gather through the slot-shard view,
+                   default; measured 0.84 vs 0.85 ms for ``push`` at N=4) or ``push``
+                   (holders store MP copies of every row: the AllGather as pushes).
+    ``saa``        NCCL/local S2 return: ``seq`` (A2A then AllGather, default; the phased
+                   overlap measured 8% slower on NVSwitch, which shares the ports) or
+                   ``phased`` (the paper's SAA, per-expert-block rotation).
+    ``peer``       None (default): S1/S2 use the fused peer-memory path whenever the world
+                   maps peers (PeerWorld / PeerLocalWorld); False: the separate collectives
+                   even there (like-for-like schedule comparisons on one transport).  The
+                   baseline (DeepSpeed-MoE ordering) always runs on the collectives."""
+
+    def __init__(self, cfg: MoEConfig, layout: ParallelLayout, world: World | None = None, device=None, *,
+                 s1_return: str = "epilogue", s2_return: str = "pull", saa: str = "seq", peer: bool | None = None):
         check_compatible(cfg, layout)
         if cfg.top_k > 8 or cfg.num_experts > 32:
             raise ValueError("B200 kernels support top_k <= 8 and num_experts <= 32")
+        for name, v, ok in (("s1_return", s1_return, S1_RETURNS), ("s2_return", s2_return, S2_RETURNS),
+                            ("saa", saa, SAA_MODES)):
+            if v not in ok:
+                raise ValueError(f"{name} must be one of {ok}, got {v!r}")
         self.cfg = cfg
         self.layout = layout
         self.world = world if world is not None else make_world(layout, device)
         self.dev = self.world.device
         self.d = Dims.of(cfg, layout)
         d = self.d
-        self.saa_phased = _saa_phased(layout)
-        # S1/S2 over NVLink peer memory (fused dispatch/return/AllGather) when the world maps peers
-        self.peer = (isinstance(self.world, PeerWorld) and d.P > 1 and os.environ.get("PARM_PEER", "1") != "0")
-        # S1's return path: holders push expert outputs into the owners' receive blocks ("push", one
-        # NVLink pass reused by combine and combine-backward) or owners gather them ("pull")
-        self.peer_push = os.environ.get("PARM_PEER_RETURN", "push") == "push"
-        # S2 pushes MP copies of every row (its AllGather), measured no faster than the owners'
-        # gathers through the slot-shard view (N=4: 0.85 vs 0.84 ms), so S2 pulls by default
-        self.peer_push_s2 = os.environ.get("PARM_PEER_RETURN_S2", "pull") == "push"
-        # S1 push from the GEMM epilogue itself (tile by tile, overlapping the math) instead of a copy kernel
-        self.peer_epilogue = os.environ.get("PARM_PEER_EPILOGUE", "1") != "0"
-        # combine backward and the dOut dispatch fused into one pass over dOut
-        self.fused_dy = os.environ.get("PARM_FUSED_DY", "1") != "0"
+        self.saa_phased = saa == "phased" and layout.mp_size > 1 and layout.ep_size > 1
+        # S1/S2 over (NVLink) peer memory: dispatch/return/AllGather fused into the kernels
+        if peer and not self.world.maps_peers:
+            raise ValueError(f"peer=True needs a world that maps peer memory, got {type(self.world).__name__}")
+        self.peer = self.world.maps_peers and d.P > 1 and peer is not False
+        self.peer_push = s1_return in ("epilogue", "push")
+        self.peer_epilogue = s1_return == "epilogue"
+        self.peer_push_s2 = s2_return == "push"
+        self.options = {"s1_return": s1_return, "s2_return": s2_return, "saa": saa, "peer": self.peer}
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -181,7 +195,8 @@ class MoELayer:
             self.st[r] = RankState(r, torch.zeros(d.E, d.Mp, **bf), torch.zeros(d.e_local, d.Hsp, d.Mp, **bf),
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **bf), torch.zeros(d.E, d.Mp, **f32),
                                    torch.zeros(d.e_local, d.Hsp, d.Mp, **f32),
-                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
+                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **f32),
+                                   gate64=torch.zeros(d.E, d.Mp, dtype=torch.float64, device=self.dev))
         self._last: str | None = None
         self._ws_gate = None
         self.refresh_gate()
@@ -209,9 +224,10 @@ class MoELayer:
         self.refresh_gate()
 
     def refresh_gate(self) -> None:
-        """Re-derive the f64 upcast of the bf16 gate weights (call after updating ``gate``)."""
+        """Re-derive the f64 upcast of the bf16 gate weights (call after updating ``gate``).
+        In place: a captured StepGraph keeps reading the same buffer and sees the update."""
         for s in self.st.values():
-            s.gate64 = s.gate.double()
+            s.gate64.copy_(s.gate)
 
     def init_random(self, seed: int = 0) -> None:
         """Synthetic weights drawn directly on the device with the reference's
@@ -249,8 +265,8 @@ class MoELayer:
         W = self.world
         b: dict = {}
         if peer and schedule == "s1":   # symmetric: every MP peer writes its slice rows into them (fused AllGather)
-            b["out"], b["out_peers"] = W.sym((d.n, d.Mp))
-            b["dx"], b["dx_peers"] = W.sym((d.n, d.Mp))
+            b["out"], b["out_peers"] = W.sym((d.n, d.Mp), rank=r)
+            b["dx"], b["dx_peers"] = W.sym((d.n, d.Mp), rank=r)
         else:
             b["out"], b["dx"] = torch.zeros(d.n, d.Mp, **bf), torch.zeros(d.n, d.Mp, **bf)
         if d.M != d.Mp:
@@ -268,9 +284,9 @@ class MoELayer:
                 b["send"] = torch.zeros(d.E, q, d.Mp, **bf)
                 b["dsend"] = torch.zeros(d.E, q, d.Mp, **bf)
             if peer:         # holders' receive buffers, written by the sources' dispatch kernels
-                b["recv"], b["recv_peers"] = W.sym((d.P, 1, el, q, d.Mp))
-                b["dyrecv"], b["dyrecv_peers"] = W.sym((d.P, 1, el, q, d.Mp))
-                b["fill_in"], b["fill_in_peers"] = W.sym((d.P, 1, el), torch.int32)
+                b["recv"], b["recv_peers"] = W.sym((d.P, 1, el, q, d.Mp), rank=r)
+                b["dyrecv"], b["dyrecv_peers"] = W.sym((d.P, 1, el, q, d.Mp), rank=r)
+                b["fill_in"], b["fill_in_peers"] = W.sym((d.P, 1, el), torch.int32, rank=r)
             elif d.P == 1:   # no exchange: the slot tensors ARE the GEMM operands
                 b["recv"] = b["send"].view(1, 1, d.E, q, d.Mp)
                 b["dyrecv"] = b["dsend"].view(1, 1, d.E, q, d.Mp)
@@ -298,20 +314,20 @@ class MoELayer:
         b["hmask"] = torch.zeros(*shape, d.Hsp // 32, dtype=torch.int32, device=dev)   # H > 0, one bit each
         b["dh"] = torch.zeros(*shape, d.Hsp, **bf)
         if peer:             # expert outputs, gathered by the owners' combine / dispatch-backward kernels
-            b["y"], b["y_peers"] = W.sym((*shape, d.Mp))
-            b["dr"], b["dr_peers"] = W.sym((*shape, d.Mp))
+            b["y"], b["y_peers"] = W.sym((*shape, d.Mp), rank=r)
+            b["dr"], b["dr_peers"] = W.sym((*shape, d.Mp), rank=r)
         else:
             b["y"] = torch.zeros(*shape, d.Mp, **bf)
             b["dr"] = torch.zeros(*shape, d.Mp, **bf)
         if peer:
             if schedule == "s1" and d.MP > 1:           # MP members' gate-gradient partials [mp_pos][E][M]
-                b["gsum"], b["gsum_peers"] = W.sym((d.MP, d.E, d.Mp), torch.float32)
+                b["gsum"], b["gsum_peers"] = W.sym((d.MP, d.E, d.Mp), torch.float32, rank=r)
             if schedule == "s1" and self.peer_push:     # owners' receive blocks [holder][i][slot]
-                b["ret"], b["ret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
-                b["dret"], b["dret_peers"] = W.sym((d.P, el, b["q"], d.Mp))
+                b["ret"], b["ret_peers"] = W.sym((d.P, el, b["q"], d.Mp), rank=r)
+                b["dret"], b["dret_peers"] = W.sym((d.P, el, b["q"], d.Mp), rank=r)
             if schedule == "s2" and self.peer_push_s2:  # owners' gathered slots [holder][MP shard][i][slot]
-                b["gath"], b["gath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp))
-                b["dgath"], b["dgath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp))
+                b["gath"], b["gath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp), rank=r)
+                b["dgath"], b["dgath_peers"] = W.sym((d.P, d.MP, el, b["q"], d.Mp), rank=r)
         elif schedule == "baseline":
             b["ret"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)        # owner side [holder j][block][i][slot]
             b["dd"] = torch.zeros(d.EP, d.ESP, el, d.T, d.Mp, **bf)
@@ -352,17 +368,10 @@ class MoELayer:
                         slots_out=None) -> None:
         """Combine backward (dlogits) and the dispatch of combine_w * dOut into the slot rows the
         dH GEMM reads (``out``, or the holders' buffers through the peer view ``dst``) -- one
-        fused pass over dOut (PARM_FUSED_DY=0: the two separate kernels)."""
-        if self.fused_dy:
-            K.combine_bwd_dispatch(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, rt.combine_w, dlogits, slot_lo,
-                                   rt.fill, out=out, dst=dst, slots_out=slots_out)
-            return
-        K.combine_bwd(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, dlogits)
-        if dst is None:
-            K.dispatch_rows(dout, rt.slot_src, self.d.k, cap, slot_lo, out, scale=rt.combine_w, fill=rt.fill)
-        else:
-            K.dispatch_rows_peer(dout, rt.slot_src, self.d.k, cap, slot_lo, slots_out, dst, scale=rt.combine_w,
-                                 fill=rt.fill)
+        fused pass over dOut (bit-identical to combine_bwd + dispatch_rows(scale=combine_w),
+        tests/test_gpu_parity.py)."""
+        K.combine_bwd_dispatch(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, rt.combine_w, dlogits, slot_lo,
+                               rt.fill, out=out, dst=dst, slots_out=slots_out)
 
     def _ffn_fwd(self, s: RankState, b: dict, y_peer: tuple | None = None) -> None:
         K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=b["fill_in"])

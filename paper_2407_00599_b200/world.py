@@ -8,15 +8,20 @@ Executors are written once, per rank, against four primitives:
 * ``allgather(kind, ins, outs)``, ``allreduce(kind, bufs)``,
   ``reduce_scatter(kind, ins, outs)`` over the MP / EP / ESP groups.
 
-Two implementations:
+Implementations:
 
 ``NcclWorld``   one process per GPU (torchrun), torch.distributed over NCCL on
                 NVLink/NVSwitch; one sub-communicator per MP/EP/ESP group.
+``PeerWorld``   NcclWorld plus NVLink peer memory (torch symmetric memory):
+                S1/S2's exchanges become loads/stores inside the kernels.
 ``LocalWorld``  every rank of a layout emulated on ONE device with
                 device-to-device copies in place of the wire — the same
                 kernels and buffers per rank, used for single-GPU parity runs
                 over layouts the box cannot host (P up to 16), exactly as the
                 reference simulates all ranks in one process.
+``PeerLocalWorld``  LocalWorld whose ranks' "symmetric" buffers are mapped to each
+                other on the one device: the PeerWorld data path (peer-pointer
+                tables, fused kernels, device barrier) on a single GPU.
 A ``GlooWorld`` variant of NcclWorld (CPU tensors) exercises the multi-process
 message plumbing in the CPU test suite.
 """
@@ -42,6 +47,7 @@ class World:
     layout: ParallelLayout
     ranks: list[int]
     device: torch.device
+    maps_peers = False   # True: ``sym``/``peer_barrier`` exist and S1/S2 run the fused peer-memory path
 
     @property
     def world_size(self) -> int:
@@ -96,23 +102,85 @@ class LocalWorld(World):
                     if chunks[i].data_ptr() != src.data_ptr():
                         chunks[i].copy_(src)
 
+    # Reductions round to the buffer dtype after every addition, as NCCL's ring does for
+    # bf16 (each hop adds in f32 and stores bf16): the emulated ranks see the numerics the
+    # NCCL transport ships (for a 2-member group, bit for bit: round(a + b)).
+    @staticmethod
+    def _sum(parts: list) -> torch.Tensor:
+        acc = parts[0]
+        for p in parts[1:]:
+            acc = (acc.float() + p.float()).to(p.dtype)
+        return acc
+
     def allreduce(self, kind: str, bufs: dict) -> None:
         for grp in groups_of(self.layout, kind):
             if len(grp) == 1:
                 continue
-            acc = bufs[grp[0]].float()
-            for s in grp[1:]:
-                acc += bufs[s].float()
+            acc = self._sum([bufs[s] for s in grp])
             for r in grp:
                 bufs[r].copy_(acc)
 
     def reduce_scatter(self, kind: str, ins: dict, outs: dict) -> None:
         for grp in groups_of(self.layout, kind):
             for i, r in enumerate(grp):
-                acc = ins[grp[0]].reshape(len(grp), -1)[i].float()
-                for s in grp[1:]:
-                    acc = acc + ins[s].reshape(len(grp), -1)[i].float()
+                acc = self._sum([ins[s].reshape(len(grp), -1)[i] for s in grp])
                 outs[r].reshape(-1).copy_(acc)
+
+
+class PeerLocalWorld(LocalWorld):
+    """Every rank of a layout on ONE device, running the NVLink peer-memory data path.
+
+    ``sym`` hands each emulated rank its own zeroed copy of a "symmetric" buffer plus
+    the addresses of every rank's copy -- exactly what ``PeerWorld`` gets from torch
+    symmetric memory, except that the peers' copies live on the same GPU.  So the
+    fused kernels (``dispatch_rows_peer``, the GEMM's peer-epilogue stores,
+    ``combine_fwd_fan``, ``combine_bwd_dispatch`` into the holders, ``dispatch_bwd_fan``,
+    ``fan_copy``, ``push_rows``) run with the same peer-pointer tables, segment
+    offsets and layouts as on a multi-GPU box and can be checked against the oracle on
+    a single GPU.  ``peer_barrier`` launches the real device barrier once per
+    emulated rank, each on its own stream forked from (and joined back to) the
+    current one, so the epoch/signal-pad protocol runs too (graph-capturable)."""
+
+    maps_peers = True
+
+    def __init__(self, layout: ParallelLayout, device: torch.device | str | None = None,
+                 barrier_timeout_s: float = 300.0):
+        super().__init__(layout, device)
+        if layout.world_size > 8:
+            raise ValueError("peer memory is supported within one 8-GPU box")
+        P = layout.world_size
+        self._groups: list[list[torch.Tensor]] = []        # allocation index -> every rank's copy
+        self._next = {r: 0 for r in self.ranks}
+        self._pads = torch.zeros(P, 64, dtype=torch.int32, device=self.device)   # pad[r][j]: epoch of j seen by r
+        self.pads = [self._pads[r].data_ptr() for r in range(P)]
+        self.counters = torch.zeros(P, 16, dtype=torch.int32, device=self.device)
+        self.timeout_s = barrier_timeout_s
+        self._streams = [torch.cuda.Stream(self.device) for _ in range(P)]
+
+    def sym(self, shape, dtype=torch.bfloat16, rank: int = 0) -> tuple[torch.Tensor, list[int]]:
+        """Rank ``rank``'s copy of the next symmetric buffer and every rank's address.
+        Like PeerWorld.sym this is 'collective': the i-th call of each rank names the
+        same buffer, so every rank must request the same buffers in the same order."""
+        i = self._next[rank]
+        self._next[rank] = i + 1
+        if i == len(self._groups):
+            self._groups.append([torch.zeros(tuple(shape), dtype=dtype, device=self.device) for _ in self.ranks])
+        grp = self._groups[i]
+        if tuple(grp[rank].shape) != tuple(shape) or grp[rank].dtype != dtype:
+            raise RuntimeError(f"symmetric allocation {i}: rank {rank} asked for {tuple(shape)} {dtype}, "
+                               f"the group holds {tuple(grp[rank].shape)} {grp[rank].dtype}")
+        return grp[rank], [t.data_ptr() for t in grp]
+
+    def peer_barrier(self) -> None:
+        from . import kernels as K
+
+        cur = torch.cuda.current_stream(self.device)
+        for r, s in enumerate(self._streams):
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                K.peer_barrier(self.pads, self.counters[r], r, self.timeout_s)
+        for s in self._streams:
+            cur.wait_stream(s)
 
 
 class NcclWorld(World):
@@ -208,9 +276,15 @@ class PeerWorld(NcclWorld):
     baseline schedule (the DeepSpeed-ordered reference stays on NCCL)."""
 
     PAD_SLOT = 2048          # u32 index of this runtime's barrier slots inside each signal pad
+    maps_peers = True
 
-    def __init__(self, layout: ParallelLayout, device: torch.device | str | None = None):
+    def __init__(self, layout: ParallelLayout, device: torch.device | str | None = None,
+                 barrier_timeout_s: float = 300.0):
+        """``barrier_timeout_s``: how long a device barrier waits for a peer before it traps
+        (a dead peer must not hang the GPU forever; host-side skew between ranks -- a
+        checkpoint save, an eval pass -- must stay well inside it)."""
         super().__init__(layout, device)
+        self.timeout_s = barrier_timeout_s
         import torch.distributed._symmetric_memory as symm_mem
 
         if layout.world_size > 8:
@@ -235,7 +309,7 @@ class PeerWorld(NcclWorld):
         self._handles.append(h)
         return t, h
 
-    def sym(self, shape, dtype=torch.bfloat16) -> tuple[torch.Tensor, list[int]]:
+    def sym(self, shape, dtype=torch.bfloat16, rank: int | None = None) -> tuple[torch.Tensor, list[int]]:
         """A zeroed symmetric buffer and the address of every rank's copy (rank order).
         Collective: every rank allocates the same buffers in the same order."""
         t, h = self._alloc(tuple(shape), dtype)
@@ -244,7 +318,7 @@ class PeerWorld(NcclWorld):
     def peer_barrier(self) -> None:
         from . import kernels as K
 
-        K.peer_barrier(self.pads, self.counter, self.rank)
+        K.peer_barrier(self.pads, self.counter, self.rank, self.timeout_s)
 
     def release(self) -> None:
         """Drop every symmetric buffer but the barrier's (after the layers using them are gone)."""
@@ -266,4 +340,4 @@ def make_world(layout: ParallelLayout, device=None) -> World:
     return LocalWorld(layout, device)
 
 
-__all__ = ["Msg", "World", "LocalWorld", "NcclWorld", "PeerWorld", "make_world", "group_members"]
+__all__ = ["Msg", "World", "LocalWorld", "PeerLocalWorld", "NcclWorld", "PeerWorld", "make_world", "group_members"]

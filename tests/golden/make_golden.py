@@ -120,6 +120,18 @@ sched_case("p4_ep4", (4, 8, 8, 8, 4, 2, 2.0), (1, 4, 1, 4), 23)
 sched_case("p2_esp2", (4, 8, 8, 16, 4, 2, 1.2), (2, 1, 2, 2), 24)
 # BASELINE config 1 (C1) on bf16-rounded data: routing-bearing row sums only (outputs are 4 MB)
 sched_case("c1_bf16", (4, 128, 256, 512, 4, 2, 1.2), (2, 2, 2, 4), 0, bf16=True, store_outputs=False)
+# the small worlds again on bf16-representable data (what the B200 path computes on), outputs stored,
+# so the drop-in run_schedule can be checked in full against the reference's own outputs
+for nm, cfg_t, lay_t, seed, contig in [
+        ("fig2", (1, 8, 4, 4, 2, 1, 2.0), (2, 2, 2, 4), 4, True),
+        ("fig2_flipped", (1, 8, 4, 4, 2, 1, 2.0), (2, 2, 2, 4), 13, False),
+        ("overflow_mp1", (1, 4, 4, 4, 2, 1, 0.5), (1, 2, 2, 4), 11, True),
+        ("overflow_mp2", (1, 8, 4, 4, 2, 1, 0.5), (2, 2, 2, 4), 12, True),
+        ("p8_c2shape_small", (2, 16, 16, 32, 8, 2, 1.2), (2, 4, 2, 8), 21, True),
+        ("p8_mp4", (2, 16, 8, 16, 8, 2, 2.4), (4, 8, 1, 8), 22, True),
+        ("p4_ep4", (4, 8, 8, 8, 4, 2, 2.0), (1, 4, 1, 4), 23, True),
+        ("p2_esp2", (4, 8, 8, 16, 4, 2, 1.2), (2, 1, 2, 2), 24, True)]:
+    sched_case(nm + "_bf16", cfg_t, lay_t, seed + 100, esp_contiguous=contig, bf16=True)
 
 # ---- fused collectives on random worlds
 for ep, esp, mp in [(2, 2, 1), (4, 2, 2), (2, 4, 2), (8, 1, 4), (1, 4, 1)]:

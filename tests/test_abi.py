@@ -52,7 +52,7 @@ def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(_lib.SlotViewC) == 8 + 4 * 4 + 5 * 8 + 8 * 8 + 2 * 4
     assert ctypes.sizeof(_lib.RowFanC) == 8 * 8 + 8
     assert ctypes.sizeof(_lib.IntFanC) == 8 * 8
-    assert ctypes.sizeof(_lib.PeerSignalC) == 8 * 8 + 8 + 8
+    assert ctypes.sizeof(_lib.PeerSignalC) == 8 * 8 + 8 + 8 + 8
     assert ctypes.sizeof(_lib.RowsC) == 8 + 4 * 8
     assert ctypes.sizeof(_lib.GemmDescC) == 12 * 4 + 4 * ctypes.sizeof(_lib.RowsC) + 8
 

@@ -90,3 +90,56 @@ def test_bench_size_layer_matches_oracle(cuda_lib):
         dw1 = xe.T @ O.round_bf16(dh)
         assert _rel(grads["dw2"][e], dw2) <= 2e-2
         assert _rel(grads["dw1"][e], dw1) <= 2e-2
+
+
+@pytest.mark.parametrize("P,lay", [(2, (2, 1, 2)), (4, (2, 2, 2))])
+def test_bench_size_peer_transport_emulated(cuda_lib, P, lay):
+    """The bench's multi-GPU layouts at full size on one GPU: S1 over PeerLocalWorld (the NVLink
+    transport's fused kernels, peer tables and GEMM-epilogue return, every rank's buffers on this
+    device) -- each rank's slice routing bit-exact against the oracle gate with the S1 quota, and
+    outputs, dx and expert weight gradients bit-identical to the copy-collective transport."""
+    from paper_2407_00599_b200.config import MoEConfig, ParallelLayout, derive_capacity
+    from paper_2407_00599_b200.runtime import MoELayer
+    from paper_2407_00599_b200.world import LocalWorld, PeerLocalWorld
+
+    cfg = MoEConfig(B, L, M, H, E, K, F)
+    mp = lay[0]
+    layout = ParallelLayout(*lay, P)
+    n = B * L
+    w = O.Weights.generate(M, H, E, seed=21)
+    w = O.Weights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
+    G = P // mp
+    rng = np.random.default_rng(22)
+    xs = [O.round_bf16(rng.normal(size=(n, M))) for _ in range(G)]
+    ds = [O.round_bf16(rng.normal(size=(n, M))) for _ in range(G)]
+    res = {}
+    for wk in ("local", "peer"):
+        W = PeerLocalWorld(layout) if wk == "peer" else LocalWorld(layout)
+        layer = MoELayer(cfg, layout, W)
+        assert layer.peer == (wk == "peer")
+        layer.load_weights(w)
+        dev = layer.dev
+        outs = layer.forward("s1", {r: torch.from_numpy(xs[r // mp]).to(dev).to(torch.bfloat16) for r in range(P)})
+        outs = {r: v.clone() for r, v in outs.items()}
+        routes = {r: (layer.routing(r).expert_idx.clone(), layer.routing(r).slot_idx.clone()) for r in range(P)}
+        dxs = layer.backward({r: torch.from_numpy(ds[r // mp]).to(dev).to(torch.bfloat16) for r in range(P)})
+        dxs = {r: v.clone() for r, v in dxs.items()}
+        grads = {r: {k: v.clone() for k, v in layer.shard_grads(r).items()} for r in range(P)}
+        res[wk] = (outs, routes, dxs, grads)
+        del layer, W
+        torch.cuda.empty_cache()
+    q = -(-derive_capacity(cfg) // mp)
+    sl = n // mp
+    for r in range(P):
+        m = layout.mp_pos(r)
+        ref = O.gate(xs[r // mp][m * sl:(m + 1) * sl], w.gate, K, q, token_offset=m * sl)
+        for wk in ("local", "peer"):
+            ei, si = (v.cpu().numpy() for v in res[wk][1][r])
+            np.testing.assert_array_equal(ei, ref.expert_index, err_msg=f"{wk} rank {r}")
+            np.testing.assert_array_equal(si, ref.slot_index, err_msg=f"{wk} rank {r}")
+        a, b = res["local"], res["peer"]
+        assert torch.equal(a[0][r], b[0][r]), f"rank {r} outputs differ"
+        assert torch.equal(a[2][r], b[2][r]), f"rank {r} dx differs"
+        for key in ("dw1", "dw2"):
+            assert torch.equal(a[3][r][key], b[3][r][key]), f"rank {r} {key} differs"
+        torch.testing.assert_close(a[3][r]["dgate"], b[3][r]["dgate"], rtol=1e-5, atol=1e-6)

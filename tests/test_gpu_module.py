@@ -66,3 +66,44 @@ def test_module_trains(cuda_lib):
         opt.step()
         losses.append(float(loss))
     assert losses[-1] < losses[0]
+
+
+def test_module_rejects_backward_of_an_overwritten_forward(cuda_lib):
+    """One activation set per module: a second forward before the first backward must not
+    silently produce gradients of the second batch."""
+    mod, cfg = _module()
+    n, M = cfg.tokens_per_rank, cfg.embed_dim
+    x1 = torch.randn(n, M, device="cuda", requires_grad=True)
+    x2 = torch.randn(n, M, device="cuda", requires_grad=True)
+    out1 = mod(x1)
+    out2 = mod(x2)
+    with pytest.raises(RuntimeError, match="overwritten by a later forward"):
+        out1.float().sum().backward()
+    out2.float().sum().backward()          # the latest forward is still valid
+    assert x2.grad is not None and torch.isfinite(x2.grad).all()
+
+
+def test_captured_step_sees_gate_weight_updates(cuda_lib):
+    """refresh_gate() updates the f64 gate copy in place, so a captured step routes with the new
+    weights (the graph's gate node keeps reading the same buffer)."""
+    from paper_2407_00599_b200.config import MoEConfig, ParallelLayout
+    from paper_2407_00599_b200.runtime import MoELayer
+    from paper_2407_00599_b200.world import LocalWorld
+
+    cfg = MoEConfig(2, 64, 128, 256, 4, 2, 1.2)
+    layout = ParallelLayout(1, 1, 1, 1)
+    layer = MoELayer(cfg, layout, LocalWorld(layout))
+    layer.init_random(0)
+    x = torch.randn(128, 128, device="cuda").to(torch.bfloat16)
+    d = torch.randn(128, 128, device="cuda").to(torch.bfloat16)
+    g = layer.capture_step("s1", {0: x}, {0: d}, warmup=1)
+    g.replay()
+    before = layer.routing(0).expert_idx.clone()
+    layer.init_random(7)                    # new gate weights, refreshed in place
+    g.replay()
+    torch.cuda.synchronize()
+    replayed = layer.routing(0).expert_idx.clone()
+    layer.forward("s1", {0: x})
+    eager = layer.routing(0).expert_idx.clone()
+    assert torch.equal(replayed, eager)
+    assert not torch.equal(before, eager)

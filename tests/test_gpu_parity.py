@@ -5,9 +5,12 @@ Bars:
   * forward activations — max_rel_error (reference dataplane.py:416) <= 1e-2;
   * gradients (dx, dW1, dW2, dWg; no reference, restated oracle) — normwise
     relative error <= 2e-2.
-All P ranks of a layout are emulated on one GPU (LocalWorld) with the same
-kernels and buffers a real rank uses; the NCCL path is covered by
-tests/test_gpu_dist.py.
+All P ranks of a layout are emulated on one GPU with the same kernels and
+buffers a real rank uses: ``LocalWorld`` (device copies in place of the NCCL
+collectives) and ``PeerLocalWorld`` (the NVLink peer-memory data path of
+``PeerWorld`` -- fused dispatch stores, GEMM-epilogue return, fan-out
+AllGathers, device barrier -- with every rank's "peer" buffers on the one
+GPU).  Real multi-GPU runs are in tests/test_gpu_dist.py.
 """
 
 from __future__ import annotations
@@ -167,10 +170,10 @@ LAYER_CASES = [
 ]
 
 
-def _run_layer(cfg_t, lay_t, contig, schedule, seed=0):
+def _run_layer(cfg_t, lay_t, contig, schedule, seed=0, world="local", **opts):
     from paper_2407_00599_b200.config import MoEConfig, ParallelLayout
     from paper_2407_00599_b200.runtime import MoELayer
-    from paper_2407_00599_b200.world import LocalWorld
+    from paper_2407_00599_b200.world import LocalWorld, PeerLocalWorld
 
     cfg = MoEConfig(*cfg_t)
     layout = ParallelLayout(*lay_t, esp_contiguous=contig)
@@ -182,7 +185,9 @@ def _run_layer(cfg_t, lay_t, contig, schedule, seed=0):
     G = layout.world_size // layout.mp_size
     inputs = O.round_bf16(rng.normal(size=(G, n, M)))
     douts = O.round_bf16(rng.normal(size=(G, n, M)))
-    layer = MoELayer(cfg, layout, LocalWorld(layout))
+    W = PeerLocalWorld(layout) if world == "peer" else LocalWorld(layout)
+    layer = MoELayer(cfg, layout, W, **opts)
+    assert layer.peer == (world == "peer" and layout.world_size > 1)
     layer.load_weights(w)
     outs = layer.forward(schedule, {r: _t(inputs[r // layout.mp_size]) for r in layer.ranks})
     routes = {r: layer.routing(r) for r in layer.ranks}
@@ -200,8 +205,9 @@ def _run_layer(cfg_t, lay_t, contig, schedule, seed=0):
 
 @pytest.mark.parametrize("schedule", ["baseline", "s1", "s2"])
 @pytest.mark.parametrize("cfg_t,lay_t,contig", LAYER_CASES)
-def test_layer_fwd_bwd_matches_oracle(cuda_lib, schedule, cfg_t, lay_t, contig):
-    layout, outs, routes, dxs, grads, ref_out, caches, drops, ref_g = _run_layer(cfg_t, lay_t, contig, schedule)
+def test_layer_fwd_bwd_matches_oracle(cuda_lib, schedule, cfg_t, lay_t, contig, world="local", **opts):
+    layout, outs, routes, dxs, grads, ref_out, caches, drops, ref_g = _run_layer(cfg_t, lay_t, contig, schedule,
+                                                                                  world=world, **opts)
     got_drops = set()
     for r in range(layout.world_size):
         g = r // layout.mp_size
@@ -231,10 +237,70 @@ def test_layer_fwd_bwd_matches_oracle(cuda_lib, schedule, cfg_t, lay_t, contig):
     ("phased", (2, 64, 128, 128, 8, 2, 2.4), (4, 8, 1, 8)),   # unbalanced rotation (one MP group)
     ("phased", (2, 64, 64, 128, 16, 4, 1.0), (2, 4, 4, 16)),  # P=16, k=4
 ])
-def test_s2_saa_modes_match_oracle(cuda_lib, monkeypatch, mode, cfg_t, lay_t):
+def test_s2_saa_modes_match_oracle(cuda_lib, mode, cfg_t, lay_t):
     """Both SAA executions (phased per expert block / A2A then AllGather) give the oracle's S2."""
-    monkeypatch.setenv("PARM_SAA", mode)
-    test_layer_fwd_bwd_matches_oracle(cuda_lib, "s2", cfg_t, lay_t, True)
+    test_layer_fwd_bwd_matches_oracle(cuda_lib, "s2", cfg_t, lay_t, True, saa=mode)
+
+
+# --------------------------------------------------------------------------- the peer-memory transport
+PEER_CASES = [c for c in LAYER_CASES if 1 < c[1][3] <= 8]      # P=16 exceeds one box (8 peers)
+PEER_MODES = [("s1", {"s1_return": "epilogue"}), ("s1", {"s1_return": "push"}), ("s1", {"s1_return": "pull"}),
+              ("s2", {"s2_return": "pull"}), ("s2", {"s2_return": "push"})]
+
+
+@pytest.mark.parametrize("schedule,opts", PEER_MODES, ids=[f"{s}-{list(o.values())[0]}" for s, o in PEER_MODES])
+@pytest.mark.parametrize("cfg_t,lay_t,contig", PEER_CASES)
+def test_peer_transport_fwd_bwd_matches_oracle(cuda_lib, schedule, opts, cfg_t, lay_t, contig):
+    """The multi-GPU default transport (PeerWorld's fused kernels and peer-pointer tables) on one GPU:
+    routing bit-exact, forward/gradients within the bars, for every return mode."""
+    test_layer_fwd_bwd_matches_oracle(cuda_lib, schedule, cfg_t, lay_t, contig, world="peer", **opts)
+
+
+@pytest.mark.parametrize("s1_return", ["epilogue", "push", "pull"])
+def test_peer_transport_equals_local_transport(cuda_lib, s1_return):
+    """S1: same arithmetic, different data movement -- the peer path's outputs, dx and expert weight
+    gradients are bit-identical to the LocalWorld (copy-collective) path's.  (S2's peer combine sums
+    the ESP partials in f32 inside the gather; its copy path rounds the ESP sum to bf16 before the
+    AllGather, so S2 is only compared against the oracle.)"""
+    schedule = "s1"
+    cfg_t, lay_t = (4, 128, 256, 512, 4, 2, 1.2), (2, 2, 2, 4)
+    a = _run_layer(cfg_t, lay_t, True, schedule, world="local")
+    b = _run_layer(cfg_t, lay_t, True, schedule, world="peer", s1_return=s1_return)
+    for r in range(4):
+        assert np.array_equal(a[1][r], b[1][r]), f"rank {r} outputs differ"
+        assert np.array_equal(a[3][r], b[3][r]), f"rank {r} dx differs"
+        for key in ("dw1", "dw2"):
+            assert np.array_equal(a[4][r][key], b[4][r][key]), f"rank {r} {key} differs"
+        # gate gradient: NCCL-order f32 all-reduce vs fixed-order sum of the fanned partials
+        np.testing.assert_allclose(a[4][r]["dgate"], b[4][r]["dgate"], rtol=1e-5, atol=1e-6)
+
+
+def test_peer_transport_graph_replay_equals_eager(cuda_lib):
+    """A captured S1 peer step (barrier epochs advance on every replay) reproduces the eager step."""
+    import torch
+
+    from paper_2407_00599_b200.config import MoEConfig, ParallelLayout
+    from paper_2407_00599_b200.runtime import MoELayer
+    from paper_2407_00599_b200.world import PeerLocalWorld
+
+    cfg = MoEConfig(4, 128, 256, 512, 4, 2, 1.2)
+    layout = ParallelLayout(2, 2, 2, 4)
+    w = O.Weights.generate(256, 512, 4, seed=3)
+    w = O.Weights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
+    rng = np.random.default_rng(4)
+    xs = {r: _t(O.round_bf16(rng.normal(size=(512, 256)))) for r in range(4)}
+    ds = {r: _t(O.round_bf16(rng.normal(size=(512, 256)))) for r in range(4)}
+    for s in ("s1", "s2"):
+        layer = MoELayer(cfg, layout, PeerLocalWorld(layout))
+        layer.load_weights(w)
+        outs = {r: v.clone() for r, v in layer.forward(s, xs).items()}
+        dxs = {r: v.clone() for r, v in layer.backward(ds).items()}
+        g = layer.capture_step(s, xs, ds, warmup=1)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        for r in range(4):
+            assert torch.equal(g.outs[r], outs[r]) and torch.equal(g.dxs[r], dxs[r]), f"{s} rank {r}"
 
 
 def test_schedules_agree_when_no_slice_overflow(cuda_lib):
@@ -248,29 +314,56 @@ def test_schedules_agree_when_no_slice_overflow(cuda_lib):
 
 # --------------------------------------------------------------------------- drop-in API vs golden reference runs
 def test_run_schedule_matches_reference_golden(cuda_lib, golden):
+    """The drop-in run_schedule against the real reference's recorded runs (tests/golden, made by
+    importing moesched), 17 worlds x 3 schedules.  Traces and ffn_rows exact everywhere.  On the
+    bf16-representable worlds (the data the B200 path computes on): drop sets exact and the FULL
+    outputs of every rank within max_rel_error 1e-2 of the reference's stored outputs (C1, whose
+    4 MB of outputs are not stored: of the oracle, pinned to that reference run by its row sums).
+    On the f64 worlds the API rounds inputs to bf16, which can legitimately move a near-tie top-k
+    choice, so drops and outputs are checked against the oracle on the rounded data instead.
+    api.oracle_errors reproduces the reference's own oracle_error on the bf16 worlds."""
     from paper_2407_00599_b200 import api
     from paper_2407_00599_b200.config import ClusterSpec, MoEConfig, ParallelLayout
 
     meta, arr = golden
     for case in meta["schedules"]:
-        if not case["bf16"]:
-            continue
         cfg = MoEConfig(*case["cfg"])
         layout = ParallelLayout(*case["layout"], esp_contiguous=case["esp_contiguous"])
+        olay = O.Layout(*case["layout"], esp_contiguous=case["esp_contiguous"])
         w = api.ExpertWeights.generate(cfg, seed=case["seed"])
-        w = api.ExpertWeights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
-        inputs = O.round_bf16(np.random.default_rng(case["seed"] + 1).normal(
-            size=(layout.world_size // layout.mp_size, cfg.tokens_per_rank, cfg.embed_dim)))
+        inputs = np.random.default_rng(case["seed"] + 1).normal(
+            size=(layout.world_size // layout.mp_size, cfg.tokens_per_rank, cfg.embed_dim))
+        if case["bf16"]:
+            w = api.ExpertWeights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
+            inputs = O.round_bf16(inputs)
+        wr = O.Weights(O.round_bf16(w.gate), O.round_bf16(w.w1), O.round_bf16(w.w2))
         cluster = ClusterSpec(1, layout.world_size, 4e-10, 4e-9)
         for s, rec in case["results"].items():
+            tag = f"{case['name']} {s}"
             res = api.run_schedule(s, cfg, layout, cluster, w, inputs)
-            assert sorted(map(list, res.dropped)) == rec["dropped"]
-            assert res.ffn_rows == rec["ffn_rows"]
+            assert res.outputs.shape == (layout.world_size, cfg.tokens_per_rank, cfg.embed_dim)
+            assert res.ffn_rows == rec["ffn_rows"], tag
             assert [[r.collective, r.group, r.group_size, r.elements, r.wire_per_rank, r.phases, r.overlapped]
-                    for r in res.trace] == rec["trace"]
-            rs = arr[rec["row_sums"]]
-            scale = max(1.0, float(np.abs(rs).max()))
-            assert float(np.abs(res.outputs.sum(axis=2) - rs).max()) / scale < 5e-2
+                    for r in res.trace] == rec["trace"], tag
+            oref, _, odrops = O.schedule_forward(s, cfg.tokens_per_rank, wr, cfg.top_k, cfg.capacity_factor, olay,
+                                                 O.round_bf16(inputs))
+            oref = np.stack([oref[r] for r in range(layout.world_size)])
+            if case["bf16"]:
+                assert sorted(map(list, res.dropped)) == rec["dropped"], tag
+                if "outputs" in rec:
+                    ref = arr[rec["outputs"]]
+                else:
+                    np.testing.assert_allclose(oref.sum(axis=2), arr[rec["row_sums"]], rtol=1e-9, atol=1e-9)
+                    ref = oref
+                oe = api.oracle_errors(cfg, layout, w, inputs, res)
+                assert abs(oe - rec["oracle_error"]) <= 2 * FWD_TOL, \
+                    f"{tag}: oracle_errors {oe:.3e} vs the reference's {rec['oracle_error']:.3e}"
+            else:
+                assert res.dropped == odrops, tag
+                ref = oref
+            for r in range(layout.world_size):
+                e = api.max_rel_error(res.outputs[r], ref[r])
+                assert e <= FWD_TOL, f"{tag} rank {r}: max_rel_error {e:.3e}"
 
 
 def test_reference_forward_golden_vector(cuda_lib, golden):
