@@ -122,10 +122,24 @@ def run_reference_arm(args, rank: int, world: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(cfg, layout, "oracle"),
-        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
+                         "reference_anchor": reference_anchor()},
         "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_anchor() -> dict | None:
+    """profiles/cpu_anchor.json (tools/cpu_anchor.py, build container): the oracle port's forward
+    timed beside the real reference's reference_forward on the same inputs and host."""
+    try:
+        a = json.loads((ROOT / "profiles" / "cpu_anchor.json").read_text())
+    except (OSError, ValueError):
+        return None
+    return {"port_speed_over_reference": {str(r["tokens"]): round(r["port_over_reference_speed"], 3)
+                                          for r in a["rows"]},
+            "outputs_identical": all(r["max_rel_error_port_vs_reference"] == 0.0 for r in a["rows"]),
+            "source": "profiles/cpu_anchor.json (moesched.reference_forward vs the port, same host, forward)"}
 
 
 def config_block(cfg, layout, schedule) -> dict:
@@ -609,7 +623,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         rate, dt, cores = oracle_step_rate(cfg, layout, CPU_SAMPLE_TOKENS, 3)
         cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"{CPU_SAMPLE_TOKENS} of {cfg.tokens_per_rank} tokens, full M/H/E, f64 NumPy oracle "
-                         f"fwd+bwd, 3 steps ({dt:.2f} s/step)"}
+                         f"fwd+bwd, 3 steps ({dt:.2f} s/step)", "reference_anchor": reference_anchor()}
     tps = tokens_per_step(cfg, layout)
     line = {
         "metric": METRIC, "value": tps / (ms / 1e3), "unit": "tokens/s", "n_gpus": args.gpus,

@@ -175,8 +175,11 @@ int parm_push_rows(const void* src, int nseg, int e_local, int rows, int M, cons
  * every MP peer, e.g. S1's gate-weight gradient partials (replaces its MP all-reduce). */
 int parm_fan_copy(const void* src, long long bytes, const parm_row_fan* dst, void* stream);
 
-/* Device-side barrier of the n peers (one tiny kernel; graph-capturable). */
-int parm_peer_barrier(const parm_peer_signal* sig, void* stream);
+/* Device-side barrier of the n peers (one tiny kernel; graph-capturable).  sigs[0..count)
+ * are the ranks this process hosts: 1 for one rank per GPU; a single-GPU emulation of
+ * all n ranks passes n descriptors and gets ONE cooperative launch with a CTA per rank,
+ * so ranks that wait on one another are co-resident by construction. */
+int parm_peer_barrier(const parm_peer_signal* sigs, int count, void* stream);
 
 /* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic two-pass).
  * accumulate != 0 adds into dwg. */

@@ -91,7 +91,7 @@ SIGNATURES = {
                                       ctypes.POINTER(RowFanC), _c_ll, _vp]),
     "parm_dispatch_bwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
                                        ctypes.POINTER(RowFanC), _c_ll, _vp]),
-    "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _vp]),
+    "parm_peer_barrier": (_c_int, [ctypes.POINTER(PeerSignalC), _c_int, _vp]),
     "parm_push_rows": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, ctypes.POINTER(RowFanC), _vp]),
     "parm_fan_copy": (_c_int, [_vp, _c_ll, ctypes.POINTER(RowFanC), _vp]),
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),

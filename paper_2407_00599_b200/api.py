@@ -84,8 +84,10 @@ def _dev() -> torch.device:
 
 
 def _bf16_dev(a, shape_cols_pad: int | None = None) -> torch.Tensor:
-    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
-    t = t.to(device=_dev(), dtype=torch.bfloat16)
+    """Host (NumPy / torch) or device array -> contiguous bf16 on the GPU; the dtype
+    conversion runs on the device after one H2D of the caller's bytes."""
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    t = t.to(device=_dev()).to(torch.bfloat16)
     if shape_cols_pad is not None and t.shape[-1] != shape_cols_pad:
         pad = torch.zeros(*t.shape[:-1], shape_cols_pad, dtype=torch.bfloat16, device=t.device)
         pad[..., :t.shape[-1]] = t
@@ -211,16 +213,16 @@ def run_schedule(schedule: str, cfg: MoEConfig, layout: ParallelLayout, cluster:
     dropped = set()
     per_rank = {}
     for r in lay.ranks:
-        per_rank[r] = outs[r].float()
+        per_rank[r] = outs[r].contiguous()      # bf16: gathered as is, widened exactly on the way out
         rt = lay.routing(r)
         si = rt.slot_idx.cpu().numpy()
         ei = rt.expert_idx.cpu().numpy()
         g = r // layout.mp_size
         dropped.update((g, rt.token_offset + int(t), int(ei[t, j])) for t, j in zip(*np.nonzero(si < 0)))
-    outputs = np.zeros((layout.world_size, cfg.tokens_per_rank, cfg.embed_dim))
+    outputs = np.empty((layout.world_size, cfg.tokens_per_rank, cfg.embed_dim))
     if isinstance(lay.world, LocalWorld):
         for r, o in per_rank.items():
-            outputs[r] = o.cpu().numpy()
+            torch.from_numpy(outputs[r]).copy_(o.double())
     else:
         import torch.distributed as dist
 
@@ -228,7 +230,7 @@ def run_schedule(schedule: str, cfg: MoEConfig, layout: ParallelLayout, cluster:
         gathered = [torch.empty_like(mine) for _ in range(layout.world_size)]
         dist.all_gather(gathered, mine)
         for r, o in enumerate(gathered):
-            outputs[r] = o.cpu().numpy()
+            torch.from_numpy(outputs[r]).copy_(o.double())
         allsets = [None] * layout.world_size
         dist.all_gather_object(allsets, sorted(dropped))
         dropped = {tuple(x) for s in allsets for x in s}

@@ -42,7 +42,7 @@ int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, 
                     cudaStream_t);
 int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
                      const RowFan&, long long, cudaStream_t);
-int peer_barrier(const PeerSignal&, cudaStream_t);
+int peer_barrier(const PeerSignal*, int, cudaStream_t);
 int push_rows(const void*, int, int, int, int, const int*, const RowFan&, cudaStream_t);
 int fan_copy(const void*, long long, const RowFan&, cudaStream_t);
 
@@ -204,12 +204,15 @@ int parm_fan_copy(const void* src, long long bytes, const parm_row_fan* dst, voi
     return parm::fan_copy(src, bytes, parm::abi_cast<parm::RowFan>(dst), S(stream));
 }
 
-int parm_peer_barrier(const parm_peer_signal* sig, void* stream) {
-    if (!sig) {
-        parm::set_error("peer_barrier: null signal descriptor");
+int parm_peer_barrier(const parm_peer_signal* sigs, int count, void* stream) {
+    if (!sigs || count < 1 || count > PARM_MAX_PEERS) {
+        parm::set_error("peer_barrier: need 1..%d signal descriptors (got %d)", PARM_MAX_PEERS, count);
         return 1;
     }
-    return parm::peer_barrier(parm::abi_cast<parm::PeerSignal>(sig), S(stream));
+    parm::PeerSignal g[PARM_MAX_PEERS];
+    static_assert(sizeof(parm::PeerSignal) == sizeof(parm_peer_signal), "peer signal ABI mismatch");
+    std::memcpy(g, sigs, sizeof(parm_peer_signal) * count);
+    return parm::peer_barrier(g, count, S(stream));
 }
 
 int parm_gemm(const parm_gemm_desc* desc, void* stream) {

@@ -655,8 +655,17 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-__global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
+// One CTA per rank hosted by this process: CTA b is rank sigs[b].rank.  A real
+// multi-GPU rank launches one CTA; the single-GPU emulation of P ranks launches all
+// P in ONE cooperative grid, so the ranks that wait on one another are guaranteed
+// to be co-resident (never as separate launches that nothing forces to overlap).
+struct PeerSignalSet {
+    PeerSignal sig[kMaxPeers];
+};
+
+__global__ void peer_barrier_kernel(const __grid_constant__ PeerSignalSet set) {
     pdl_entry();
+    const PeerSignal& sig = set.sig[blockIdx.x];
     __shared__ unsigned epoch;
     if (threadIdx.x == 0) {
         unsigned* cnt = reinterpret_cast<unsigned*>(sig.counter);
@@ -681,13 +690,32 @@ __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignal sig) {
     __syncthreads();
 }
 
-int peer_barrier(const PeerSignal& sig, cudaStream_t s) {
-    PARM_CHECK_ARG(sig.n >= 1 && sig.n <= kMaxPeers && sig.rank >= 0 && sig.rank < sig.n,
-                   "peer_barrier: bad rank %d of %d", sig.rank, sig.n);
-    PARM_CHECK_ARG(sig.counter != nullptr, "peer_barrier: null epoch counter");
-    PeerSignal g = sig;
-    if (g.timeout_ns <= 0) g.timeout_ns = 300ll * 1000000000ll;
-    launch_k(peer_barrier_kernel, 1, 32, 0, s, g);
+int peer_barrier(const PeerSignal* sigs, int count, cudaStream_t s) {
+    PARM_CHECK_ARG(sigs != nullptr && count >= 1 && count <= kMaxPeers, "peer_barrier: %d local ranks", count);
+    PeerSignalSet set{};
+    for (int b = 0; b < count; ++b) {
+        const PeerSignal& g = sigs[b];
+        PARM_CHECK_ARG(g.n >= 1 && g.n <= kMaxPeers && g.rank >= 0 && g.rank < g.n,
+                       "peer_barrier: bad rank %d of %d", g.rank, g.n);
+        PARM_CHECK_ARG(g.counter != nullptr, "peer_barrier: null epoch counter");
+        PARM_CHECK_ARG(count == 1 || g.n == sigs[0].n, "peer_barrier: local ranks disagree on the group size");
+        set.sig[b] = g;
+        if (set.sig[b].timeout_ns <= 0) set.sig[b].timeout_ns = 300ll * 1000000000ll;
+    }
+    if (count == 1) {
+        launch_k(peer_barrier_kernel, 1, 32, 0, s, set);
+    } else {   // co-residency of the waiting ranks is guaranteed only by a cooperative launch
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(count);
+        cfg.blockDim = dim3(32);
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, peer_barrier_kernel, set);
+    }
     PARM_CHECK_LAUNCH("peer_barrier");
     return 0;
 }

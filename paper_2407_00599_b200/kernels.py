@@ -238,16 +238,19 @@ def fan_copy(src: torch.Tensor, dst_ptrs: list) -> None:
     _lib.call("parm_fan_copy", src.data_ptr(), src.numel() * src.element_size(), ctypes.byref(f), _stream())
 
 
-def peer_barrier(pads: list, counter: torch.Tensor, rank: int, timeout_s: float = 300.0) -> None:
-    """Device-side barrier of len(pads) ranks (signal-pad addresses of every rank, this rank's epoch
-    counter); a rank still waiting after ``timeout_s`` traps rather than hanging the GPU."""
-    s = _lib.PeerSignalC()
-    for i, a in enumerate(pads):
-        s.pad[i] = a
-    s.counter = counter.data_ptr()
-    s.rank, s.n = rank, len(pads)
-    s.timeout_ns = int(timeout_s * 1e9)
-    _lib.call("parm_peer_barrier", ctypes.byref(s), _stream())
+def peer_barrier(pads: list, counters: list, ranks: list, timeout_s: float = 300.0) -> None:
+    """Device-side barrier of len(pads) ranks (signal-pad addresses of every rank) for the ranks
+    this process hosts (``ranks``, each with its epoch counter tensor in ``counters``): one launch,
+    cooperative when it hosts several; a rank still waiting after ``timeout_s`` traps rather than
+    hanging the GPU."""
+    sigs = (_lib.PeerSignalC * len(ranks))()
+    for s, c, r in zip(sigs, counters, ranks):
+        for i, a in enumerate(pads):
+            s.pad[i] = a
+        s.counter = c.data_ptr()
+        s.rank, s.n = r, len(pads)
+        s.timeout_ns = int(timeout_s * 1e9)
+    _lib.call("parm_peer_barrier", sigs, len(ranks), _stream())
 
 
 def esp_sum(view: SlotView, out: torch.Tensor) -> None:

@@ -137,9 +137,9 @@ class PeerLocalWorld(LocalWorld):
     ``combine_fwd_fan``, ``combine_bwd_dispatch`` into the holders, ``dispatch_bwd_fan``,
     ``fan_copy``, ``push_rows``) run with the same peer-pointer tables, segment
     offsets and layouts as on a multi-GPU box and can be checked against the oracle on
-    a single GPU.  ``peer_barrier`` launches the real device barrier once per
-    emulated rank, each on its own stream forked from (and joined back to) the
-    current one, so the epoch/signal-pad protocol runs too (graph-capturable)."""
+    a single GPU.  ``peer_barrier`` runs the real device barrier for all emulated
+    ranks as ONE cooperative launch (a CTA per rank, co-resident by construction), so
+    the epoch/signal-pad protocol runs too (graph-capturable)."""
 
     maps_peers = True
 
@@ -155,7 +155,6 @@ class PeerLocalWorld(LocalWorld):
         self.pads = [self._pads[r].data_ptr() for r in range(P)]
         self.counters = torch.zeros(P, 16, dtype=torch.int32, device=self.device)
         self.timeout_s = barrier_timeout_s
-        self._streams = [torch.cuda.Stream(self.device) for _ in range(P)]
 
     def sym(self, shape, dtype=torch.bfloat16, rank: int = 0) -> tuple[torch.Tensor, list[int]]:
         """Rank ``rank``'s copy of the next symmetric buffer and every rank's address.
@@ -174,13 +173,7 @@ class PeerLocalWorld(LocalWorld):
     def peer_barrier(self) -> None:
         from . import kernels as K
 
-        cur = torch.cuda.current_stream(self.device)
-        for r, s in enumerate(self._streams):
-            s.wait_stream(cur)
-            with torch.cuda.stream(s):
-                K.peer_barrier(self.pads, self.counters[r], r, self.timeout_s)
-        for s in self._streams:
-            cur.wait_stream(s)
+        K.peer_barrier(self.pads, [self.counters[r] for r in self.ranks], self.ranks, self.timeout_s)
 
 
 class NcclWorld(World):
@@ -318,7 +311,7 @@ class PeerWorld(NcclWorld):
     def peer_barrier(self) -> None:
         from . import kernels as K
 
-        K.peer_barrier(self.pads, self.counter, self.rank, self.timeout_s)
+        K.peer_barrier(self.pads, [self.counter], [self.rank], self.timeout_s)
 
     def release(self) -> None:
         """Drop every symmetric buffer but the barrier's (after the layers using them are gone)."""
