@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 13
+#define PARM_ABI_VERSION 14
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -73,34 +73,35 @@ typedef struct parm_peer_signal {
 int parm_abi_version(void);
 const char* parm_last_error(void);
 
-/* Gate, forward: logits (f64 accumulation of bf16 inputs), softmax, stable
- * top-k.  Replaces moesched.dataplane.gate (dataplane.py:86-103).
- * x: (n, M) bf16 row stride ldx; wg_t: gate weights TRANSPOSED, (E, M) f64
- * (the exact upcast of the bf16 weights: no per-element conversion in the
- * f64 dot products).
+/* Gate, forward: logits (f64 accumulation of bf16 inputs -- every product exact,
+ * FP64 tensor cores), softmax, stable top-k.  Replaces moesched.dataplane.gate
+ * (dataplane.py:86-103).
+ * x: (n, M) bf16 row stride ldx; wg_t: gate weights TRANSPOSED, (E, M) bf16.
  * Outputs: expert_idx (n, k) int32 in selection order, combine_w (n, k) f32
- * (= softmax score of the pick), probs (n, E) f32 (nullable). */
+ * (= softmax score of the pick), probs (n, E) f32 (nullable), tile_counts
+ * (nullable, parm_gate_counts_bytes(n, E) bytes): per 8-token tile, the number of
+ * its tokens that picked each expert -- the input of parm_route_dispatch. */
 int parm_gate_fwd(const void* x, long long ldx, const void* wg_t, int n, int M, int E, int k, int* expert_idx,
-                  float* combine_w, float* probs, void* stream);
+                  float* combine_w, float* probs, int* tile_counts, void* stream);
+size_t parm_gate_counts_bytes(int n, int E);
 
-/* Gate, slot pass: token-major capacity fill (dataplane.py:104-116).
- * slot_idx (n, k) int32 (-1 = dropped); slot_src (E, cap) int32 = t*k+j of
- * the pick occupying (e, slot) or -1; fill (E) = filled slots per expert.
- * workspace: parm_gate_slots_workspace(n, E) bytes (per-chunk counts). */
-size_t parm_gate_slots_workspace(int n, int E);
-int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
-                    void* workspace, size_t workspace_bytes, void* stream);
-
-/* Dispatch build by gather: out[e][s'] = x[t] (times scale[t*k+j] when scale
- * is non-null) for the pick in slot s = slot_lo + s', zeros when unfilled or
- * s >= cap.  Writes straight into an AlltoAll send layout.  Replaces the
+/* Slot pass + dispatch in one kernel: token-major capacity fill (dataplane.py:104-116)
+ * from the gate's tile counts -> slot_idx (n, k) int32 (-1 = dropped), slot_src (E, cap)
+ * int32 (= t*k+j of the pick in (e, slot), -1 unfilled), fill (E); and every kept pick
+ * with slot s in [slot_lo, slot_lo + slots_out) copies its token row to row (e, s - slot_lo)
+ * of `out` (E x slots_out rows, strides in elements) -- or, with `dst` (peer view, n_p =
+ * N_ESP dump copies), straight into the holders' receive buffers over NVLink, with the
+ * per-segment fill counts stored into fill_dst (the EP&ESP dispatch AlltoAll fused,
+ * collectives.py:256-283).  Without `dst`, fill_dst (nullable) gets the (E) per-expert fill
+ * of the slot range in ptr[0]; with neither `out` nor `dst` only the slot pass runs.
+ * Rows between each expert's (segment) fill and its last 128-row GEMM tile are zeroed;
+ * rows beyond are not touched.  Replaces the
  * GateOutput.dispatch fill (dataplane.py:101,112) and S2's slot split + pad
- * (dataplane.py:373-378); with scale it is the adjoint of the combine.
- * fill (nullable, per expert): rows s' >= ceil128(clamp(fill[e] - slot_lo, 0,
- * slots_out)) are left untouched -- no GEMM tile reads them. */
-int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
-                       int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
-                       long long out_stride_s, const int* fill, void* stream);
+ * (dataplane.py:373-378). */
+int parm_route_dispatch(const void* x, long long ldx, const int* expert_idx, const int* tile_counts, int n, int k,
+                        int E, int cap, int M, int* slot_idx, int* slot_src, int* fill, int slot_lo, int slots_out,
+                        void* out, long long out_stride_e, long long out_stride_s, const parm_slot_view* dst,
+                        const parm_int_fan* fill_dst, void* stream);
 
 /* Combine: out[t] = sum_j combine_w[t,j] * sum_p Y_p[e_j, s_j] (dropped
  * picks contribute 0).  Fuses fused_combine's local ESP sum
@@ -108,21 +109,14 @@ int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const 
 int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
                      int n, int k, int M, void* out, long long ldo, void* stream);
 
-/* Combine backward: dlogits (n, E) f32 through the softmax scores of the kept
- * picks.  No reference counterpart (the reference has no backward). */
-int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
-                     const int* slot_idx, const float* probs, int n, int k, int E, int M, float* dlogits,
-                     void* stream);
-
-/* Combine backward fused with the backward dispatch of dOut (ABI v12): the
- * dlogits of parm_combine_bwd, and in the same pass over dOut the slot rows
- * parm_dispatch_rows(dOut, scale = combine_w, fill) writes -- row (e, s - slot_lo)
- * <- combine_w[t, j] * dOut[t] for each kept pick with s in [slot_lo, slot_lo +
- * slots_out), zero rows up to each expert's last 128-row GEMM tile.  Rows go to
- * out (+ e * out_stride_e + s * out_stride_s) or, when dst is non-null, to the
- * N_ESP holders through the peer view (the EP&ESP AlltoAll fused, as in
- * parm_dispatch_rows_peer).  Replaces combine_bwd + dispatch_rows (one read of
- * dOut instead of two, one launch instead of two). */
+/* Combine backward fused with the backward dispatch of dOut: the softmax adjoint
+ * dlogits[t, e] = p_e (dS_e - sum_e' p_e' dS_e') with dS_e = <dOut[t], sum_p Y_p[e, s]>
+ * on the kept picks (no reference: SURVEY §8 a27), and in the same pass over dOut the
+ * slot rows -- row (e, s - slot_lo) <- combine_w[t, j] * dOut[t] for each kept pick with
+ * s in [slot_lo, slot_lo + slots_out), zero rows up to each expert's last 128-row GEMM
+ * tile.  Rows go to out (+ e * out_stride_e + s * out_stride_s) or, when dst is
+ * non-null, to the N_ESP holders through the peer view (the EP&ESP AlltoAll fused, as
+ * in parm_route_dispatch).  One read of dOut, one launch. */
 int parm_combine_bwd_dispatch(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
                               const int* slot_idx, const float* probs, const float* combine_w, int n, int k, int E,
                               int M, float* dlogits, int slot_lo, int slots_out, const int* fill, void* out,
@@ -143,15 +137,6 @@ int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, vo
  * into the kernel that produces or consumes the rows.  Buffers are mapped
  * into this process (torch symmetric memory / CUDA IPC); the caller orders
  * them with parm_peer_barrier. */
-
-/* Dispatch fused with the EP&ESP AlltoAll and its dump (collectives.py:256-283):
- * slot rows of this source are stored into every holder's receive buffer,
- * row(e, s, p) of `dst` for p < dst->n_p (the N_ESP holders of e's block),
- * plus the per-segment fill counts clamp(fill[e] - slot_lo, 0, slots_out) into
- * fill_dst->ptr[ep * dst->peer_ep + p * dst->peer_p][e % e_local]. */
-int parm_dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E,
-                            int cap, int slot_lo, int slots_out, int M, const parm_slot_view* dst, const int* fill,
-                            const parm_int_fan* fill_dst, void* stream);
 
 /* combine_fwd reading the expert outputs through a (peer) view -- the return
  * AlltoAll + ESP sum fused into the combine -- and writing each output row to
@@ -201,12 +186,12 @@ typedef struct parm_rows {
 /* Grouped tcgen05/TMEM/TMA GEMM over the MoE layer's segmented expert rows
  * (every row tensor is the AlltoAll receive layout [src_hi][src_lo][expert][r < seg_len][col]).
  * kind 0 (ROW):  D[hi][lo][g][r][n] = alpha * sum_k A[hi][lo][g][r][k] * B[g][n][k]
- *                b_major 0: B stored [g][n][k]; 1: B stored [g][k][n].  K, N % 64 == 0.
+ *                b_major 0: B stored [g][n][k]; 1: B stored [g][k][n].  K % 64 == 0, N % 128 == 0.
  *                epi 0 bf16, 1 relu -> bf16, 2 keep where aux > 0 -> bf16 (aux shaped like D),
  *                5 relu -> bf16 and aux (u32 rows of N/32 words) <- bit mask of the stored
  *                values > 0, 6 keep where that bit mask is set -> bf16.
  * kind 1 (WGT):  D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n]
- *                M % 128 == 0, N % 64 == 0; epi 3 f32, 4 f32 accumulate.
+ *                M % 128 == 0, N % 128 == 0; epi 3 f32, 4 f32 accumulate.
  * fill (nullable, int32 [hi][lo][g]): rows >= fill of a segment are skipped
  * (capacity padding); they must be zero in A for ROW partial tiles.
  * Replaces expert_shard_forward (dataplane.py:122-128) and its adjoints. */

@@ -67,15 +67,13 @@ class GemmDescC(ctypes.Structure):
 SIGNATURES = {
     "parm_abi_version": (_c_int, []),
     "parm_last_error": (ctypes.c_char_p, []),
-    "parm_gate_fwd": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
-    "parm_gate_slots_workspace": (_size, [_c_int, _c_int]),
-    "parm_gate_slots": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _size, _vp]),
-    "parm_dispatch_rows": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
-                                    _c_ll, _c_ll, _vp, _vp]),
+    "parm_gate_fwd": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "parm_gate_counts_bytes": (_size, [_c_int, _c_int]),
+    "parm_route_dispatch": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int,
+                                     _c_int, _vp, _c_ll, _c_ll, ctypes.POINTER(SlotViewC), ctypes.POINTER(IntFanC),
+                                     _vp]),
     "parm_combine_fwd": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_ll,
                                   _vp]),
-    "parm_combine_bwd": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
-                                  _c_int, _vp, _vp]),
     "parm_combine_bwd_dispatch": (_c_int, [_vp, _c_ll, ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int,
                                            _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_ll, _c_ll,
                                            ctypes.POINTER(SlotViewC), _vp]),
@@ -85,8 +83,6 @@ SIGNATURES = {
     "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
     "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
     "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
-    "parm_dispatch_rows_peer": (_c_int, [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
-                                         ctypes.POINTER(SlotViewC), _vp, ctypes.POINTER(IntFanC), _vp]),
     "parm_combine_fwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
                                       ctypes.POINTER(RowFanC), _c_ll, _vp]),
     "parm_dispatch_bwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
@@ -97,7 +93,7 @@ SIGNATURES = {
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 13
+ABI_VERSION = 14
 
 
 class ParmError(RuntimeError):
@@ -134,7 +130,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
 
 
 # Kernel launches each entry point issues on success (bench.py's gpu_launches).
-LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2, "parm_gate_slots": 2}
+LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2}
 launch_count = 0
 
 

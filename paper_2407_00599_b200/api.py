@@ -108,8 +108,8 @@ def gate(tokens, gate_weights, k: int, capacity: int, token_offset: int = 0) -> 
         raise ValueError(f"top_k ({k}) exceeds number of experts ({n_experts})")
     Mp = _ceil(embed, 8)
     x = _bf16_dev(tokens, Mp)
-    wg = torch.zeros(n_experts, Mp, dtype=torch.float64, device=x.device)   # transposed (E, M), f64 upcast of bf16
-    wg[:, :embed] = _bf16_dev(np.ascontiguousarray(np.asarray(gate_weights).T)).double()
+    wg = torch.zeros(n_experts, Mp, dtype=torch.bfloat16, device=x.device)   # transposed (E, M)
+    wg[:, :embed] = _bf16_dev(np.ascontiguousarray(np.asarray(gate_weights).T))
     dev = x.device
     ei = torch.empty(n, k, dtype=torch.int32, device=dev)
     cw = torch.empty(n, k, dtype=torch.float32, device=dev)
@@ -117,14 +117,14 @@ def gate(tokens, gate_weights, k: int, capacity: int, token_offset: int = 0) -> 
     si = torch.empty(n, k, dtype=torch.int32, device=dev)
     ss = torch.empty(n_experts, capacity, dtype=torch.int32, device=dev)
     fill = torch.empty(n_experts, dtype=torch.int32, device=dev)
+    counts = torch.empty(max(1, (n + 7) // 8 * n_experts), dtype=torch.int32, device=dev)
+    disp = torch.zeros(n_experts, capacity, Mp, dtype=torch.bfloat16, device=dev)
     if n:
-        K.gate_fwd(x, wg, k, ei, cw, pr)
-        K.gate_slots(ei, n_experts, capacity, si, ss, fill)
-    disp = torch.empty(n_experts, capacity, Mp, dtype=torch.bfloat16, device=dev)
-    if n:
-        K.dispatch_rows(x, ss, k, capacity, 0, disp)
+        K.gate_fwd(x, wg, k, ei, cw, pr, counts)
+        K.route_dispatch(x, ei, counts, capacity, si, ss, fill, 0, out=disp)
     else:
-        disp.zero_()
+        ss.fill_(-1)
+        fill.zero_()
     ei_h = ei.cpu().numpy().astype(np.int64)
     si_h = si.cpu().numpy().astype(np.int64)
     dropped = {(token_offset + int(t), int(ei_h[t, j])) for t, j in zip(*np.nonzero(si_h < 0))}
@@ -139,7 +139,7 @@ def expert_shard_forward(rows, w1_shard, w2_shard) -> np.ndarray:
         raise ValueError(f"row width {rows.shape[1]} does not match weight rows {w1_shard.shape[0]}")
     n, M = rows.shape
     Hs = w1_shard.shape[1]
-    Mp, Hp, Rp = _ceil(M, 64), _ceil(Hs, 64), _ceil(max(n, 1), 128)
+    Mp, Hp, Rp = _ceil(M, 128), _ceil(Hs, 128), _ceil(max(n, 1), 128)
     dev = _dev()
     x = torch.zeros(1, Rp, Mp, dtype=torch.bfloat16, device=dev)
     x[0, :n, :M] = _bf16_dev(rows)

@@ -18,16 +18,13 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_err; }
 
-int gate_fwd(const void*, long long, const void*, int, int, int, int, int*, float*, float*, cudaStream_t);
-size_t gate_slots_workspace(int, int);
-int gate_slots(const int*, int, int, int, int, int*, int*, int*, int*, size_t, cudaStream_t);
+int gate_fwd(const void*, long long, const void*, int, int, int, int, int*, float*, float*, int*, cudaStream_t);
+size_t gate_counts_bytes(int, int);
+int route_dispatch(const void*, long long, const int*, const int*, int, int, int, int, int, int*, int*, int*, int, int,
+                   void*, long long, long long, const SlotView*, const IntFan*, cudaStream_t);
 size_t gate_wgrad_workspace(int, int, int);
 int gate_wgrad(const void*, long long, const float*, int, int, int, float*, size_t, float*, int, cudaStream_t);
-int dispatch_rows(const void*, long long, const int*, const float*, int, int, int, int, int, int, void*, long long,
-                  long long, const int*, cudaStream_t);
 int combine_fwd(const SlotView&, const int*, const int*, const float*, int, int, int, void*, long long, cudaStream_t);
-int combine_bwd(const void*, long long, const SlotView&, const int*, const int*, const float*, int, int, int, int,
-                float*, cudaStream_t);
 int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int, void*,
                  long long, cudaStream_t);
 int combine_bwd_dispatch(const void*, long long, const SlotView&, const int*, const int*, const float*, const float*,
@@ -36,8 +33,6 @@ int combine_bwd_dispatch(const void*, long long, const SlotView&, const int*, co
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
 int moe_gemm(const parm_gemm_desc&, cudaStream_t);
 int moe_gemm_peer(const parm_gemm_desc&, const RowFan*, long long, long long, cudaStream_t);
-int dispatch_rows_peer(const void*, long long, const int*, const float*, int, int, int, int, int, int,
-                       const SlotView&, const int*, const IntFan*, cudaStream_t);
 int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, int, int, const RowFan&, long long,
                     cudaStream_t);
 int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
@@ -74,23 +69,23 @@ int parm_abi_version(void) { return PARM_ABI_VERSION; }
 const char* parm_last_error(void) { return parm::last_error(); }
 
 int parm_gate_fwd(const void* x, long long ldx, const void* wg, int n, int M, int E, int k, int* expert_idx,
-                  float* combine_w, float* probs, void* stream) {
-    return parm::gate_fwd(x, ldx, wg, n, M, E, k, expert_idx, combine_w, probs, S(stream));
+                  float* combine_w, float* probs, int* tile_counts, void* stream) {
+    return parm::gate_fwd(x, ldx, wg, n, M, E, k, expert_idx, combine_w, probs, tile_counts, S(stream));
 }
 
-size_t parm_gate_slots_workspace(int n, int E) { return parm::gate_slots_workspace(n, E); }
+size_t parm_gate_counts_bytes(int n, int E) { return parm::gate_counts_bytes(n, E); }
 
-int parm_gate_slots(const int* expert_idx, int n, int k, int E, int cap, int* slot_idx, int* slot_src, int* fill,
-                    void* workspace, size_t workspace_bytes, void* stream) {
-    return parm::gate_slots(expert_idx, n, k, E, cap, slot_idx, slot_src, fill, reinterpret_cast<int*>(workspace),
-                            workspace_bytes, S(stream));
-}
-
-int parm_dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
-                       int slot_lo, int slots_out, int M, void* out, long long out_stride_e,
-                       long long out_stride_s, const int* fill, void* stream) {
-    return parm::dispatch_rows(x, ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, out, out_stride_e,
-                               out_stride_s, fill, S(stream));
+int parm_route_dispatch(const void* x, long long ldx, const int* expert_idx, const int* tile_counts, int n, int k,
+                        int E, int cap, int M, int* slot_idx, int* slot_src, int* fill, int slot_lo, int slots_out,
+                        void* out, long long out_stride_e, long long out_stride_s, const parm_slot_view* dst,
+                        const parm_int_fan* fill_dst, void* stream) {
+    parm::SlotView v;
+    parm::IntFan f;
+    if (dst) v = to_view(dst);
+    if (fill_dst) f = parm::abi_cast<parm::IntFan>(fill_dst);
+    return parm::route_dispatch(x, ldx, expert_idx, tile_counts, n, k, E, cap, M, slot_idx, slot_src, fill, slot_lo,
+                                slots_out, out, out_stride_e, out_stride_s, dst ? &v : nullptr,
+                                fill_dst ? &f : nullptr, S(stream));
 }
 
 int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,
@@ -100,16 +95,6 @@ int parm_combine_fwd(const parm_slot_view* y, const int* expert_idx, const int* 
         return 1;
     }
     return parm::combine_fwd(to_view(y), expert_idx, slot_idx, combine_w, n, k, M, out, ldo, S(stream));
-}
-
-int parm_combine_bwd(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
-                     const int* slot_idx, const float* probs, int n, int k, int E, int M, float* dlogits,
-                     void* stream) {
-    if (!y) {
-        parm::set_error("combine_bwd: null slot view");
-        return 1;
-    }
-    return parm::combine_bwd(dout, ld_dout, to_view(y), expert_idx, slot_idx, probs, n, k, E, M, dlogits, S(stream));
 }
 
 int parm_combine_bwd_dispatch(const void* dout, long long ld_dout, const parm_slot_view* y, const int* expert_idx,
@@ -151,19 +136,6 @@ int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, i
                     size_t workspace_bytes, float* dwg, int accumulate, void* stream) {
     return parm::gate_wgrad(x, ldx, dlogits, n, M, E, reinterpret_cast<float*>(workspace), workspace_bytes, dwg,
                             accumulate, S(stream));
-}
-
-int parm_dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E,
-                            int cap, int slot_lo, int slots_out, int M, const parm_slot_view* dst, const int* fill,
-                            const parm_int_fan* fill_dst, void* stream) {
-    if (!dst) {
-        parm::set_error("dispatch_rows_peer: null destination view");
-        return 1;
-    }
-    parm::IntFan fan{};
-    if (fill_dst) fan = parm::abi_cast<parm::IntFan>(fill_dst);
-    return parm::dispatch_rows_peer(x, ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, to_view(dst), fill,
-                                    fill_dst ? &fan : nullptr, S(stream));
 }
 
 int parm_combine_fwd_fan(const parm_slot_view* y, const int* expert_idx, const int* slot_idx, const float* combine_w,

@@ -40,44 +40,19 @@ const char* last_error();
 
 constexpr int kNumSMs = 148;
 
-// ---------------------------------------------------------------- programmatic dependent launch
-// Every kernel of the layer can be launched with programmatic stream
-// serialization (PDL): its CTAs may be scheduled while the previous kernel on the stream is
-// still draining, run their independent prologue (barrier init, TMEM alloc,
-// descriptor prefetch), and block in pdl_wait() -- griddepcontrol.wait, which
-// returns once the previous grid has completed and its memory is visible --
-// before touching any buffer.  pdl_trigger() lets the next kernel launch early.
-// Without the launch attribute both are no-ops.  Off by default: in the
-// graph-captured step it measured no faster (0.764 vs 0.763 ms at N=1) --
-// the kernels' inputs all come from the kernel before, so only launch latency
-// overlaps, and graph launches already hide that.  PARM_PDL=1 turns it on.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_entry() {
-    pdl_wait();
-    pdl_trigger();
-}
-
-inline bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("PARM_PDL");
-        return e != nullptr && e[0] == '1';
-    }();
-    return on;
-}
-
+// Kernel launch through cudaLaunchKernelEx (one place to attach launch attributes).
+// Programmatic dependent launch was measured and left out: inside the graph-captured
+// step every kernel's inputs come from the kernel before it, so only launch latency
+// could overlap, and graph launches already hide that (0.764 vs 0.763 ms at N=1).
 template <typename... Exp, typename... Act>
 inline void launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Act&&... args) {
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
     cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
 }
 

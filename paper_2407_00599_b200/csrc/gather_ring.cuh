@@ -16,6 +16,9 @@
 // shuffles.  Arithmetic, order of accumulation and outputs are those of the
 // register kernels; the views must be local (n_peer == 0) with every row
 // 16-byte aligned -- otherwise the host launches the register kernels.
+// (Measured against an 8-token-group variant that issued one bulk copy per
+// (token, pick) lane: bulk-copy operands must be warp-uniform, so per-lane
+// copies serialise in a waterfall loop -- 22 vs 14 us for combine_fwd.)
 #pragma once
 
 namespace ring {
@@ -118,8 +121,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_ring(const __grid_
                                                                 const float* __restrict__ combine_w, int n, int k,
                                                                 int M, const __grid_constant__ RowFan out,
                                                                 long long ldo) {
-    pdl_entry();
-    constexpr int KT = 2, R = KT * NP, STAGE = R * kCols;
+        constexpr int KT = 2, R = KT * NP, STAGE = R * kCols;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     bf16* ring = reinterpret_cast<bf16*>(smem) + (size_t)warp * S * STAGE;
@@ -208,8 +210,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
                                                                  const bf16* __restrict__ wgT, int n, int k, int E,
                                                                  int M, const __grid_constant__ RowFan dx,
                                                                  long long ldx) {
-    pdl_entry();
-    constexpr int KT = 2, R = KT * NP, STAGE = R * kCols + 64;   // + 32 f32 of logit gradients (as bf16 units)
+        constexpr int KT = 2, R = KT * NP, STAGE = R * kCols + 64;   // + 32 f32 of logit gradients (as bf16 units)
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     bf16* ring = reinterpret_cast<bf16*>(smem) + (size_t)warp * S * STAGE;
@@ -302,121 +303,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
     }
 }
 
-// ---------------------------------------------------------------- dispatch (slot rows)
-// Slot row (e, slot_lo + sp) <- x[slot_src / k] (scaled), zero when unfilled;
-// rows past the segment's last 128-row GEMM tile are skipped.  PEER: stored
-// into the holders' receive buffers (NVLink) instead of out.
-template <bool PEER, int S>
-__global__ void __launch_bounds__(kRowThreads, 4) dispatch_rows_ring(
-    const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
-    int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
-    long long out_stride_s, const __grid_constant__ SlotView dstv, const int* __restrict__ fill) {
-    pdl_entry();
-    constexpr int STAGE = kCols;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    bf16* ring = reinterpret_cast<bf16*>(smem) + (size_t)warp * S * STAGE;
-    const uint32_t bar0 = saddr(smem + (size_t)kWarps * S * STAGE * 2) + warp * S * 8;
-    init_bars(bar0, S, lane);
-    const long long wg = (long long)blockIdx.x * kWarps + warp, nw = (long long)gridDim.x * kWarps;
-    const long long rows = (long long)E * slots_out;
-    const int nch = (M + kCols - 1) / kCols;
-    uint32_t phase_base = 0;
-    for (long long base = wg; base < rows; base += 32 * nw) {
-        const long long left = (rows - 1 - base) / nw + 1;
-        const int nrow = left < 32 ? (int)left : 32;
-        // this lane's row: source token (-1 zero row, -2 skipped), scale, destination offset
-        int src = -2, ep = 0;
-        long long doff = 0;
-        float w = 1.0f;
-        if (lane < nrow) {
-            const long long r = base + lane * nw;
-            const int e = (int)(r / slots_out);
-            const int sp = (int)(r - (long long)e * slots_out);
-            const int s = slot_lo + sp;
-            bool live = true;
-            if (fill != nullptr) {
-                int sf = __ldg(fill + e) - slot_lo;
-                sf = sf < 0 ? 0 : (sf > slots_out ? slots_out : sf);
-                live = sp < ((sf + 127) & ~127);
-            }
-            if (live) {
-                src = (s < cap) ? __ldg(slot_src + (long long)e * cap + s) : -1;
-                if (PEER)
-                    doff = slot_inbuf(dstv, e, sp, ep);
-                else
-                    doff = (long long)e * out_stride_e + (long long)sp * out_stride_s;
-                if (scale != nullptr && src >= 0) w = __ldg(scale + src);
-            }
-        }
-        const int items = nrow * nch;
-        auto issue = [&](int q) {
-            const int i = q / nch, c0 = (q - i * nch) * kCols;
-            const int cols = min(kCols, M - c0);
-            const uint32_t qs = phase_base + q, st = qs % S;
-            const int sr = __shfl_sync(0xffffffffu, src, i);
-            if (lane == 0) {
-                proxy_fence();
-                bar_expect(bar0 + 8 * st, sr >= 0 ? cols * 2 : 0);
-                if (sr >= 0)
-                    bulk_g2s(saddr(ring + st * STAGE), x + (long long)(sr / k) * ldx + c0, cols * 2, bar0 + 8 * st);
-            }
-        };
-        const int pre = items < S - 1 ? items : S - 1;
-        for (int q = 0; q < pre; ++q) issue(q);
-        for (int q = 0; q < items; ++q) {
-            if (q + S - 1 < items) issue(q + S - 1);
-            const int i = q / nch, c0 = (q - i * nch) * kCols;
-            const int cols = min(kCols, M - c0);
-            const uint32_t qs = phase_base + q, st = qs % S;
-            const int sr = __shfl_sync(0xffffffffu, src, i);
-            const float wr = __shfl_sync(0xffffffffu, w, i);
-            const int er = __shfl_sync(0xffffffffu, ep, i);
-            const long long dr = shfl_ll(doff, i);
-            bar_wait(bar0 + 8 * st, (qs / S) & 1);
-            if (sr != -2) {
-                const bf16* sb = ring + st * STAGE;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = lane * 8 + h * 256;
-                    if (c >= cols) continue;
-                    int4 o = make_int4(0, 0, 0, 0);
-                    if (sr >= 0) {
-                        o = lds16(sb + c);
-                        if (scale != nullptr) {
-                            Vec8 t8;
-                            *reinterpret_cast<int4*>(&t8) = o;
-                            float f[8];
-                            vec8_to_f32(t8, f);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) f[u] *= wr;
-                            const Vec8 r8 = f32_to_vec8(f);
-                            o = *reinterpret_cast<const int4*>(&r8);
-                        }
-                    }
-                    if (PEER) {
-                        for (int pp = 0; pp < dstv.n_p; ++pp)
-                            *reinterpret_cast<int4*>(const_cast<bf16*>(slot_base(dstv, er, pp)) + dr + c0 + c) = o;
-                    } else {
-                        *reinterpret_cast<int4*>(out + dr + c0 + c) = o;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        phase_base += items;
-    }
-}
-
 // ---------------------------------------------------------------- host side
-inline bool enabled() {
-    static const int on = [] {
-        const char* e = getenv("PARM_RING");
-        return (e == nullptr || e[0] != '0') ? 1 : 0;
-    }();
-    return on != 0;
-}
-
 inline bool view_aligned(const SlotView& v) {
     if (v.n_peer != 0) return false;   // bulk copies read local HBM only
     return v.stride_ep % 8 == 0 && v.stride_i % 8 == 0 && v.stride_p % 8 == 0 && v.stride_shi % 8 == 0 &&

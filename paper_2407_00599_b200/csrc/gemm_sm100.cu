@@ -14,13 +14,15 @@
 //   WGT   D[g][m][n] = sum_{s,r} A[s][g][r][m] * B[s][g][r][n] -- dW1^T = dH^T R,
 //         dW2^T = dY^T H (both operands MN-major over the segmented K)
 //
-// Structure (one CTA per SM, persistent over 128 x BN tiles):
-//   warp 0      TMA producer (one lane), STAGES-deep smem ring, 128B swizzle
-//   warp 1      MMA issuer  (one lane), tcgen05.mma.cta_group::1.kind::f16,
-//               M=128 N=BN K=16, fp32 accumulators in TMEM (2 x BN columns,
-//               double-buffered so the epilogue of tile i overlaps MMA of i+1)
+// Structure (CTA pairs on a TPC, cta_group::2, persistent over 256 x BN pair tiles):
+//   warp 0      TMA producer (one lane per CTA), STAGES-deep smem ring, 128B swizzle;
+//               each CTA stages its 128 A rows and half of the B tile
+//   warp 1      MMA issuer (leader CTA, one lane): tcgen05.mma.cta_group::2.kind::f16,
+//               M=256 N=BN K=16, fp32 accumulators in TMEM (2 x BN columns,
+//               double-buffered so the epilogue of tile i overlaps the MMA of i+1)
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused op -> swizzled
+//               staging -> TMA bulk-tensor store (or reduce-add)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdlib>
@@ -54,7 +56,6 @@ __device__ __forceinline__ uint32_t bf16_pos_bits(uint32_t packed) {   // bit0: 
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 256;
-constexpr int kSmemBudget = 196 * 1024;
 
 struct Params {
     int G, nhi, nlo, L;        // row space: segments (hi, lo), rows per segment
@@ -66,12 +67,9 @@ struct Params {
     const bf16* aux;
     long long x_ld, x_g, x_lo, x_hi;
     const int* fill;           // [hi][lo][g] valid rows, or null
-    int pairs;                 // CTA-pair kernel: max 256-row pair tiles per group
-    int debug;                 // PARM_GEMM_DEBUG bits (perf experiments only): 1 = no epilogue stores, 2 = no TMA,
-                               // 4 = no MMA (pair kernel), 8 = per-thread stores instead of TMA stores
-    int seg_peer;              // ROW: rows of segment (hi, lo) stored into seg_dst[hi * nlo + lo] (peer buffers)
-    bf16* seg_dst[kMaxPeers];  //   + g * sd_g + r * sd_ld + n -- the return AlltoAll fused into the epilogue
-    long long sd_g, sd_ld;
+    int pairs;                 // max 256-row pair tiles per group
+    int seg_peer;              // ROW: rows of segment (hi, lo) stored through SegMaps.m[hi * nlo + lo] (the
+                               //   owners' receive blocks, peer memory) -- the return AlltoAll fused into the epilogue
 };
 
 // Per-segment 3-D store maps (N, rows, G) over peer destinations: the TMA-store
@@ -189,46 +187,12 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-// ---------------------------------------------------------------- tile bookkeeping
-struct Tile {
-    int g, hi, lo, m0, n0;
-};
-
-__device__ __forceinline__ Tile decode_tile(const Params& p, int tile, int kind, int bn) {
-    Tile t;
-    if (kind == kRow) {
-        const int per_seg = p.m_tiles * p.n_blocks;
-        const int per_g = p.nhi * p.nlo * per_seg;
-        t.g = tile / per_g;
-        int rem = tile - t.g * per_g;
-        const int seg = rem / per_seg;
-        rem -= seg * per_seg;
-        t.hi = seg / p.nlo;
-        t.lo = seg - t.hi * p.nlo;
-        t.m0 = (rem / p.n_blocks) * BM;
-        t.n0 = (rem % p.n_blocks) * bn;
-    } else {
-        const int per_g = p.m_tiles * p.n_blocks;
-        t.g = tile / per_g;
-        const int rem = tile - t.g * per_g;
-        t.hi = t.lo = 0;
-        t.m0 = (rem / p.n_blocks) * BM;
-        t.n0 = (rem % p.n_blocks) * bn;
-    }
-    return t;
-}
-
 // Fill counts are staged into shared memory once per CTA (kMaxFill entries): the
 // single-thread producer/MMA loops must not pay a global-load latency per K block.
 constexpr int kMaxFill = 2048;
 
 __device__ __forceinline__ int seg_fill(const Params& p, const int* sfill, int g, int hi, int lo) {
     return p.fill ? sfill[(hi * p.nlo + lo) * p.G + g] : p.L;
-}
-
-// ROW tiles beyond the segment's fill carry no work.
-__device__ __forceinline__ bool row_tile_live(const Params& p, const int* sfill, const Tile& t) {
-    return t.m0 < seg_fill(p, sfill, t.g, t.hi, t.lo);
 }
 
 // The live K blocks of one tile, in order: ROW walks k0 = 0, BK, ... K; WGT walks each
@@ -244,294 +208,6 @@ __device__ __forceinline__ void for_each_kblock(const Params& p, const int* sfil
                 const int f = min(seg_fill(p, sfill, g, hi, lo), p.L);
                 for (int r0 = 0; r0 < f; r0 += BK) body(hi, lo, r0);
             }
-    }
-}
-
-// Epilogue of one accumulator tile for the calling thread's row: 32-column
-// chunks tcgen05.ld 32x32b -> registers -> fused op -> 16-byte global stores.
-// The ReLU-mask source (aux) of chunk c+1 is fetched while chunk c is
-// processed, so its global-load latency is exposed once per tile, not per chunk.
-template <int BN, int EPI>
-__device__ __forceinline__ void drain_tile(const Params& p, uint32_t taddr, long long drow, long long xrow,
-                                           bool row_ok, int n0, bool empty, void* dbase) {
-    constexpr int NC = BN / 32;
-    uint32_t* mrow = reinterpret_cast<uint32_t*>(const_cast<bf16*>(p.aux)) + xrow + n0 / 32;   // mask epilogues
-    int4 ax_next[4];
-    if (EPI == kEpiDReluBF16 && row_ok) {
-        const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) ax_next[v] = __ldg(src + v);
-    }
-#pragma unroll 1
-    for (int c = 0; c < NC; ++c) {
-        int4 ax_cur[4];
-        if (EPI == kEpiDReluBF16) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) ax_cur[v] = ax_next[v];
-            if (row_ok && c + 1 < NC) {
-                const int4* src = reinterpret_cast<const int4*>(p.aux + xrow + n0 + (c + 1) * 32);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) ax_next[v] = __ldg(src + v);
-            }
-        }
-        uint32_t r[32];
-        PARM_TMEM_LD32(taddr + c * 32, r);
-        tmem_ld_wait();
-        if (empty) {
-#pragma unroll
-            for (int v = 0; v < 32; ++v) r[v] = 0u;
-        }
-        if (!row_ok || (p.debug & 1)) continue;
-        const int col = n0 + c * 32;
-        if (EPI == kEpiF32 || EPI == kEpiF32Acc) {
-            float* dst = reinterpret_cast<float*>(dbase) + drow + col;
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                float4 o = make_float4(p.alpha * __uint_as_float(r[4 * v]), p.alpha * __uint_as_float(r[4 * v + 1]),
-                                       p.alpha * __uint_as_float(r[4 * v + 2]),
-                                       p.alpha * __uint_as_float(r[4 * v + 3]));
-                if (EPI == kEpiF32Acc) {
-                    float4 prev = reinterpret_cast<float4*>(dst)[v];
-                    o.x += prev.x;
-                    o.y += prev.y;
-                    o.z += prev.z;
-                    o.w += prev.w;
-                }
-                reinterpret_cast<float4*>(dst)[v] = o;
-            }
-        } else {
-            bf16* dst = reinterpret_cast<bf16*>(dbase) + drow + col;
-            float f[32];
-#pragma unroll
-            for (int v = 0; v < 32; ++v) f[v] = p.alpha * __uint_as_float(r[v]);
-            if (EPI == kEpiReluBF16) {
-#pragma unroll
-                for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
-            }
-            if (EPI == kEpiDReluBF16) {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    Vec8 a8;
-                    *reinterpret_cast<int4*>(&a8) = ax_cur[v];
-                    float a[8];
-                    vec8_to_f32(a8, a);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) f[8 * v + u] = a[u] > 0.0f ? f[8 * v + u] : 0.0f;
-                }
-            }
-            if (EPI == kEpiDMaskBF16) {
-                const uint32_t m = __ldg(mrow + c);
-#pragma unroll
-                for (int v = 0; v < 32; ++v) f[v] = ((m >> v) & 1u) ? f[v] : 0.0f;
-            }
-            if (EPI == kEpiReluMaskBF16) {
-#pragma unroll
-                for (int v = 0; v < 32; ++v) f[v] = fmaxf(f[v], 0.0f);
-            }
-            uint32_t bits = 0;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const Vec8 o8 = f32_to_vec8(f + 8 * v);
-                st_vec8(dst + 8 * v, o8);
-                if (EPI == kEpiReluMaskBF16) {
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(&o8);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) bits |= bf16_pos_bits(w[u]) << (8 * v + 2 * u);
-                }
-            }
-            if (EPI == kEpiReluMaskBF16) mrow[c] = bits;
-        }
-    }
-}
-
-// ---------------------------------------------------------------- the kernel
-template <int BN, int KIND, int MB, int EPI>
-struct Cfg {
-    static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
-    static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (kSmemBudget - 1024) / kStageBytes > 8 ? 8 : (kSmemBudget - 1024) / kStageBytes;
-    static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/ +
-                                      kMaxFill * 4;
-};
-
-template <int BN, int KIND, int MB, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
-    moe_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const Params p) {
-    pdl_entry();
-    using C = Cfg<BN, KIND, MB, EPI>;
-    constexpr int STAGES = C::kStages;
-    constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
-    constexpr int MBX = (KIND == kRow) ? MB : kMNMajor;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* smem_a = smem;
-    uint8_t* smem_b = smem + STAGES * C::kABytes;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
-    uint64_t* empty_bar = full_bar + STAGES;
-    uint64_t* tfull_bar = empty_bar + STAGES;
-    uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-    int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + 256);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    if (p.fill)
-        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
-
-    if (warp == 0 && lane == 0) {
-        prefetch_tmap(&tmap_a);
-        prefetch_tmap(&tmap_b);
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&tfull_bar[s], 1);
-            mbar_init(&tempty_bar[s], 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"((uint32_t)C::kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ------------------------------------------------ TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const Tile t = decode_tile(p, tile, KIND, BN);
-                if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
-                for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
-                    mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                    uint8_t* sa = smem_a + stage * C::kABytes;
-                    uint8_t* sb = smem_b + stage * C::kBBytes;
-                    if (KIND == kRow) {
-                        const int k0 = r0;
-                        tma_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
-                        if (MB == kKMajor) {
-                            tma_load_3d(&tmap_b, &full_bar[stage], sb, k0, t.n0, t.g);
-                        } else {
-#pragma unroll
-                            for (int a = 0; a < BN / 64; ++a)
-                                tma_load_3d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), t.n0 + a * 64, k0, t.g);
-                        }
-                    } else {
-#pragma unroll
-                        for (int a = 0; a < BM / 64; ++a)
-                            tma_load_5d(&tmap_a, &full_bar[stage], sa + a * (BK * 128), t.m0 + a * 64, r0, t.g, lo,
-                                        hi);
-#pragma unroll
-                        for (int a = 0; a < BN / 64; ++a)
-                            tma_load_5d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), t.n0 + a * 64, r0, t.g, lo,
-                                        hi);
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                });
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
-            constexpr uint32_t idesc = instr_desc<BN, MA, MBX>();
-            // K-major: 8-row core groups 1024 B apart, K advance of 16 elems = 32 B.
-            // MN-major: 64-element MN atoms BK*128 B apart, K advance of 16 rows = 2048 B.
-            constexpr uint32_t a_lbo = (MA == kKMajor) ? 0 : BK * 128;
-            constexpr uint32_t b_lbo = (MBX == kKMajor) ? 0 : BK * 128;
-            constexpr uint32_t a_kstep = (MA == kKMajor) ? 32 : 16 * 128;
-            constexpr uint32_t b_kstep = (MBX == kKMajor) ? 32 : 16 * 128;
-            int stage = 0;
-            uint32_t phase = 0;
-            int it_tile = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const Tile t = decode_tile(p, tile, KIND, BN);
-                if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
-                const int as = it_tile & 1;
-                const uint32_t aphase = (it_tile >> 1) & 1;
-                ++it_tile;
-                mbar_wait(&tempty_bar[as], aphase ^ 1);
-                tc_fence_after();
-                const uint32_t tmem_d = tmem_base + as * BN;
-                bool first = true;
-                for_each_kblock<KIND>(p, sfill, t.g, [&](int, int, int) {
-                    mbar_wait(&full_bar[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
-                    const uint32_t sb = smem_u32(smem_b + stage * C::kBBytes);
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
-                        uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
-                        tc_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
-                    }
-                    first = false;
-                    tc_commit(&empty_bar[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                });
-                tc_commit(&tfull_bar[as]);   // also fires for an all-skipped WGT tile (epilogue writes zeros)
-            }
-        }
-    } else if (warp >= 4) {
-        // ---------------------------------------------------- epilogue
-        const int ew = warp & 3;  // TMEM lane quarter this warp may access
-        int it_tile = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            const Tile t = decode_tile(p, tile, KIND, BN);
-            if (KIND == kRow && !row_tile_live(p, sfill, t)) continue;
-            const int as = it_tile & 1;
-            const uint32_t aphase = (it_tile >> 1) & 1;
-            ++it_tile;
-            bool empty = false;
-            if (KIND == kWgt && p.fill) {
-                empty = true;
-                for (int seg = 0; seg < p.nhi * p.nlo && empty; ++seg)
-                    empty = seg_fill(p, sfill, t.g, seg / p.nlo, seg % p.nlo) <= 0;
-            }
-            mbar_wait(&tfull_bar[as], aphase);
-            tc_fence_after();
-            const int row = t.m0 + ew * 32 + lane;
-            const bool row_ok = (KIND == kWgt) || row < p.L;
-            long long drow, xrow = 0;
-            if (KIND == kRow) {
-                drow = (long long)t.g * p.d_g + (long long)t.lo * p.d_lo + (long long)t.hi * p.d_hi +
-                       (long long)row * p.d_ld;
-                xrow = (long long)t.g * p.x_g + (long long)t.lo * p.x_lo + (long long)t.hi * p.x_hi +
-                       (long long)row * p.x_ld;
-            } else {
-                drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
-            }
-            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
-            drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty, p.D);
-            tc_fence_before();
-            mbar_arrive(&tempty_bar[as]);
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"((uint32_t)C::kTmemCols)
-                     : "memory");
     }
 }
 
@@ -894,7 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     // everything above is independent of the previous kernel (PDL prologue); fill counts and operands are not
-    pdl_entry();
     if (p.fill)
         for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
     // ROW: work list = live 256-row pair tiles only (groups' live row pairs, prefix-summed), so the
@@ -934,18 +609,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (!t.live) continue;
                 for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
-                    const bool no_tma = (p.debug & 2) != 0;
                     if (leader)
-                        mbar_expect_tx(&full_bar[stage], no_tma ? 0u : 2u * C::kStageBytes);
+                        mbar_expect_tx(&full_bar[stage], 2u * C::kStageBytes);
                     else
                         mbar_arrive_remote(&full_bar[stage], 0);
-                    if (no_tma) {
-                        if (++stage == STAGES) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                        return;
-                    }
                     uint8_t* sa = smem_a + stage * C::kABytes;
                     uint8_t* sb = smem_b + stage * C::kBBytes;
                     const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
@@ -1006,7 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < BK / 16; ++k) {
                         uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
                         uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
-                        if (!(p.debug & 4)) tc2_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+                        tc2_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
                     }
                     first = false;
                     tc2_commit_both(&empty_bar[stage]);
@@ -1051,14 +718,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
             (void)drow;
-            if (KIND == kRow && p.seg_peer == 2) {   // TMA stores straight into the owner's receive block
+            if (KIND == kRow && p.seg_peer) {   // TMA stores straight into the owner's receive block
                 drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
                                               xrow, empty, my_stage, ebuf, &segmaps.m[t.hi * p.nlo + t.lo]);
-            } else if (KIND == kRow && p.seg_peer) {   // per-thread stores into the owner's receive block
-                const long long prow = (long long)t.g * p.sd_g + (long long)row * p.sd_ld;
-                drain_tile<BN, EPI>(p, taddr, prow, xrow, row_ok, t.n0, empty, p.seg_dst[t.hi * p.nlo + t.lo]);
-            } else if (p.debug & 9) {   // 8: per-thread global stores instead of the TMA-store staging
-                drain_tile<BN, EPI>(p, taddr, drow, xrow, row_ok, t.n0, empty, p.D);
             } else {
                 drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
                                               xrow, empty, my_stage, ebuf);
@@ -1124,22 +786,6 @@ static int make_tmap(CUtensorMap* map, const void* base, int rank, const long lo
     return 0;
 }
 
-template <int BN, int KIND, int MB, int EPI>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t stream) {
-    using C = Cfg<BN, KIND, MB, EPI>;
-    auto kern = moe_gemm_kernel<BN, KIND, MB, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        attr_set = true;
-    }
-    int grid = p.num_tiles < kNumSMs ? p.num_tiles : kNumSMs;
-    if (grid < 1) grid = 1;
-    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, ta, tb, p);
-    PARM_CHECK_LAUNCH("moe_gemm");
-    return 0;
-}
-
 static SegMaps g_segmaps;   // per-call store maps of moe_gemm_peer (host calls are stream-ordered, one thread)
 
 template <int BN, int KIND, int MB, int EPI>
@@ -1160,25 +806,10 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
 }
 
 template <int KIND, int MB, int EPI>
-static int dispatch_bn(bool pair, int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
-                       const Params& p, cudaStream_t s) {
-    if (pair) {
-        if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, td, p, s);
-        return launch_pair<128, KIND, MB, EPI>(ta, tb, td, p, s);
-    }
-    if (bn == 256) return launch<256, KIND, MB, EPI>(ta, tb, p, s);
-    if (bn == 128) return launch<128, KIND, MB, EPI>(ta, tb, p, s);
-    return launch<64, KIND, MB, EPI>(ta, tb, p, s);
-}
-
-// CTA pairs (cta_group::2) by default; PARM_GEMM_SINGLE_CTA=1 selects the 1-CTA kernel (A/B comparisons).
-static bool pair_mode() {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("PARM_GEMM_SINGLE_CTA");
-        mode = (e && e[0] == '1') ? 0 : 1;
-    }
-    return mode == 1;
+static int dispatch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const Params& p,
+                       cudaStream_t s) {
+    if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, td, p, s);
+    return launch_pair<128, KIND, MB, EPI>(ta, tb, td, p, s);
 }
 
 }  // namespace gemm
@@ -1192,7 +823,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     using namespace gemm;
     PARM_CHECK_ARG(q.kind == kRow || q.kind == kWgt, "gemm: bad kind %d", q.kind);
     PARM_CHECK_ARG(q.groups > 0 && q.nhi > 0 && q.nlo > 0 && q.seg_len > 0, "gemm: empty row space");
-    PARM_CHECK_ARG(q.N > 0 && q.N % 64 == 0, "gemm: N=%d must be a positive multiple of 64", q.N);
+    PARM_CHECK_ARG(q.N > 0 && q.N % 128 == 0, "gemm: N=%d must be a positive multiple of 128", q.N);
     PARM_CHECK_ARG(q.epi >= 0 && q.epi <= 6, "gemm: bad epilogue %d", q.epi);
     PARM_CHECK_ARG((q.epi != kEpiDReluBF16 && q.epi != kEpiReluMaskBF16 && q.epi != kEpiDMaskBF16) ||
                        q.aux.ptr != nullptr, "gemm: relu-mask epilogue needs aux");
@@ -1210,38 +841,19 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     p.K = q.K;
     p.alpha = q.alpha;
     p.fill = q.fill;
-    {
-        static int dbg = -1;
-        if (dbg < 0) {
-            const char* e = getenv("PARM_GEMM_DEBUG");
-            dbg = e ? atoi(e) : 0;
-        }
-        p.debug = dbg;
-    }
     p.seg_peer = 0;
-    p.sd_g = p.sd_ld = 0;
-    for (int i = 0; i < kMaxPeers; ++i) p.seg_dst[i] = nullptr;
     if (seg_dst != nullptr) {
         PARM_CHECK_ARG(q.kind == kRow && (q.epi == kEpiBF16 || q.epi == kEpiReluBF16),
                        "gemm: peer segment outputs need a ROW GEMM with a bf16 epilogue");
         PARM_CHECK_ARG(seg_dst->n == q.nhi * q.nlo, "gemm: %d peer outputs for %d segments", seg_dst->n,
                        q.nhi * q.nlo);
-        PARM_CHECK_ARG(pair_mode(), "gemm: peer segment outputs need the CTA-pair kernel");
         PARM_CHECK_ARG(sd_ld % 8 == 0 && sd_g % 8 == 0, "gemm: peer output rows must be 16-byte aligned");
-        static int mode = -1;     // PARM_GEMM_PEER_STORES=thread: per-thread stores instead of TMA stores
-        if (mode < 0) {
-            const char* e = getenv("PARM_GEMM_PEER_STORES");
-            mode = (e && e[0] == 't') ? 1 : 2;
-        }
-        p.seg_peer = mode;
+        p.seg_peer = 1;
         for (int i = 0; i < seg_dst->n; ++i) {
-            p.seg_dst[i] = seg_dst->ptr[i];
             const long long dd[3] = {q.N, q.seg_len, q.groups};
             const long long ds[2] = {sd_ld, sd_g};
             if (int rc = make_tmap(&g_segmaps.m[i], seg_dst->ptr[i], 3, dd, ds, 32, 2, 64)) return rc;
         }
-        p.sd_g = sd_g;
-        p.sd_ld = sd_ld;
     }
     p.D = const_cast<void*>(q.d.ptr);
     p.d_ld = q.d.ld;
@@ -1253,8 +865,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     p.x_g = q.aux.g_stride;
     p.x_lo = q.aux.lo_stride;
     p.x_hi = q.aux.hi_stride;
-    const int bn = (q.N % 256 == 0) ? 256 : (q.N % 128 == 0 ? 128 : 64);
-    const bool pair = pair_mode() && bn >= 128;
+    const int bn = (q.N % 256 == 0) ? 256 : 128;
     p.n_blocks = q.N / bn;
     CUtensorMap ta, tb, td;
     int rc;
@@ -1273,7 +884,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
                        "gemm: row GEMMs produce bf16");
         p.m_tiles = (q.seg_len + BM - 1) / BM;
         p.pairs = (p.nhi * p.nlo * p.m_tiles + 1) / 2;
-        p.num_tiles = pair ? p.G * p.pairs * p.n_blocks : p.G * p.nhi * p.nlo * p.m_tiles * p.n_blocks;
+        p.num_tiles = p.G * p.pairs * p.n_blocks;
         p.k_iters = q.K / BK;
         // A: [hi][lo][g][r][k] -> dims (K, L, G, nlo, nhi)
         const long long ad[5] = {q.K, q.seg_len, q.groups, q.nlo, q.nhi};
@@ -1282,7 +893,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
         if (q.b_major == kKMajor) {   // B[g][n][k]
             const long long bd[3] = {q.K, q.N, q.groups};
             const long long bs[2] = {q.b.ld, q.b.g_stride};
-            rc = make_tmap(&tb, q.b.ptr, 3, bd, bs, pair ? bn / 2 : bn);
+            rc = make_tmap(&tb, q.b.ptr, 3, bd, bs, bn / 2);   // each CTA of the pair stages half of B
         } else {                      // B[g][k][n]
             const long long bd[3] = {q.N, q.K, q.groups};
             const long long bs[2] = {q.b.ld, q.b.g_stride};
@@ -1291,21 +902,21 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
         if (rc) return rc;
         const int combo = q.b_major;
         if (combo == kKMajor) {
-            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(bn, ta, tb, td, p, stream);
             if (q.epi == kEpiReluMaskBF16)
-                return dispatch_bn<kRow, kKMajor, kEpiReluMaskBF16>(pair, bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
+                return dispatch_bn<kRow, kKMajor, kEpiReluMaskBF16>(bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(bn, ta, tb, td, p, stream);
         } else {
-            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(pair, bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiDMaskBF16) return dispatch_bn<kRow, kMNMajor, kEpiDMaskBF16>(pair, bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(pair, bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiDMaskBF16) return dispatch_bn<kRow, kMNMajor, kEpiDMaskBF16>(bn, ta, tb, td, p, stream);
+            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(bn, ta, tb, td, p, stream);
         }
     } else {
         PARM_CHECK_ARG(q.M > 0 && q.M % BM == 0, "gemm: M=%d must be a positive multiple of %d", q.M, BM);
         PARM_CHECK_ARG(q.epi == kEpiF32 || q.epi == kEpiF32Acc, "gemm: weight GEMMs produce f32");
         p.m_tiles = q.M / BM;
         p.pairs = (p.m_tiles + 1) / 2;
-        p.num_tiles = pair ? p.G * p.pairs * p.n_blocks : p.G * p.m_tiles * p.n_blocks;
+        p.num_tiles = p.G * p.pairs * p.n_blocks;
         p.k_iters = p.nhi * p.nlo * ((q.seg_len + BK - 1) / BK);
         const long long ad[5] = {q.M, q.seg_len, q.groups, q.nlo, q.nhi};
         const long long as[4] = {q.a.ld, q.a.g_stride, q.a.lo_stride, q.a.hi_stride};
@@ -1313,8 +924,8 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
         const long long bd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
         const long long bs[4] = {q.b.ld, q.b.g_stride, q.b.lo_stride, q.b.hi_stride};
         if ((rc = make_tmap(&tb, q.b.ptr, 5, bd, bs, BK))) return rc;
-        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(pair, bn, ta, tb, td, p, stream);
-        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(pair, bn, ta, tb, td, p, stream);
+        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(bn, ta, tb, td, p, stream);
+        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(bn, ta, tb, td, p, stream);
     }
     set_error("gemm: unsupported combination kind=%d b_major=%d epi=%d", q.kind, q.b_major, q.epi);
     return 1;

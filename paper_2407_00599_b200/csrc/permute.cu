@@ -19,7 +19,8 @@
 // (KT picks x 4 chunks in flight per lane) — the memory-level parallelism
 // these kernels live on.  Accumulation is f32.  dispatch, combine_fwd and
 // dispatch_bwd run as bulk-copy rings (gather_ring.cuh) whenever their views
-// are local and 16-byte aligned (PARM_RING=0: the register kernels below).
+// are local and 16-byte aligned; peer views use the register kernels below.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -47,96 +48,6 @@ static int row_grid(long long rows) {
 }
 
 __device__ __forceinline__ int4 ldg16(const bf16* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
-
-// ------------------------------------------------------------------ dispatch (gather into slots)
-// Four rows per warp iteration: their slot_src entries, then their token rows,
-// are loaded together.  PEER: each row is stored straight into the receive
-// buffers of its N_ESP holders on other GPUs (NVLink stores through the
-// symmetric-memory mapping) -- the EP&ESP dispatch AlltoAll with its dump,
-// fused into the gather (collectives.py:256-283).
-template <bool PEER>
-__global__ void __launch_bounds__(kRowThreads) dispatch_rows_kernel(
-    const bf16* __restrict__ x, long long ldx, const int* __restrict__ slot_src, const float* __restrict__ scale,
-    int k, int E, int cap, int slot_lo, int slots_out, int M, bf16* __restrict__ out, long long out_stride_e,
-    long long out_stride_s, const __grid_constant__ SlotView dstv, const int* __restrict__ fill) {
-    pdl_entry();
-    constexpr int R = 4;
-    const int lane = threadIdx.x & 31;
-    const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
-    const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
-    const long long rows = (long long)E * slots_out;
-    for (long long r0 = warp_global * R; r0 < rows; r0 += num_warps * R) {
-        int src[R];
-        bf16* dst[R];
-        int dep[R];
-        long long doff[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const long long r = r0 + q;
-            src[q] = -2;
-            if (r < rows) {
-                const int e = (int)(r / slots_out);
-                const int sp = (int)(r - (long long)e * slots_out);
-                const int s = slot_lo + sp;
-                if (fill != nullptr) {   // rows past the segment's last 128-row GEMM tile are never read
-                    int sf = __ldg(fill + e) - slot_lo;
-                    sf = sf < 0 ? 0 : (sf > slots_out ? slots_out : sf);
-                    if (sp >= ((sf + 127) & ~127)) continue;
-                }
-                src[q] = (s < cap) ? __ldg(slot_src + (long long)e * cap + s) : -1;
-                if (PEER) {
-                    int ep;
-                    const long long off = slot_inbuf(dstv, e, sp, ep);
-                    dst[q] = const_cast<bf16*>(slot_base(dstv, ep, 0)) + off;
-                    dep[q] = ep;
-                    doff[q] = off;
-                } else {
-                    dst[q] = out + (long long)e * out_stride_e + (long long)sp * out_stride_s;
-                }
-            }
-        }
-        float w[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) w[q] = (scale != nullptr && src[q] >= 0) ? __ldg(scale + src[q]) : 1.0f;
-        for (int g0 = 0; g0 < M; g0 += kGroupCols) {
-            int4 v[R][kChunks];
-#pragma unroll
-            for (int q = 0; q < R; ++q)
-#pragma unroll
-                for (int i = 0; i < kChunks; ++i) {
-                    const int c = g0 + lane * 8 + i * 256;
-                    v[q][i] = make_int4(0, 0, 0, 0);
-                    if (src[q] >= 0 && c < M) v[q][i] = ldg16(x + (long long)(src[q] / k) * ldx + c);
-                }
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                if (src[q] == -2) continue;
-#pragma unroll
-                for (int i = 0; i < kChunks; ++i) {
-                    const int c = g0 + lane * 8 + i * 256;
-                    if (c >= M) continue;
-                    int4 o = v[q][i];
-                    if (scale != nullptr && src[q] >= 0) {
-                        Vec8 t;
-                        *reinterpret_cast<int4*>(&t) = v[q][i];
-                        float f[8];
-                        vec8_to_f32(t, f);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) f[u] *= w[q];
-                        const Vec8 r8 = f32_to_vec8(f);
-                        o = *reinterpret_cast<const int4*>(&r8);
-                    }
-                    if (PEER) {
-                        for (int pp = 0; pp < dstv.n_p; ++pp)
-                            *reinterpret_cast<int4*>(const_cast<bf16*>(slot_base(dstv, dep[q], pp)) + doff[q] + c) = o;
-                    } else {
-                        *reinterpret_cast<int4*>(dst[q] + c) = o;
-                    }
-                }
-            }
-        }
-    }
-}
 
 // ------------------------------------------------------------------ token-side gathers
 // Routing of one token's picks (lane-uniform).
@@ -197,7 +108,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_fwd_kernel(const __gri
                                                                       const float* __restrict__ combine_w, int n, int k,
                                                                       int M, const __grid_constant__ RowFan out,
                                                                       long long ldo) {
-    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -264,7 +174,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
                                                                       int E, int M, float* __restrict__ dlogits,
                                                                       const __grid_constant__ DyScatter sc,
                                                                       const __grid_constant__ SlotView dstv) {
-    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -359,7 +268,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
 // are all in flight together, and each 16-byte Wg^T load (bf16, the gate
 // weights as stored) feeds all four tokens -- the gate term's weight traffic
 // is 1/TB of a token-per-warp loop's.
-template <int KT, int TB, int EMAX>   // EMAX > 0: E <= EMAX, logit gradients kept in registers
+template <int KT, int TB>
 __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __grid_constant__ SlotView dr,
                                                                        const int* __restrict__ expert_idx,
                                                                        const int* __restrict__ slot_idx,
@@ -368,7 +277,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
                                                                        int E, int M,
                                                                        const __grid_constant__ RowFan dx,
                                                                        long long ldx) {
-    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -384,14 +292,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
                 epk[b][j] = 0;
                 off[b][j] = sl >= 0 ? slot_inbuf(dr, __ldg(expert_idx + t * k + j), sl, epk[b][j]) : -1;
             }
-        float dl[TB][EMAX > 0 ? EMAX : 1];   // gate-logit gradients, held across the column groups when E <= EMAX
-        if (EMAX > 0) {
-#pragma unroll
-            for (int b = 0; b < TB; ++b)
-#pragma unroll
-                for (int e = 0; e < (EMAX > 0 ? EMAX : 1); ++e)
-                    dl[b][e] = (dlogits != nullptr && t0 + b < n && e < E) ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
-        }
         for (int c0 = 0; c0 < M; c0 += 256) {
             const int c = c0 + lane * 8;
             if (c >= M) continue;
@@ -414,23 +314,13 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
                     for (int j = 0; j < KT; ++j) fma_bf16x8(acc[b], 1.0f, buf[b][j]);
             }
             if (dlogits != nullptr) {
-                if (EMAX > 0) {
-#pragma unroll
-                    for (int e = 0; e < (EMAX > 0 ? EMAX : 1); ++e) {
-                        if (e >= E) break;
-                        const int4 wv = ldg16(wgT + (long long)e * M + c);
-#pragma unroll
-                        for (int b = 0; b < TB; ++b) fma_bf16x8(acc[b], dl[b][e], wv);
-                    }
-                } else {
 #pragma unroll 2
-                    for (int e = 0; e < E; ++e) {
-                        const int4 wv = ldg16(wgT + (long long)e * M + c);
+                for (int e = 0; e < E; ++e) {
+                    const int4 wv = ldg16(wgT + (long long)e * M + c);
 #pragma unroll
-                        for (int b = 0; b < TB; ++b) {
-                            const float d = t0 + b < n ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
-                            fma_bf16x8(acc[b], d, wv);
-                        }
+                    for (int b = 0; b < TB; ++b) {
+                        const float d = t0 + b < n ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
+                        fma_bf16x8(acc[b], d, wv);
                     }
                 }
             }
@@ -447,7 +337,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
 __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const __grid_constant__ SlotView y, int E, int slots,
                                                                   int M,
                                                                   bf16* __restrict__ out) {
-    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -495,71 +384,299 @@ static int check_view(const SlotView& v, int M, const char* what) {
     return 0;
 }
 
-int dispatch_rows(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
-                  int slot_lo, int slots_out, int M, void* out, long long out_stride_e, long long out_stride_s,
-                  const int* fill, cudaStream_t s) {
-    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && out_stride_s % 8 == 0 && out_stride_e % 8 == 0,
-                   "dispatch_rows: rows must be 16-byte aligned (M=%d)", M);
-    const long long rows = (long long)E * slots_out;
-    if (rows == 0) return 0;
-    SlotView none{};
-    if (ring::enabled() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-        constexpr int S = 6;
-        static int per_sm = 0;
-        const int smem = ring::ring_smem(S, 1, 0);
-        auto kern = ring::dispatch_rows_ring<false, S>;
-        launch_k(kern, ring::grid_for(kern, smem, rows, per_sm), kRowThreads, smem, s, 
-            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
-            reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none, fill);
-        PARM_CHECK_LAUNCH("dispatch_rows");
-        return 0;
-    }
-    launch_k(dispatch_rows_kernel<false>, row_grid((rows + 3) / 4), kRowThreads, 0, s, 
-        reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M,
-        reinterpret_cast<bf16*>(out), out_stride_e, out_stride_s, none, fill);
-    PARM_CHECK_LAUNCH("dispatch_rows");
-    return 0;
+// ------------------------------------------------------------------ route + dispatch
+// The slot pass of the gate (dataplane.py:104-116: token-major fill, first come first
+// served per expert) fused with the dispatch it feeds (dataplane.py:101,112 and the
+// S2 slot split + pad, :373-378), as ONE persistent kernel over the gate's per-8-token
+// tile pick counts:
+//   1. each CTA owns a contiguous range of tiles; its per-expert base is the sum of the
+//      counts of all earlier tiles (exact prefix, read from L2), the totals give fill;
+//   2. slots of the CTA's tokens in token order (warp ballots per 32-token chunk,
+//      chunk bases by an exclusive scan in shared memory) -> slot_idx, slot_src;
+//   3. each kept pick whose slot falls in [slot_lo, slot_lo + slots_out) gets the token
+//      row: lane 0 of each warp streams x rows into a shared-memory ring with
+//      cp.async.bulk and stores each to its slot row(s) with bulk stores (local tensor,
+//      or the N_ESP holders' receive buffers over NVLink -- the EP&ESP dispatch AlltoAll
+//      with its dump, collectives.py:256-283); x is read once per token, not per pick;
+//   4. rows between each expert's fill and its last 128-row GEMM tile are zeroed, and
+//      the unfilled tail of slot_src is set to -1 (grid-strided over all CTAs).
+constexpr int kRdWarps = 8;
+constexpr int kRdCols = 1024;                 // row chunk per ring stage (2 KB of bf16)
+constexpr int kRdStages = 10;
+constexpr int kRdLag = 2;                     // a stage is refilled kRdLag items after its stores were issued
+
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
 }
 
-// Per-segment fill counts of this source's slot range, stored into every holder's table.
-__global__ void fan_fill_kernel(const int* __restrict__ fill, int E, int slot_lo, int slots_out,
-                                const __grid_constant__ SlotView dstv, const __grid_constant__ IntFan fan) {
-    pdl_entry();
-    const int e = threadIdx.x;
-    if (e >= E) return;
-    int c = __ldg(fill + e) - slot_lo;
-    c = c < 0 ? 0 : (c > slots_out ? slots_out : c);
-    const int ep = e / dstv.e_local, i = e - ep * dstv.e_local;
-    for (int p = 0; p < dstv.n_p; ++p) fan.ptr[ep * dstv.peer_ep + p * dstv.peer_p][i] = c;
+template <int EMAX>
+__global__ void __launch_bounds__(kRdWarps * 32) route_dispatch_kernel(
+    const bf16* __restrict__ x, long long ldx, const int* __restrict__ expert_idx, const int* __restrict__ counts,
+    int n, int k, int E, int cap, int M, int* __restrict__ slot_idx, int* __restrict__ slot_src,
+    int* __restrict__ fill, int slot_lo, int slots_out, bf16* __restrict__ out, long long out_stride_e,
+    long long out_stride_s, const __grid_constant__ SlotView dstv, const __grid_constant__ IntFan fan, int peer) {
+    __shared__ int s_base[32], s_tot[32];
+    __shared__ int s_red[kRdWarps][32];
+    __shared__ int s_chunk[64][32];                // per 32-token chunk counts -> exclusive chunk bases
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tiles = (n + 7) / 8;
+    const int tb = (int)((long long)tiles * blockIdx.x / gridDim.x);
+    const int te = (int)((long long)tiles * (blockIdx.x + 1) / gridDim.x);
+    // ---- 0. this CTA's token rows start streaming into a per-warp shared-memory ring now
+    //        (cp.async.bulk, lane 0 of each warp): the slot pass below overlaps their latency
+    const int t_begin = tb * 8, t_end = min(te * 8, n);
+    const int nch = (M + kRdCols - 1) / kRdCols;
+    const int ntok = t_end - t_begin;
+    const int my_tok = warp < ntok ? (ntok - 1 - warp) / kRdWarps + 1 : 0;
+    const int items = slots_out > 0 ? my_tok * nch : 0;   // slots_out == 0: slot pass only
+    unsigned char* ring = smem + (size_t)warp * kRdStages * kRdCols * 2;
+    const uint32_t bar0 = ring::saddr(smem + (size_t)kRdWarps * kRdStages * kRdCols * 2) + warp * kRdStages * 8;
+    auto tok_of = [&](int it) { return t_begin + warp + (it / nch) * kRdWarps; };
+    auto rd_load = [&](int it) {
+        const int t = tok_of(it), c0 = (it % nch) * kRdCols;
+        const int cols = min(kRdCols, M - c0);
+        const uint32_t st = (uint32_t)it % kRdStages;
+        ring::bar_expect(bar0 + 8 * st, cols * 2);
+        ring::bulk_g2s(ring::saddr(ring + st * kRdCols * 2), x + (long long)t * ldx + c0, cols * 2, bar0 + 8 * st);
+    };
+    if (lane == 0 && items > 0) {
+        for (int s = 0; s < kRdStages; ++s) ring::bar_init(bar0 + 8 * s);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int it = 0; it < min(items, kRdStages - kRdLag); ++it) rd_load(it);
+    }
+    // ---- 1. base (tiles < tb) and totals, per expert
+    {
+        int pre[EMAX], tot[EMAX];
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) pre[e] = tot[e] = 0;
+        constexpr int TU = 4;   // tiles per thread per batch, all loads issued before use
+        for (int i0 = 0; i0 < tiles; i0 += TU * blockDim.x) {
+            int cv[TU][EMAX];
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const int i = i0 + u * blockDim.x + threadIdx.x;
+#pragma unroll
+                for (int e = 0; e < EMAX; ++e) cv[u][e] = (e < E && i < tiles) ? __ldg(counts + (long long)i * E + e) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < TU; ++u) {
+                const int i = i0 + u * blockDim.x + threadIdx.x;
+#pragma unroll
+                for (int e = 0; e < EMAX; ++e) {
+                    tot[e] += cv[u][e];
+                    if (i < tb) pre[e] += cv[u][e];
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) break;
+            int a = pre[e], b = tot[e];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+            }
+            if (lane == e) {
+                s_red[warp][e] = a;
+            }
+            pre[e] = b;   // reuse: warp total of expert e
+        }
+        __syncthreads();
+        if (threadIdx.x < E) {
+            int a = 0;
+            for (int w = 0; w < kRdWarps; ++w) a += s_red[w][threadIdx.x];
+            s_base[threadIdx.x] = a;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) break;
+            if (lane == e) s_red[warp][e] = pre[e];
+        }
+        __syncthreads();
+        if (threadIdx.x < E) {
+            int b = 0;
+            for (int w = 0; w < kRdWarps; ++w) b += s_red[w][threadIdx.x];
+            s_tot[threadIdx.x] = b;
+            if (blockIdx.x == 0) fill[threadIdx.x] = b < cap ? b : cap;
+        }
+        __syncthreads();
+    }
+    // ---- 2. slots of this CTA's tokens, in token order
+    const int nchunk = (t_end - t_begin + 31) / 32;   // <= 64 (host caps tokens per CTA at 2048)
+    unsigned my_mask[2] = {0u, 0u};                    // picks per chunk of this warp (lane = token), by expert bit
+    for (int c = warp; c < nchunk; c += kRdWarps) {
+        const int t = t_begin + c * 32 + lane;
+        unsigned m = 0;
+        if (t < t_end)
+            for (int j = 0; j < k; ++j) m |= 1u << __ldg(expert_idx + (long long)t * k + j);
+        if (c / kRdWarps < 2) my_mask[c / kRdWarps] = m;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) break;
+            const int cnt = __popc(__ballot_sync(0xffffffffu, (m >> e) & 1u));
+            if (lane == 0) s_chunk[c][e] = cnt;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {                              // exclusive scan over chunks, from the CTA base
+        int a = s_base[threadIdx.x];
+        for (int c = 0; c < nchunk; ++c) {
+            const int v = s_chunk[c][threadIdx.x];
+            s_chunk[c][threadIdx.x] = a;
+            a += v;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int c = warp; c < nchunk; c += kRdWarps) {
+        const int t = t_begin + c * 32 + lane;
+        unsigned m = 0;
+        if (c / kRdWarps < 2) {
+            m = my_mask[c / kRdWarps];
+        } else if (t < t_end) {
+            for (int j = 0; j < k; ++j) m |= 1u << __ldg(expert_idx + (long long)t * k + j);
+        }
+        int pre_e[EMAX];
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) break;
+            pre_e[e] = __popc(__ballot_sync(0xffffffffu, (m >> e) & 1u) & lt);
+        }
+        if (t < t_end) {
+            for (int j = 0; j < k; ++j) {
+                const int e = __ldg(expert_idx + (long long)t * k + j);
+                int p = 0;
+#pragma unroll
+                for (int ee = 0; ee < EMAX; ++ee)
+                    if (ee == e) p = pre_e[ee];
+                const int slot = s_chunk[c][e] + p;
+                if (slot < cap) {
+                    slot_idx[(long long)t * k + j] = slot;
+                    slot_src[(long long)e * cap + slot] = t * k + j;
+                } else {
+                    slot_idx[(long long)t * k + j] = -1;
+                }
+            }
+        }
+    }
+    __syncthreads();   // slot_idx of the CTA's tokens visible to every warp (global memory, same CTA)
+    // ---- 3. token rows -> slot rows: wait for the rows streamed in since step 0, store each
+    //        to its kept picks' slot rows (bulk stores), refill the ring
+    if (lane == 0 && items > 0) {
+        for (int it = 0; it < items; ++it) {
+            if (it + kRdStages - kRdLag < items) {
+                // the stage being refilled held item it - kRdLag: its stores must have read it
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kRdLag - 1) : "memory");
+                rd_load(it + kRdStages - kRdLag);
+            }
+            const int t = tok_of(it), ch = it % nch, c0 = ch * kRdCols;
+            const int cols = min(kRdCols, M - c0);
+            const uint32_t st = (uint32_t)it % kRdStages;
+            ring::bar_wait(bar0 + 8 * st, ((uint32_t)it / kRdStages) & 1);
+            const uint32_t src = ring::saddr(ring + st * kRdCols * 2);
+            for (int j = 0; j < k; ++j) {
+                const int sl = slot_idx[(long long)t * k + j];
+                if (sl < slot_lo || sl >= slot_lo + slots_out) continue;
+                const int e = __ldg(expert_idx + (long long)t * k + j);
+                const int sp = sl - slot_lo;
+                if (peer) {
+                    int ep;
+                    const long long off = slot_inbuf(dstv, e, sp, ep);
+                    for (int pp = 0; pp < dstv.n_p; ++pp)
+                        bulk_s2g(const_cast<bf16*>(slot_base(dstv, ep, pp)) + off + c0, src, cols * 2);
+                } else {
+                    bulk_s2g(out + (long long)e * out_stride_e + (long long)sp * out_stride_s + c0, src, cols * 2);
+                }
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    // ---- 4. zero rows up to each expert's last GEMM tile; unfilled slot_src entries
+    {
+        const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const long long gn = (long long)gridDim.x * blockDim.x;
+        const int vec = M / 8;
+        for (int e = 0; e < E; ++e) {
+            const int f = min(s_tot[e], cap);
+            int sf = f - slot_lo;
+            sf = sf < 0 ? 0 : (sf > slots_out ? slots_out : sf);
+            const int end = min((sf + 127) & ~127, slots_out);
+            const long long work = (long long)(end - sf) * vec;
+            for (long long i = gt; i < work; i += gn) {
+                const int r = sf + (int)(i / vec), c = (int)(i % vec) * 8;
+                if (peer) {
+                    int ep;
+                    const long long off = slot_inbuf(dstv, e, r, ep);
+                    for (int pp = 0; pp < dstv.n_p; ++pp)
+                        *reinterpret_cast<int4*>(const_cast<bf16*>(slot_base(dstv, ep, pp)) + off + c) =
+                            make_int4(0, 0, 0, 0);
+                } else {
+                    *reinterpret_cast<int4*>(out + (long long)e * out_stride_e + (long long)r * out_stride_s + c) =
+                        make_int4(0, 0, 0, 0);
+                }
+            }
+            for (long long i = gt; i < cap - f; i += gn) slot_src[(long long)e * cap + f + i] = -1;
+        }
+        if (blockIdx.x == 0 && threadIdx.x < E && fan.ptr[0] != nullptr) {   // per-segment fill counts
+            const int e = threadIdx.x;
+            int c = min(s_tot[e], cap) - slot_lo;
+            c = c < 0 ? 0 : (c > slots_out ? slots_out : c);
+            if (peer) {   // into each holder's table
+                const int ep = e / dstv.e_local, i = e - ep * dstv.e_local;
+                for (int p = 0; p < dstv.n_p; ++p) fan.ptr[ep * dstv.peer_ep + p * dstv.peer_p][i] = c;
+            } else {      // local: one (E) table
+                fan.ptr[0][e] = c;
+            }
+        }
+    }
 }
 
-int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const float* scale, int k, int E, int cap,
-                       int slot_lo, int slots_out, int M, const SlotView& dst, const int* fill, const IntFan* fill_dst,
-                       cudaStream_t s) {
-    PARM_CHECK_ARG(dst.n_peer >= 1 && dst.n_peer <= kMaxPeers, "dispatch_rows_peer: destination must be a peer view");
-    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && dst.stride_i % 8 == 0 && dst.stride_slo % 8 == 0,
-                   "dispatch_rows_peer: rows must be 16-byte aligned (M=%d)", M);
-    PARM_CHECK_ARG(E <= 1024, "dispatch_rows_peer: too many experts");
-    const long long rows = (long long)E * slots_out;
-    if (rows > 0 && ring::enabled() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && dst.stride_shi % 8 == 0) {
-        constexpr int S = 6;
-        static int per_sm = 0;
-        const int smem = ring::ring_smem(S, 1, 0);
-        auto kern = ring::dispatch_rows_ring<true, S>;
-        launch_k(kern, ring::grid_for(kern, smem, rows, per_sm), kRowThreads, smem, s, 
-            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
-            dst, fill);
-        PARM_CHECK_LAUNCH("dispatch_rows_peer");
-    } else if (rows > 0) {
-        launch_k(dispatch_rows_kernel<true>, row_grid((rows + 3) / 4), kRowThreads, 0, s, 
-            reinterpret_cast<const bf16*>(x), ldx, slot_src, scale, k, E, cap, slot_lo, slots_out, M, nullptr, 0, 0,
-            dst, fill);
-        PARM_CHECK_LAUNCH("dispatch_rows_peer");
+int route_dispatch(const void* x, long long ldx, const int* expert_idx, const int* counts, int n, int k, int E,
+                   int cap, int M, int* slot_idx, int* slot_src, int* fill, int slot_lo, int slots_out, void* out,
+                   long long out_stride_e, long long out_stride_s, const SlotView* dst, const IntFan* fill_dst,
+                   cudaStream_t s) {
+    PARM_CHECK_ARG(k >= 1 && k <= 8 && E >= 1 && E <= 32 && k <= E, "route_dispatch: need 1 <= k <= min(8, E), E <= 32");
+    PARM_CHECK_ARG(cap >= 1 && counts != nullptr && slot_idx != nullptr && slot_src != nullptr && fill != nullptr,
+                   "route_dispatch: capacity >= 1 and counts/slot_idx/slot_src/fill required");
+    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0,
+                   "route_dispatch: token rows must be 16-byte aligned (M=%d)", M);
+    const bool peer = dst != nullptr;
+    if (peer) {
+        PARM_CHECK_ARG(dst->n_peer >= 1 && dst->n_peer <= kMaxPeers, "route_dispatch: destination must be a peer view");
+        PARM_CHECK_ARG(dst->stride_i % 8 == 0 && dst->stride_slo % 8 == 0 && dst->stride_shi % 8 == 0,
+                       "route_dispatch: destination rows must be 16-byte aligned");
+        for (int i = 0; i < dst->n_peer; ++i)
+            PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(dst->peer[i]) & 15) == 0,
+                           "route_dispatch: peer buffer %d not 16-byte aligned", i);
+    } else if (out != nullptr) {
+        PARM_CHECK_ARG((reinterpret_cast<uintptr_t>(out) & 15) == 0 && out_stride_e % 8 == 0 && out_stride_s % 8 == 0,
+                       "route_dispatch: output rows must be 16-byte aligned");
+    } else {
+        slots_out = 0;   // slot pass only
     }
-    if (fill != nullptr && fill_dst != nullptr) {
-        launch_k(fan_fill_kernel, 1, ((E + 31) / 32) * 32, 0, s, fill, E, slot_lo, slots_out, dst, *fill_dst);
-        PARM_CHECK_LAUNCH("dispatch_rows_peer(fill)");
+    PARM_CHECK_ARG(slots_out >= 0 && slot_lo >= 0, "route_dispatch: bad slot range");
+    const int tiles = (n + 7) / 8;
+    // one CTA per SM, at most 2048 tokens (64 ballot chunks) per CTA
+    int grid = std::max(1, std::min(tiles, kNumSMs));
+    grid = std::max(grid, (tiles + 255) / 256);
+    const SlotView none{};
+    IntFan nofan{};
+    const int smem = kRdWarps * kRdStages * (kRdCols * 2 + 8);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(route_dispatch_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(route_dispatch_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
     }
+    launch_k(E <= 8 ? route_dispatch_kernel<8> : route_dispatch_kernel<32>, grid, kRdWarps * 32, smem, s, reinterpret_cast<const bf16*>(x), ldx, expert_idx,
+             counts, n, k, E, cap, M, slot_idx, slot_src, fill, slot_lo, slots_out, reinterpret_cast<bf16*>(out),
+             out_stride_e, out_stride_s, peer ? *dst : none, fill_dst ? *fill_dst : nofan, peer ? 1 : 0);
+    PARM_CHECK_LAUNCH("route_dispatch");
     return 0;
 }
 
@@ -571,7 +688,6 @@ int dispatch_rows_peer(const void* x, long long ldx, const int* slot_src, const 
 __global__ void __launch_bounds__(kRowThreads) push_rows_kernel(const bf16* __restrict__ src, int nseg, int el,
                                                                 int rows, int M, const int* __restrict__ fill,
                                                                 const __grid_constant__ RowFan dst) {
-    pdl_entry();
     const int lane = threadIdx.x & 31;
     const long long warp_global = ((long long)blockIdx.x * kRowThreads + threadIdx.x) >> 5;
     const long long num_warps = ((long long)gridDim.x * kRowThreads) >> 5;
@@ -607,11 +723,7 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
     PARM_CHECK_ARG(M % 8 == 0 && fill != nullptr, "push_rows: M=%d must be a multiple of 8, fill required", M);
     const long long total = (long long)nseg * el * rows;
     if (total == 0) return 0;
-    int grid = row_grid(total);
-    if (const char* e = getenv("PARM_PUSH_MAX_CTAS")) {   // probe knob: NVLink store rate vs issuing SMs
-        const int cap = atoi(e);
-        if (cap > 0 && cap < grid) grid = cap;
-    }
+    const int grid = row_grid(total);
     launch_k(push_rows_kernel, grid, kRowThreads, 0, s, reinterpret_cast<const bf16*>(src), nseg, el, rows, M,
         fill, dst);
     PARM_CHECK_LAUNCH("push_rows");
@@ -622,7 +734,6 @@ int push_rows(const void* src, int nseg, int el, int rows, int M, const int* fil
 // `bytes` of src stored into each dst.ptr[i] (16-byte vectors): small payloads
 // replicated to every MP peer (the gate-gradient exchange of S1).
 __global__ void fan_copy_kernel(const int4* __restrict__ src, long long vecs, const __grid_constant__ RowFan dst) {
-    pdl_entry();
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < vecs; i += (long long)gridDim.x * blockDim.x) {
         const int4 v = __ldg(src + i);
         for (int f = 0; f < dst.n; ++f) reinterpret_cast<int4*>(dst.ptr[f])[i] = v;
@@ -664,7 +775,6 @@ struct PeerSignalSet {
 };
 
 __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignalSet set) {
-    pdl_entry();
     const PeerSignal& sig = set.sig[blockIdx.x];
     __shared__ unsigned epoch;
     if (threadIdx.x == 0) {
@@ -744,7 +854,7 @@ int combine_fwd_fan(const SlotView& y, const int* expert_idx, const int* slot_id
     PARM_CHECK_ARG(k >= 1 && k <= 8, "combine_fwd: top_k must be in [1, 8]");
     PARM_CHECK_ARG(O.n >= 1 && O.n <= kMaxPeers, "combine_fwd: output fan of %d buffers", O.n);
     if (n == 0) return 0;
-    if (ring::enabled() && k <= 2 && y.n_p <= 2 && ring::view_aligned(y) && ring::fan_aligned(O, ldo)) {
+    if (k <= 2 && y.n_p <= 2 && ring::view_aligned(y) && ring::fan_aligned(O, ldo)) {
         constexpr int S = 4;
         static int per_sm1 = 0, per_sm2 = 0;
         const int smem = ring::ring_smem(S, 2 * y.n_p, 0);
@@ -765,24 +875,6 @@ int combine_fwd_fan(const SlotView& y, const int* expert_idx, const int* slot_id
     else
         launch_k(combine_fwd_kernel<8>, resident_grid(n, 2), kRowThreads, 0, s, y, expert_idx, slot_idx, combine_w, n, k, M, O, ldo);
     PARM_CHECK_LAUNCH("combine_fwd");
-    return 0;
-}
-
-int combine_bwd(const void* dout, long long ldd, const SlotView& y, const int* expert_idx, const int* slot_idx,
-                const float* probs, int n, int k, int E, int M, float* dlogits, cudaStream_t s) {
-    if (int rc = check_view(y, M, "combine_bwd")) return rc;
-    PARM_CHECK_ARG(k <= 8 && E <= 32, "combine_bwd: k<=8 and E<=32 required");
-    if (n == 0) return 0;
-    auto D = reinterpret_cast<const bf16*>(dout);
-    const DyScatter none{};
-    const SlotView nov{};
-    if (k <= 2)
-        launch_k(combine_bwd_kernel<2, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
-            probs, n, k, E, M, dlogits, none, nov);
-    else
-        launch_k(combine_bwd_kernel<8, 0>, resident_grid(n, 2), kRowThreads, 0, s, D, ldd, y, expert_idx, slot_idx,
-            probs, n, k, E, M, dlogits, none, nov);
-    PARM_CHECK_LAUNCH("combine_bwd");
     return 0;
 }
 
@@ -843,7 +935,7 @@ int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_
     if (n == 0) return 0;
     auto W = reinterpret_cast<const bf16*>(wg);
     PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0, "dispatch_bwd: rows must be 16-byte aligned (M=%d)", M);
-    if (ring::enabled() && k <= 2 && dr.n_p <= 2 && ring::view_aligned(dr) && ring::fan_aligned(DX, ldx) &&
+    if (k <= 2 && dr.n_p <= 2 && ring::view_aligned(dr) && ring::fan_aligned(DX, ldx) &&
         (dlogits == nullptr || (E % 4 == 0 && (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0))) {
         constexpr int S = 4;
         static int per_sm1 = 0, per_sm2 = 0;
@@ -860,16 +952,11 @@ int dispatch_bwd_fan(const SlotView& dr, const int* expert_idx, const int* slot_
         PARM_CHECK_LAUNCH("dispatch_bwd");
         return 0;
     }
-    // (the E <= 8 variant that keeps the logit gradients in registers spills at 128 registers and
-    // measured 39 us against 30 us for loading them per use; kept for E <= 8 experiments only)
-    if (k <= 2 && E <= 8 && getenv("PARM_DBWD_REGS"))
-        launch_k(dispatch_bwd_kernel<2, 4, 8>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
-            W, n, k, E, M, DX, ldx);
-    else if (k <= 2)
-        launch_k(dispatch_bwd_kernel<2, 4, 0>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
+    if (k <= 2)
+        launch_k(dispatch_bwd_kernel<2, 4>, row_grid((n + 3) / 4), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits,
             W, n, k, E, M, DX, ldx);
     else
-        launch_k(dispatch_bwd_kernel<8, 1, 0>, row_grid(n), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits, W, n, k,
+        launch_k(dispatch_bwd_kernel<8, 1>, row_grid(n), kRowThreads, 0, s, dr, expert_idx, slot_idx, dlogits, W, n, k,
             E, M, DX, ldx);
     PARM_CHECK_LAUNCH("dispatch_bwd");
     return 0;

@@ -88,41 +88,52 @@ def plain_view(t: torch.Tensor, e_local: int | None = None) -> SlotView:
 
 
 def gate_fwd(x: torch.Tensor, wg: torch.Tensor, k: int, expert_idx: torch.Tensor, combine_w: torch.Tensor,
-             probs: torch.Tensor | None) -> None:
+             probs: torch.Tensor | None, counts: torch.Tensor | None = None) -> None:
+    """wg: gate weights transposed, (E, M) bf16.  counts: int32 (ceil(n/8), E) per-tile pick counts."""
     _need(x, torch.bfloat16, "tokens")
-    _need(wg, torch.float64, "gate weights (f64 upcast, transposed (E, M))")
+    _need(wg, torch.bfloat16, "gate weights (bf16, transposed (E, M))")
     n, M = x.shape
     E = wg.shape[0]          # gate weights are stored transposed: (E, M)
-    if x.stride(1) != 1 or not wg.is_contiguous():
-        raise ValueError("tokens rows and gate weights must be contiguous")
+    if x.stride(1) != 1 or not wg.is_contiguous() or wg.shape[1] != M:
+        raise ValueError("tokens rows and (E, M) gate weights must be contiguous")
+    if counts is not None and (counts.dtype != torch.int32 or counts.numel() < (n + 7) // 8 * E):
+        raise ValueError("counts must be int32 with ceil(n/8) * E entries")
     _lib.call("parm_gate_fwd", x.data_ptr(), x.stride(0), wg.data_ptr(), n, M, E, k, expert_idx.data_ptr(),
-              combine_w.data_ptr(), _ptr(probs), _stream())
+              combine_w.data_ptr(), _ptr(probs), _ptr(counts), _stream())
 
 
-def gate_slots_workspace(n: int, E: int) -> int:
-    return int(_lib.load().parm_gate_slots_workspace(n, E))
-
-
-def gate_slots(expert_idx: torch.Tensor, E: int, cap: int, slot_idx: torch.Tensor, slot_src: torch.Tensor,
-               fill: torch.Tensor, workspace: torch.Tensor | None = None) -> None:
+def route_dispatch(x: torch.Tensor, expert_idx: torch.Tensor, counts: torch.Tensor, cap: int, slot_idx: torch.Tensor,
+                   slot_src: torch.Tensor, fill: torch.Tensor, slot_lo: int = 0, out: torch.Tensor | None = None,
+                   dst: SlotView | None = None, slots_out: int | None = None, fill_fan: list | None = None) -> None:
+    """Slot pass + dispatch (one kernel): slots from the gate's tile counts, and every kept pick's
+    token row into ``out`` (E, S_out, M) rows [slot_lo, slot_lo + S_out) -- or, with ``dst``, into
+    the holders' receive buffers (peer view; per-segment fill counts to ``fill_fan``)."""
+    _need(x, torch.bfloat16, "tokens")
     n, k = expert_idx.shape
-    if workspace is None:
-        workspace = torch.empty(max(1, gate_slots_workspace(n, E) // 4), dtype=torch.int32, device=expert_idx.device)
-    _lib.call("parm_gate_slots", expert_idx.data_ptr(), n, k, E, cap, slot_idx.data_ptr(), slot_src.data_ptr(),
-              fill.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(), _stream())
-
-
-def dispatch_rows(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, out: torch.Tensor,
-                  scale: torch.Tensor | None = None, fill: torch.Tensor | None = None) -> None:
-    """out: (E, S_out, M) view (any strides with unit inner stride).  With ``fill`` (per-expert
-    counts) rows past the segment's last 128-row GEMM tile are not written."""
-    _need(x, torch.bfloat16, "rows source")
+    E = slot_src.shape[0]
+    if x.shape[0] != n or x.stride(1) != 1:
+        raise ValueError("route_dispatch: x must be (n, M) with unit inner stride")
+    if dst is not None:
+        if slots_out is None:
+            raise ValueError("route_dispatch: slots_out required with a peer destination")
+        dv = dst.c()
+        ff = _fan(fill_fan, _lib.IntFanC) if fill_fan is not None else None
+        _lib.call("parm_route_dispatch", x.data_ptr(), x.stride(0), expert_idx.data_ptr(), counts.data_ptr(), n, k, E,
+                  cap, x.shape[1], slot_idx.data_ptr(), slot_src.data_ptr(), fill.data_ptr(), slot_lo, slots_out, None,
+                  0, 0, ctypes.byref(dv), None if ff is None else ctypes.byref(ff), _stream())
+        return
+    ff = _fan(fill_fan, _lib.IntFanC) if fill_fan is not None else None
+    if out is None:                      # slot pass only
+        _lib.call("parm_route_dispatch", x.data_ptr(), x.stride(0), expert_idx.data_ptr(), counts.data_ptr(), n, k, E,
+                  cap, x.shape[1], slot_idx.data_ptr(), slot_src.data_ptr(), fill.data_ptr(), slot_lo, 0, None, 0, 0,
+                  None, None if ff is None else ctypes.byref(ff), _stream())
+        return
     _need(out, torch.bfloat16, "dispatch out")
-    E, S, M = out.shape
-    if out.stride(2) != 1 or x.stride(1) != 1:
-        raise ValueError("dispatch rows need unit inner stride")
-    _lib.call("parm_dispatch_rows", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
-              slot_lo, S, M, out.data_ptr(), out.stride(0), out.stride(1), _ptr(fill), _stream())
+    if out.stride(2) != 1 or out.shape[0] != E:
+        raise ValueError("route_dispatch: out must be (E, S_out, M) with unit inner stride")
+    _lib.call("parm_route_dispatch", x.data_ptr(), x.stride(0), expert_idx.data_ptr(), counts.data_ptr(), n, k, E,
+              cap, x.shape[1], slot_idx.data_ptr(), slot_src.data_ptr(), fill.data_ptr(), slot_lo, out.shape[1],
+              out.data_ptr(), out.stride(0), out.stride(1), None, None if ff is None else ctypes.byref(ff), _stream())
 
 
 def combine_fwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,
@@ -134,22 +145,12 @@ def combine_fwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor
               combine_w.data_ptr(), n, k, M, out.data_ptr(), out.stride(0), _stream())
 
 
-def combine_bwd(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor,
-                probs: torch.Tensor, dlogits: torch.Tensor) -> None:
-    n, M = dout.shape
-    k = expert_idx.shape[1]
-    E = probs.shape[1]
-    v = view.c()
-    _lib.call("parm_combine_bwd", dout.data_ptr(), dout.stride(0), ctypes.byref(v), expert_idx.data_ptr(),
-              slot_idx.data_ptr(), probs.data_ptr(), n, k, E, M, dlogits.data_ptr(), _stream())
-
-
 def combine_bwd_dispatch(dout: torch.Tensor, view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor,
                          probs: torch.Tensor, combine_w: torch.Tensor, dlogits: torch.Tensor, slot_lo: int,
                          fill: torch.Tensor, out: torch.Tensor | None = None, dst: SlotView | None = None,
                          slots_out: int | None = None) -> None:
-    """combine_bwd + dispatch_rows(dout, scale=combine_w, fill) in one pass over dOut: the slot rows
-    go to ``out`` (E, S_out, M) or, with ``dst``, to the holders through the peer view."""
+    """Combine backward (dlogits) and the dispatch of combine_w * dOut into slot rows in one pass
+    over dOut: the rows go to ``out`` (E, S_out, M) or, with ``dst``, to the holders (peer view)."""
     _need(dout, torch.bfloat16, "dOut")
     n, M = dout.shape
     k = expert_idx.shape[1]
@@ -182,23 +183,6 @@ def dispatch_bwd(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tenso
     v = view.c()
     _lib.call("parm_dispatch_bwd", ctypes.byref(v), expert_idx.data_ptr(), slot_idx.data_ptr(), _ptr(dlogits),
               _ptr(wg), n, k, E, M, dx.data_ptr(), dx.stride(0), _stream())
-
-
-def dispatch_rows_peer(x: torch.Tensor, slot_src: torch.Tensor, k: int, cap: int, slot_lo: int, slots_out: int,
-                       dst: SlotView, fill: torch.Tensor | None = None, fill_fan: list | None = None,
-                       scale: torch.Tensor | None = None) -> None:
-    """Dispatch fused with the EP&ESP AlltoAll: slot rows [slot_lo, slot_lo+slots_out) stored
-    into the holders' receive buffers through the peer view ``dst`` (n_p = N_ESP dump copies);
-    with ``fill`` the per-segment fill counts go to ``fill_fan`` (int32 addresses, view indexing)."""
-    _need(x, torch.bfloat16, "rows source")
-    E = slot_src.shape[0]
-    v = dst.c()
-    ff = _fan(fill_fan, _lib.IntFanC) if fill_fan is not None else None
-    _lib.call("parm_dispatch_rows_peer", x.data_ptr(), x.stride(0), slot_src.data_ptr(), _ptr(scale), k, E, cap,
-              slot_lo, slots_out, x.shape[1], ctypes.byref(v), _ptr(fill), None if ff is None else ctypes.byref(ff),
-              _stream())
-    if ff is not None and fill is not None:
-        _lib.launch_count += 1            # the fill-count fan-out kernel
 
 
 def combine_fwd_fan(view: SlotView, expert_idx: torch.Tensor, slot_idx: torch.Tensor, combine_w: torch.Tensor,

@@ -92,7 +92,6 @@ class ParmMoE(nn.Module):
             s.gate[:, :d.M].copy_(self.gate)
             s.w1t[:, :d.Hs, :d.M].copy_(self.w1.transpose(1, 2))
             s.w2t[:, :d.M, :d.Hs].copy_(self.w2.transpose(1, 2))
-        self.layer.refresh_gate()
         self._synced = key
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:

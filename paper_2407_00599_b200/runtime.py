@@ -94,21 +94,26 @@ class Routing:
     fill: torch.Tensor         # (E,) int32
     cap: int
     token_offset: int = 0
-    ws: torch.Tensor | None = None     # gate_slots per-chunk counts
+    counts: torch.Tensor | None = None   # per-8-token-tile pick counts (gate -> slot pass)
 
     @classmethod
     def alloc(cls, n: int, k: int, E: int, cap: int, dev, token_offset: int = 0,
               fill: torch.Tensor | None = None) -> "Routing":
         i32 = dict(dtype=torch.int32, device=dev)
         f32 = dict(dtype=torch.float32, device=dev)
-        ws = torch.empty(max(1, K.gate_slots_workspace(n, E) // 4), **i32)
         return cls(torch.empty(n, k, **i32), torch.empty(n, k, **f32), torch.empty(n, E, **f32),
                    torch.empty(n, k, **i32), torch.empty(E, max(cap, 1), **i32),
-                   fill if fill is not None else torch.zeros(E, **i32), cap, token_offset, ws)
+                   fill if fill is not None else torch.zeros(E, **i32), cap, token_offset,
+                   torch.empty(max(1, (n + 7) // 8 * E), **i32))
 
-    def run(self, x: torch.Tensor, wg_t: torch.Tensor, k: int) -> None:
-        K.gate_fwd(x, wg_t, k, self.expert_idx, self.combine_w, self.probs)
-        K.gate_slots(self.expert_idx, wg_t.shape[0], self.cap, self.slot_idx, self.slot_src, self.fill, self.ws)
+    def run(self, x: torch.Tensor, wg_t: torch.Tensor, k: int, out: torch.Tensor | None = None, slot_lo: int = 0,
+            dst: K.SlotView | None = None, slots_out: int | None = None, fill_fan: list | None = None) -> None:
+        """Gate (f64 tensor-core logits, softmax, stable top-k, tile counts), then the slot pass
+        fused with the dispatch of the token rows into ``out`` / the holders (``dst``), or the
+        slot pass alone when neither is given."""
+        K.gate_fwd(x, wg_t, k, self.expert_idx, self.combine_w, self.probs, self.counts)
+        K.route_dispatch(x, self.expert_idx, self.counts, self.cap, self.slot_idx, self.slot_src, self.fill, slot_lo,
+                         out=out, dst=dst, slots_out=slots_out, fill_fan=fill_fan)
 
 
 @dataclass
@@ -121,7 +126,6 @@ class RankState:
     dw1t: torch.Tensor            # (e_local, Hsp, Mp) f32
     dw2t: torch.Tensor            # (e_local, Mp, Hsp) f32
     bufs: dict = field(default_factory=dict)
-    gate64: torch.Tensor | None = None   # exact f64 upcast of `gate` for the f64 logits (refresh_gate(), in place)
 
 
 @dataclass
@@ -195,11 +199,9 @@ class MoELayer:
             self.st[r] = RankState(r, torch.zeros(d.E, d.Mp, **bf), torch.zeros(d.e_local, d.Hsp, d.Mp, **bf),
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **bf), torch.zeros(d.E, d.Mp, **f32),
                                    torch.zeros(d.e_local, d.Hsp, d.Mp, **f32),
-                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **f32),
-                                   gate64=torch.zeros(d.E, d.Mp, dtype=torch.float64, device=self.dev))
+                                   torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
         self._last: str | None = None
         self._ws_gate = None
-        self.refresh_gate()
 
     # ------------------------------------------------------------ weights
     def local_experts(self, rank: int) -> range:
@@ -221,13 +223,6 @@ class MoELayer:
                 w2 = np.ascontiguousarray(weights.w2[e][p * d.Hs:(p + 1) * d.Hs, :].T)   # (M, Hs)
                 s.w1t[i, :d.Hs, :d.M].copy_(torch.from_numpy(w1).to(torch.float32).to(self.dev).to(torch.bfloat16))
                 s.w2t[i, :d.M, :d.Hs].copy_(torch.from_numpy(w2).to(torch.float32).to(self.dev).to(torch.bfloat16))
-        self.refresh_gate()
-
-    def refresh_gate(self) -> None:
-        """Re-derive the f64 upcast of the bf16 gate weights (call after updating ``gate``).
-        In place: a captured StepGraph keeps reading the same buffer and sees the update."""
-        for s in self.st.values():
-            s.gate64.copy_(s.gate)
 
     def init_random(self, seed: int = 0) -> None:
         """Synthetic weights drawn directly on the device with the reference's
@@ -244,7 +239,6 @@ class MoELayer:
                                         / math.sqrt(d.M))
             s.w2t[:, :d.M, :d.Hs].copy_(torch.randn(d.e_local, d.M, d.Hs, generator=gen, device=self.dev)
                                         / math.sqrt(d.H))
-        self.refresh_gate()
 
     def shard_grads(self, rank: int) -> dict:
         """Gradients in the reference layout: dw1 (e_local, M, Hs), dw2 (e_local, Hs, M), dgate (M, E)."""
@@ -368,8 +362,7 @@ class MoELayer:
                         slots_out=None) -> None:
         """Combine backward (dlogits) and the dispatch of combine_w * dOut into the slot rows the
         dH GEMM reads (``out``, or the holders' buffers through the peer view ``dst``) -- one
-        fused pass over dOut (bit-identical to combine_bwd + dispatch_rows(scale=combine_w),
-        tests/test_gpu_parity.py)."""
+        fused pass over dOut."""
         K.combine_bwd_dispatch(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, rt.combine_w, dlogits, slot_lo,
                                rt.fill, out=out, dst=dst, slots_out=slots_out)
 
@@ -495,8 +488,7 @@ class MoELayer:
             x = self._input(b, xs[r], "x")
             b["xin"] = x
             rt = b["route"]
-            rt.run(x, s.gate64, d.k)
-            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, 0, b["send"], fill=rt.fill)
+            rt.run(x, s.gate, d.k, out=b["send"])
             self._ffn_fwd(s, b)
             K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
             outs[r] = b["out"][:, :d.M]
@@ -557,9 +549,8 @@ class MoELayer:
             xs_ = x[m * sl:(m + 1) * sl]
             b["xslice"] = xs_
             rt = b["route"]
-            rt.run(xs_, s.gate64, d.k)
-            K.dispatch_rows_peer(xs_, rt.slot_src, d.k, rt.cap, 0, b["q"], self._peer_view(b, "recv", r),
-                                 fill=rt.fill, fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
+            rt.run(xs_, s.gate, d.k, dst=self._peer_view(b, "recv", r), slots_out=b["q"],
+                   fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
         self.world.peer_barrier()                                     # receive buffers complete
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
@@ -631,8 +622,7 @@ class MoELayer:
             xs_ = x[m * sl:(m + 1) * sl]                # MP split: this rank's token slice
             b["xslice"] = xs_
             rt = b["route"]
-            rt.run(xs_, s.gate64, d.k)
-            K.dispatch_rows(xs_, rt.slot_src, d.k, rt.cap, 0, b["send"], fill=rt.fill)
+            rt.run(xs_, s.gate, d.k, out=b["send"])
         self.world.exchange(self._fused_msgs("s1", "send", "recv", with_fill=True))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
@@ -772,11 +762,9 @@ class MoELayer:
             x = self._input(b, xs[r], "x")
             b["xin"] = x
             rt = b["route"]
-            rt.run(x, s.gate64, d.k)
             # this MP rank's slot shard [m q, (m+1) q) straight into the holders (dispatch + A2A + dump)
-            K.dispatch_rows_peer(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["q"],
-                                 self._peer_view(b, "recv", r), fill=rt.fill,
-                                 fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
+            rt.run(x, s.gate, d.k, slot_lo=L.mp_pos(r) * b["q"], dst=self._peer_view(b, "recv", r), slots_out=b["q"],
+                   fill_fan=[a + 4 * r * el for a in b["fill_in_peers"]])
         self.world.peer_barrier()
         for r in self.ranks:
             b = self.st[r].bufs["s2"]
@@ -825,13 +813,10 @@ class MoELayer:
             x = self._input(b, xs[r], "x")
             b["xin"] = x
             rt = b["route"]
-            rt.run(x, s.gate64, d.k)
-            K.dispatch_rows(x, rt.slot_src, d.k, rt.cap, L.mp_pos(r) * b["q"], b["send"], fill=rt.fill)
-            # fill of this rank's slot shard [m*q, (m+1)*q): clamp(fill - m*q, 0, q) per expert
+            # this rank's slot shard [m*q, (m+1)*q), and its fill clamp(fill - m*q, 0, q) per expert
             if "shard_fill" not in b:
                 b["shard_fill"] = torch.zeros(d.E, dtype=torch.int32, device=self.dev)
-            torch.sub(rt.fill, L.mp_pos(r) * b["q"], out=b["shard_fill"])
-            b["shard_fill"].clamp_(0, b["q"])
+            rt.run(x, s.gate, d.k, out=b["send"], slot_lo=L.mp_pos(r) * b["q"], fill_fan=[b["shard_fill"].data_ptr()])
         self.world.exchange(self._fused_msgs("s2", "send", "recv", with_fill=True, fill_key="shard_fill"))
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
@@ -881,15 +866,14 @@ class MoELayer:
             s, b = self.st[r], self._plan("baseline", r)
             x = self._input(b, xs[r], "x")
             b["xin"] = x
-            b["route"].run(x, s.gate64, d.k)                       # combine weights of the own block
+            b["route"].run(x, s.gate, d.k)                         # routing of the own block (slot pass only)
             ins[r], outs[r] = x, b["xg"]
         self.world.allgather("esp", ins, outs)                   # ESP-AllGather of raw tokens
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             for q in range(d.ESP):                               # re-gate every gathered block
                 rt = b["route_blk"][q]
-                rt.run(b["xg"][q], s.gate64, d.k)
-                K.dispatch_rows(b["xg"][q], rt.slot_src, d.k, d.T, 0, b["disp"][q], fill=rt.fill)
+                rt.run(b["xg"][q], s.gate, d.k, out=b["disp"][q])
         self.world.exchange(self._ep_dispatch_msgs("disp", "recv", with_fill=True))
         ys = {}
         for r in self.ranks:

@@ -133,7 +133,7 @@ class PeerLocalWorld(LocalWorld):
     ``sym`` hands each emulated rank its own zeroed copy of a "symmetric" buffer plus
     the addresses of every rank's copy -- exactly what ``PeerWorld`` gets from torch
     symmetric memory, except that the peers' copies live on the same GPU.  So the
-    fused kernels (``dispatch_rows_peer``, the GEMM's peer-epilogue stores,
+    fused kernels (``route_dispatch`` into the holders, the GEMM's peer-epilogue stores,
     ``combine_fwd_fan``, ``combine_bwd_dispatch`` into the holders, ``dispatch_bwd_fan``,
     ``fan_copy``, ``push_rows``) run with the same peer-pointer tables, segment
     offsets and layouts as on a multi-GPU box and can be checked against the oracle on

@@ -30,9 +30,9 @@ def lib():
 
 def test_header_lists_the_boundary():
     fns = header_functions()
-    for required in ("parm_gate_fwd", "parm_gate_slots", "parm_dispatch_rows", "parm_combine_fwd",
-                     "parm_combine_bwd", "parm_dispatch_bwd", "parm_esp_sum", "parm_gate_wgrad",
-                     "parm_gemm", "parm_last_error", "parm_abi_version", "parm_dispatch_rows_peer",
+    for required in ("parm_gate_fwd", "parm_gate_counts_bytes", "parm_route_dispatch", "parm_combine_fwd",
+                     "parm_dispatch_bwd", "parm_esp_sum", "parm_gate_wgrad",
+                     "parm_gemm", "parm_last_error", "parm_abi_version",
                      "parm_combine_fwd_fan", "parm_dispatch_bwd_fan", "parm_peer_barrier", "parm_push_rows",
                      "parm_fan_copy", "parm_gemm_peer", "parm_combine_bwd_dispatch"):
         assert required in fns
@@ -65,11 +65,14 @@ def _expect_arg_error(fn, *args, match):
 
 def test_argument_validation_without_a_gpu(lib):
     # validation happens on the host before any launch, with the reference's error wording
-    _expect_arg_error(lib.parm_gate_fwd, None, 8, None, 4, 8, 2, 3, None, None, None, None,
+    _expect_arg_error(lib.parm_gate_fwd, None, 8, None, 4, 8, 2, 3, None, None, None, None, None,
                       match=r"top_k \(3\) exceeds number of experts \(2\)")
-    _expect_arg_error(lib.parm_gate_slots, None, 4, 9, 2, 4, None, None, None, None, 0, None, match="top_k must be")
-    _expect_arg_error(lib.parm_dispatch_rows, None, 10, None, None, 1, 2, 4, 0, 4, 10, None, 10, 10, None, None,
-                      match="16-byte aligned")
+    _expect_arg_error(lib.parm_route_dispatch, None, 8, None, None, 16, 9, 8, 4, 8, None, None, None, 0, 4, None, 8,
+                      8, None, None, None, match="route_dispatch: need 1 <= k")
+    _expect_arg_error(lib.parm_route_dispatch, None, 10, None, None, 16, 2, 8, 4, 10, None, None, None, 0, 4, None,
+                      10, 10, None, None, None, match="counts/slot_idx/slot_src/fill required")
+    _expect_arg_error(lib.parm_route_dispatch, 16, 10, None, 32, 16, 2, 8, 4, 10, 64, 64, 64, 0, 4, None, 10, 10,
+                      None, None, None, match="16-byte aligned")
     _expect_arg_error(lib.parm_combine_fwd, None, None, None, None, 4, 1, 8, None, 8, None,
                       match="null slot view")
     _expect_arg_error(lib.parm_combine_bwd_dispatch, None, 8, None, None, None, None, None, 4, 2, 4, 8, None, 0, 4,
@@ -86,8 +89,8 @@ def test_argument_validation_without_a_gpu(lib):
 
 
 def test_gate_wgrad_workspace_query(lib):
-    assert lib.parm_gate_wgrad_workspace(8192, 1024, 8) == 64 * 1024 * 8 * 4      # 64 token chunks
-    assert lib.parm_gate_slots_workspace(8192, 8) == 32 * 8 * 4                   # 256-token chunks
+    assert lib.parm_gate_wgrad_workspace(8192, 1024, 8) == 148 * 1024 * 8 * 4     # one partial per SM
+    assert lib.parm_gate_counts_bytes(8192, 8) == 1024 * 8 * 4                    # 8-token tiles
 
 
 def test_missing_library_fails_loudly(tmp_path):

@@ -40,44 +40,69 @@ def _norm_err(got, ref):
 
 
 # --------------------------------------------------------------------------- gate
-@pytest.mark.parametrize("n,M,E,k,cap", [
-    (512, 256, 4, 2, 308),      # config 1 block, capacity T
-    (256, 256, 4, 2, 154),      # config 1 S1 slice, quota ceil(T/2)
-    (8192, 1024, 8, 2, 2458),   # config 2 block
-    (4096, 1024, 8, 2, 1229),   # config 2 S1 slice
-    (1000, 64, 16, 4, 100),     # overflow, E=16, k=4
-    (777, 128, 32, 2, 30),      # E=32, heavy overflow, ragged n
-    (3, 8, 2, 2, 1),
-])
-def test_gate_routing_bit_exact(cuda_lib, n, M, E, k, cap):
+def _gate_and_route(x, wg_t, k, cap, slot_lo=0, slots_out=None):
+    """gate_fwd (tile counts) + route_dispatch into a NaN-poisoned slot tensor."""
     from paper_2407_00599_b200 import kernels as K
 
-    rng = np.random.default_rng(n + M + E)
-    x = O.round_bf16(rng.normal(size=(n, M)))
-    wg = O.round_bf16(rng.normal(size=(M, E)))
-    ref = O.gate(x, wg, k, cap)
-    xd, wd = _t(x), _t(wg.T).double()   # gate weights live transposed (E, M), f64 upcast of bf16
+    n, M = x.shape
+    E = wg_t.shape[0]
+    slots_out = cap if slots_out is None else slots_out
     ei = torch.empty(n, k, dtype=torch.int32, device="cuda")
     cw = torch.empty(n, k, dtype=torch.float32, device="cuda")
     pr = torch.empty(n, E, dtype=torch.float32, device="cuda")
     si = torch.empty(n, k, dtype=torch.int32, device="cuda")
     ss = torch.empty(E, cap, dtype=torch.int32, device="cuda")
     fill = torch.empty(E, dtype=torch.int32, device="cuda")
-    K.gate_fwd(xd, wd, k, ei, cw, pr)
-    K.gate_slots(ei, E, cap, si, ss, fill)
+    counts = torch.empty((n + 7) // 8 * E, dtype=torch.int32, device="cuda")
+    rows = torch.full((E, slots_out, M), float("nan"), dtype=torch.bfloat16, device="cuda")
+    K.gate_fwd(x, wg_t, k, ei, cw, pr, counts)
+    K.route_dispatch(x, ei, counts, cap, si, ss, fill, slot_lo, out=rows)
+    return ei, cw, pr, si, ss, fill, counts, rows
+
+
+@pytest.mark.parametrize("n,M,E,k,cap", [
+    (512, 256, 4, 2, 308),      # config 1 block, capacity T
+    (256, 256, 4, 2, 154),      # config 1 S1 slice, quota ceil(T/2)
+    (8192, 1024, 8, 2, 2458),   # config 2 block
+    (4096, 1024, 8, 2, 1229),   # config 2 S1 slice
+    (1000, 64, 16, 4, 100),     # overflow, E=16, k=4
+    (777, 128, 32, 2, 30),      # E=32, heavy overflow, ragged n (fallback gate)
+    (3, 8, 2, 2, 1),            # tiny, M % 32 != 0 (fallback gate)
+    (20000, 512, 8, 2, 6000),   # several tiles per warp (ring wraps across tiles)
+    (5000, 2048, 8, 1, 700),    # M = 2048: 8 ring chunks per tile, k = 1
+])
+def test_gate_routing_bit_exact(cuda_lib, n, M, E, k, cap):
+    """Routing (expert_index, slot_index, drop set) bit-exact vs the oracle gate (dataplane.py:86-119),
+    scores to f32 rounding; the dispatched slot rows are exactly the token rows, zero up to each
+    expert's last 128-row tile; slot_src inverts slot_index."""
+    rng = np.random.default_rng(n + M + E)
+    x = O.round_bf16(rng.normal(size=(n, M)))
+    wg = O.round_bf16(rng.normal(size=(M, E)))
+    ref = O.gate(x, wg, k, cap)
+    xd = _t(x)
+    ei, cw, pr, si, ss, fill, counts, rows = _gate_and_route(xd, _t(wg.T).contiguous(), k, cap)
     np.testing.assert_array_equal(ei.cpu().numpy(), ref.expert_index)
     np.testing.assert_array_equal(si.cpu().numpy(), ref.slot_index)
     np.testing.assert_allclose(cw.cpu().numpy(), ref.combine_weights, rtol=2e-6, atol=1e-30)
     np.testing.assert_allclose(pr.cpu().numpy(), ref.scores, rtol=2e-6, atol=1e-30)
-    counts = np.bincount(ref.expert_index[ref.slot_index >= 0], minlength=E)
-    np.testing.assert_array_equal(fill.cpu().numpy(), counts)
-    # inverse map: every filled slot points back at its pick
+    counts_ref = np.bincount(ref.expert_index[ref.slot_index >= 0], minlength=E)
+    np.testing.assert_array_equal(fill.cpu().numpy(), counts_ref)
+    tiles = np.zeros(((n + 7) // 8, E), dtype=np.int64)
+    for t in range(n):
+        for j in range(k):
+            tiles[t // 8, ref.expert_index[t, j]] += 1
+    np.testing.assert_array_equal(counts.view((n + 7) // 8, E).cpu().numpy(), tiles)
     ssh = ss.cpu().numpy()
+    rows_h = rows.float().cpu().numpy()
     for e in range(E):
-        for s in range(counts[e]):
-            t, j = divmod(int(ssh[e, s]), k)
-            assert ref.expert_index[t, j] == e and ref.slot_index[t, j] == s
-        assert (ssh[e, counts[e]:] == -1).all()
+        t_of = ssh[e, :counts_ref[e]] // k
+        j_of = ssh[e, :counts_ref[e]] % k
+        assert (ref.expert_index[t_of, j_of] == e).all() and (ref.slot_index[t_of, j_of] == np.arange(counts_ref[e])).all()
+        assert (ssh[e, counts_ref[e]:] == -1).all()
+        np.testing.assert_array_equal(rows_h[e, :counts_ref[e]], x[t_of])
+        end = min(-(-counts_ref[e] // 128) * 128, cap)
+        assert (rows_h[e, counts_ref[e]:end] == 0).all()
+        assert np.isnan(rows_h[e, end:]).all()           # never touched beyond the last GEMM tile
 
 
 @pytest.mark.parametrize("n,M,E,k,cap,slot_lo,slots_out", [
@@ -86,38 +111,50 @@ def test_gate_routing_bit_exact(cuda_lib, n, M, E, k, cap):
     (777, 128, 16, 1, 40, 0, 48),          # k=1, heavy overflow, padded shard past cap
     (300, 64, 8, 4, 90, 0, 90),            # k=4 (KT=8 kernel)
 ])
-def test_combine_bwd_dispatch_matches_separate_kernels(cuda_lib, n, M, E, k, cap, slot_lo, slots_out):
-    """The fused combine-backward + dOut dispatch writes exactly what combine_bwd and
-    dispatch_rows(scale = combine weights, fill) write (bit-identical dlogits and slot rows)."""
+def test_combine_bwd_dispatch_matches_reference(cuda_lib, n, M, E, k, cap, slot_lo, slots_out):
+    """The fused combine backward + dOut dispatch: dlogits against the f64 softmax adjoint, and the
+    slot rows exactly bf16(combine_w * dOut) (f32 product, round to nearest even), zero up to each
+    expert's last 128-row tile, untouched beyond; also the forward route_dispatch of a slot shard."""
     from paper_2407_00599_b200 import kernels as K
 
     rng = np.random.default_rng(n + k)
-    x = _t(O.round_bf16(rng.normal(size=(n, M))))
-    wg = _t(O.round_bf16(rng.normal(size=(M, E))).T).double()
-    ei = torch.empty(n, k, dtype=torch.int32, device="cuda")
-    cw = torch.empty(n, k, dtype=torch.float32, device="cuda")
-    pr = torch.empty(n, E, dtype=torch.float32, device="cuda")
-    si = torch.empty(n, k, dtype=torch.int32, device="cuda")
-    ss = torch.empty(E, cap, dtype=torch.int32, device="cuda")
-    fill = torch.empty(E, dtype=torch.int32, device="cuda")
-    K.gate_fwd(x, wg, k, ei, cw, pr)
-    K.gate_slots(ei, E, cap, si, ss, fill)
-    y = _t(O.round_bf16(rng.normal(size=(E, cap, M))))
+    xh = O.round_bf16(rng.normal(size=(n, M)))
+    x = _t(xh)
+    wg = _t(O.round_bf16(rng.normal(size=(M, E))).T).contiguous()
+    ei, cw, pr, si, ss, fill, counts, fwd_rows = _gate_and_route(x, wg, k, cap, slot_lo, slots_out)
+    yh = O.round_bf16(rng.normal(size=(E, cap, M)))
+    y = _t(yh)
     view = K.SlotView(y, e_local=E, stride_i=cap * M, stride_slo=M)
-    dout = _t(O.round_bf16(rng.normal(size=(n, M))))
-    poison = float("nan")
-    dl_a = torch.full((n, E), poison, device="cuda")
-    dl_b = torch.full((n, E), poison, device="cuda")
-    rows_a = torch.full((E, slots_out, M), poison, device="cuda", dtype=torch.bfloat16)
-    rows_b = rows_a.clone()
-    K.combine_bwd(dout, view, ei, si, pr, dl_a)
-    K.dispatch_rows(dout, ss, k, cap, slot_lo, rows_a, scale=cw, fill=fill)
-    K.combine_bwd_dispatch(dout, view, ei, si, pr, cw, dl_b, slot_lo, fill, out=rows_b)
+    douth = O.round_bf16(rng.normal(size=(n, M)))
+    dout = _t(douth)
+    dl = torch.full((n, E), float("nan"), device="cuda")
+    rows = torch.full((E, slots_out, M), float("nan"), device="cuda", dtype=torch.bfloat16)
+    K.combine_bwd_dispatch(dout, view, ei, si, pr, cw, dl, slot_lo, fill, out=rows)
     torch.cuda.synchronize()
-    assert torch.equal(dl_a, dl_b)
-    # rows the GEMM reads (up to each expert's last 128-row tile) are identical, NaN poison included
-    assert torch.equal(rows_a.isnan(), rows_b.isnan())
-    assert torch.equal(torch.nan_to_num(rows_a.float()), torch.nan_to_num(rows_b.float()))
+    ei_h, si_h, pr_h = ei.cpu().numpy(), si.cpu().numpy(), pr.cpu().numpy().astype(np.float64)
+    cw_t = cw.cpu()
+    dS = np.zeros((n, E))
+    for t in range(n):
+        for j in range(k):
+            if si_h[t, j] >= 0:
+                dS[t, ei_h[t, j]] = douth[t] @ yh[ei_h[t, j], si_h[t, j]]
+    dl_ref = pr_h * (dS - (pr_h * dS).sum(axis=1, keepdims=True))
+    np.testing.assert_allclose(dl.cpu().numpy(), dl_ref, rtol=1e-4, atol=1e-4 * np.abs(dl_ref).max())
+    fill_h = fill.cpu().numpy()
+    rows_h = rows.float().cpu()
+    fwd_h = fwd_rows.float().cpu().numpy()
+    ss_h = ss.cpu().numpy()
+    dout_c = dout.float().cpu()
+    for e in range(E):
+        sf = int(np.clip(fill_h[e] - slot_lo, 0, slots_out))
+        end = min(-(-sf // 128) * 128, slots_out)
+        src = ss_h[e, slot_lo:slot_lo + sf]
+        t, j = torch.from_numpy(src // k), torch.from_numpy(src % k)
+        want = (dout_c[t] * cw_t[t, j][:, None]).to(torch.bfloat16).float()
+        assert torch.equal(rows_h[e, :sf], want), e
+        np.testing.assert_array_equal(fwd_h[e, :sf], xh[src // k])
+        assert (rows_h[e, sf:end] == 0).all() and (fwd_h[e, sf:end] == 0).all()
+        assert rows_h[e, end:].isnan().all() and np.isnan(fwd_h[e, end:]).all()
 
 
 def test_gate_ties_go_to_lower_expert(cuda_lib):
@@ -396,3 +433,25 @@ def test_input_validation_messages(cuda_lib):
                          np.zeros((4, 8, 4)))
     with pytest.raises(ValueError, match="exceeds"):
         api.gate(np.ones((2, 3)), np.ones((3, 2)), k=3, capacity=4)
+
+
+@pytest.mark.parametrize("n,M,E", [(8192, 1024, 8), (300, 64, 4), (5000, 2048, 16), (777, 128, 32), (40000, 256, 8)])
+def test_gate_wgrad_matches_f64(cuda_lib, n, M, E):
+    """dWg^T (E, M) = dlogits^T x: one partial per SM over contiguous token ranges, summed in a
+    fixed order -- against the f64 product, and bit-identical run to run (deterministic)."""
+    from paper_2407_00599_b200 import kernels as K
+
+    rng = np.random.default_rng(n + M)
+    xh = O.round_bf16(rng.normal(size=(n, M)))
+    dl = rng.normal(size=(n, E)).astype(np.float32)
+    x, dlt = _t(xh), torch.from_numpy(dl).cuda()
+    ws = torch.empty(K.gate_wgrad_workspace(n, M, E) // 4, dtype=torch.float32, device="cuda")
+    out = torch.full((E, M), float("nan"), device="cuda")
+    K.gate_wgrad(x, dlt, out, ws)
+    ref = dl.astype(np.float64).T @ xh
+    assert _norm_err(out.cpu().numpy(), ref) <= 1e-6
+    again = torch.zeros_like(out)
+    K.gate_wgrad(x, dlt, again, ws)
+    assert torch.equal(out, again)
+    K.gate_wgrad(x, dlt, again, ws, accumulate=True)
+    torch.testing.assert_close(again, 2 * out, rtol=1e-6, atol=1e-6)

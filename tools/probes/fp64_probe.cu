@@ -31,6 +31,22 @@ __global__ void k_dfma(double* out, int iters, double a, double b) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_cvt(double* out, int iters, const float* in) {
+    float x[8];
+    for (int i = 0; i < 8; ++i) x[i] = in[(threadIdx.x + i) & 255];
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            acc[i] = acc[i] + (double)x[i];   // F2F + DADD
+            x[i] = __int_as_float(__float_as_int(x[i]) ^ 1);
+        }
+    }
+    double s = 0;
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
     double* out;
     cudaMalloc(&out, 148 * 64 * 1024 * sizeof(double));
@@ -61,6 +77,36 @@ int main() {
             cudaEventElapsedTime(&ms, e0, e1);
             double fl = 148.0 * warps * 32 * iters * 8 * 2.0;
             if (rep) printf("DFMA  warps/SM=%2d chains=8: %.3f ms  %.1f TFLOP/s\n", warps, ms, fl / ms / 1e9);
+        }
+    }
+    {
+        float* in;
+        cudaMalloc(&in, 256 * 4);
+        cudaMemset(in, 0, 256 * 4);
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            k_cvt<<<148, 512>>>(out, iters, in);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            double ops = 148.0 * 512 * iters * 8;
+            if (rep) printf("F2F.F64.F32+DADD: %.3f ms  %.1f G conv/s  (%.2f per clk per SM at 1.9 GHz)\n", ms,
+                            ops / ms / 1e6, ops / (ms * 1e-3) / 1.9e9 / 148);
+        }
+    }
+    for (int ch : {1, 2, 4}) {
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            if (ch == 1) k_dmma<1><<<148, 128>>>(out, iters, 1.0000001, 0.999999);
+            if (ch == 2) k_dmma<2><<<148, 128>>>(out, iters, 1.0000001, 0.999999);
+            if (ch == 4) k_dmma<4><<<148, 128>>>(out, iters, 1.0000001, 0.999999);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            double fl = 148.0 * 4 * iters * ch * 512.0;
+            if (rep) printf("DMMA 4 warps/SM chains=%d: %.1f TFLOP/s\n", ch, fl / ms / 1e9);
         }
     }
     // latency: one chain, one warp

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--cfg", default=None, help="B,L,M,H,E,k,f (default: bench C2)")
     ap.add_argument("--layout", default=None, help="MP,EP,ESP (default: bench layout)")
+    ap.add_argument("--transport", choices=("peer", "nccl"), default="peer")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -52,7 +53,7 @@ def main():
         layout = ParallelLayout(mp, ep, esp, args.gpus)
     else:
         layout = bench.layout_for(args.gpus)
-    peer = os.environ.get("PARM_PEER", "1") != "0"
+    peer = args.transport == "peer"
     w = ((PeerWorld if peer else NcclWorld)(layout, dev)) if world > 1 else LocalWorld(layout, dev)
     layer = MoELayer(cfg, layout, w)
     layer.init_random(0)
