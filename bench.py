@@ -658,6 +658,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
 
 
 def main():
+    # the one stdout line is the JSON result: NCCL's own log lines (e.g. "NCCL version ...",
+    # printed when NCCL_DEBUG is set in the environment) go to stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

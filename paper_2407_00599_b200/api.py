@@ -24,7 +24,7 @@ import torch
 from . import kernels as K
 from .config import ClusterSpec, MoEConfig, ParallelLayout, check_compatible, derive_capacity
 from .runtime import SCHEDULES, MoELayer
-from .trace import CommTrace, schedule_ffn_rows, schedule_trace
+from .trace import CommTrace, schedule_ffn_rows
 from .world import LocalWorld, make_world
 
 
@@ -236,8 +236,8 @@ def run_schedule(schedule: str, cfg: MoEConfig, layout: ParallelLayout, cluster:
         dropped = {tuple(x) for s in allsets for x in s}
     # S1 keeps one (slice-local) drop set per MP rank; all ranks of a group agree
     # on baseline/s2, so the union equals the reference's per-group record.
-    return ScheduleResult(outputs, schedule_trace(schedule, cfg, layout), dropped,
-                          schedule_ffn_rows(schedule, cfg, layout))
+    # the trace is the one the executed exchanges emitted (MoELayer.last_trace)
+    return ScheduleResult(outputs, lay.last_trace, dropped, schedule_ffn_rows(schedule, cfg, layout))
 
 
 def max_rel_error(outputs, reference) -> float:

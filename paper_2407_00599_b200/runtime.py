@@ -47,6 +47,7 @@ import torch
 
 from . import kernels as K
 from .config import MoEConfig, ParallelLayout, check_compatible, derive_capacity, group_members
+from .trace import CommTrace, rec_allgather, rec_allreduce, rec_alltoall, rec_dump, rec_split
 from .world import Msg, World, make_world
 
 SCHEDULES = ("baseline", "s1", "s2")
@@ -202,6 +203,8 @@ class MoELayer:
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
         self._last: str | None = None
         self._ws_gate = None
+        self._trace: CommTrace | None = None
+        self.last_trace: CommTrace | None = None      # records of the last forward's exchanges
 
     # ------------------------------------------------------------ weights
     def local_experts(self, rank: int) -> range:
@@ -435,13 +438,39 @@ class MoELayer:
                           stride_p=c * blk, stride_slo=d.Mp)
 
     # ------------------------------------------------------------ public API
+    # ------------------------------------------------------------ communication trace
+    # Each exchange the executors run appends the reference's record for it (collectives.py
+    # :131-139 semantics: elements = gathered length for allgather, per-rank buffer otherwise,
+    # unpadded embed), its sizes taken from the buffers / message plan actually used -- so a
+    # change of the message plan shows up in ``last_trace``.  NVTX ranges name every step.
+    def _unpad(self, elems: int) -> int:
+        return elems * self.d.M // self.d.Mp
+
+    def _emit(self, rec) -> None:
+        if self._trace is not None:
+            self._trace.add(rec)
+
+    def _sent(self, msgs: list[Msg]) -> int:
+        """bf16 elements the first hosted rank sends in a message plan (unpadded embed)."""
+        r0 = self.ranks[0]
+        return self._unpad(sum(m.send.numel() for m in msgs
+                               if m.src == r0 and m.send is not None and m.send.dtype == torch.bfloat16))
+
+    @staticmethod
+    def _nvtx(name: str):
+        return torch.cuda.nvtx.range(f"parm.{name}")
+
     def forward(self, schedule: str, xs: dict) -> dict:
         if schedule not in SCHEDULES:
             raise ValueError(f"unknown schedule {schedule!r}")
-        if self.d.P == 1:
-            return self._fwd_local(schedule, xs)
-        fn = {"baseline": self._fwd_baseline, "s1": self._fwd_s1, "s2": self._fwd_s2}[schedule]
-        return fn(xs)
+        self._trace = CommTrace()
+        with self._nvtx(f"{schedule}.fwd"):
+            if self.d.P == 1:
+                out = self._fwd_local(schedule, xs)
+            else:
+                out = {"baseline": self._fwd_baseline, "s1": self._fwd_s1, "s2": self._fwd_s2}[schedule](xs)
+        self.last_trace, self._trace = self._trace, None
+        return out
 
     def backward(self, douts: dict) -> dict:
         if self._last is None:
@@ -449,7 +478,8 @@ class MoELayer:
         if self.d.P == 1:
             return self._bwd_local(douts)
         fn = {"baseline": self._bwd_baseline, "s1": self._bwd_s1, "s2": self._bwd_s2}[self._last]
-        return fn(douts)
+        with self._nvtx(f"{self._last}.bwd"):
+            return fn(douts)
 
     def capture_step(self, schedule: str, xs: dict, douts: dict, warmup: int = 2) -> StepGraph:
         """Record one forward+backward of ``schedule`` (every kernel and every
@@ -492,8 +522,30 @@ class MoELayer:
             self._ffn_fwd(s, b)
             K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w, b["out"])
             outs[r] = b["out"][:, :d.M]
+        self._emit_local(schedule, self.st[self.ranks[0]].bufs["_local"])
         self._last = schedule
         return outs
+
+    def _emit_local(self, schedule: str, b: dict) -> None:
+        """P = 1: every exchange is the identity; the records (zero wire) keep the schedule's shape."""
+        x, send = self._unpad(b["xin"].numel()), self._unpad(b["send"].numel())
+        if schedule == "baseline":
+            self._emit(rec_allgather("esp", 1, x))
+            self._emit(rec_alltoall("ep", 1, send))
+            self._emit(rec_allreduce("esp", 1, send))
+            self._emit(rec_alltoall("ep", 1, send))
+            self._emit(rec_split("esp", 1, send))
+            return
+        self._emit(rec_split("mp", 1, x if schedule == "s1" else send))
+        self._emit(rec_dump(1, send))
+        self._emit(rec_alltoall("ep_esp", 1, send))
+        self._emit(rec_alltoall("ep_esp", 1, send))
+        if schedule == "s2":
+            self._trace.retag_overlapped(1, 1)
+            self._emit(rec_allgather("mp", 1, send))
+            self._trace.retag_overlapped(1, 1)
+        else:
+            self._emit(rec_allgather("mp", 1, x))
 
     def _bwd_local(self, douts: dict) -> dict:
         d = self.d
@@ -542,6 +594,13 @@ class MoELayer:
     def _fwd_s1_peer(self, xs: dict) -> dict:
         d, L = self.d, self.layout
         sl, el = d.n // d.MP, d.e_local
+        b0 = self._plan("s1", self.ranks[0])
+        self._emit(rec_split("mp", d.MP, d.n * d.M))
+        buf = d.E * b0["q"] * d.M                      # the dump-source slot tensor each rank dispatches
+        self._emit(rec_dump(d.ESP, buf))
+        self._emit(rec_alltoall("ep_esp", d.P, buf * d.ESP))   # rows stored into the N_ESP holders
+        self._emit(rec_alltoall("ep_esp", d.P, self._unpad(b0["y"].numel())))   # epilogue / push return
+        self._emit(rec_allgather("mp", d.MP, sl * d.M))         # combine's fan-out to the MP peers
         for r in self.ranks:
             s, b = self.st[r], self._plan("s1", r)
             x = self._input(b, xs[r], "x")
@@ -623,10 +682,17 @@ class MoELayer:
             b["xslice"] = xs_
             rt = b["route"]
             rt.run(xs_, s.gate, d.k, out=b["send"])
-        self.world.exchange(self._fused_msgs("s1", "send", "recv", with_fill=True))
+        self._emit(rec_split("mp", d.MP, xs[self.ranks[0]].numel()))
+        msgs = self._fused_msgs("s1", "send", "recv", with_fill=True)
+        sent = self._sent(msgs)                         # the dumped buffer posted to every destination
+        self._emit(rec_dump(d.ESP, sent // d.ESP))
+        self._emit(rec_alltoall("ep_esp", d.P, sent))
+        self.world.exchange(msgs)
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s1"])
-        self.world.exchange(self._return_msgs("s1", "y", "ret"))
+        msgs = self._return_msgs("s1", "y", "ret")
+        self._emit(rec_alltoall("ep_esp", d.P, self._sent(msgs)))
+        self.world.exchange(msgs)
         ins, outs = {}, {}
         for r in self.ranks:
             b = self.st[r].bufs["s1"]
@@ -635,6 +701,7 @@ class MoELayer:
             K.combine_fwd(self._ret_view(b, "ret"), rt.expert_idx, rt.slot_idx, rt.combine_w,
                           b["out"][m * sl:(m + 1) * sl])
             ins[r], outs[r] = b["out"][m * sl:(m + 1) * sl], b["out"]
+        self._emit(rec_allgather("mp", d.MP, self._unpad(ins[self.ranks[0]].numel())))
         self.world.allgather("mp", ins, outs)
         self._last = "s1"
         return {r: self.st[r].bufs["s1"]["out"][:, :d.M] for r in self.ranks}
@@ -696,6 +763,11 @@ class MoELayer:
         d, L = self.d, self.layout
         el = d.e_local
         msgs = self._return_msgs("s2", src_key, ret_key)
+        if self._trace is not None:       # forward: the SAA pair, both overlapped over P phases
+            self._emit(rec_alltoall("ep_esp", d.P, self._sent(msgs)))
+            self._trace.retag_overlapped(1, d.P)
+            self._emit(rec_allgather("mp", d.MP, self._unpad(self.st[self.ranks[0]].bufs["s2"][comb_key].numel())))
+            self._trace.retag_overlapped(1, d.P)
         if not self.saa_phased:
             self.world.exchange(msgs)
             ins, outs = {}, {}
@@ -757,6 +829,15 @@ class MoELayer:
     def _fwd_s2_peer(self, xs: dict) -> dict:
         d, L = self.d, self.layout
         el = d.e_local
+        b0 = self._plan("s2", self.ranks[0])
+        buf = d.E * b0["q"] * d.M                      # this rank's slot shard [m q, (m + 1) q)
+        self._emit(rec_split("mp", d.MP, buf * d.MP))
+        self._emit(rec_dump(d.ESP, buf))
+        self._emit(rec_alltoall("ep_esp", d.P, buf * d.ESP))
+        self._emit(rec_alltoall("ep_esp", d.P, self._unpad(b0["y"].numel())))   # combine gathers from holders
+        self._trace.retag_overlapped(1, d.P)
+        self._emit(rec_allgather("mp", d.MP, buf))                              # ... of every MP shard
+        self._trace.retag_overlapped(1, d.P)
         for r in self.ranks:
             s, b = self.st[r], self._plan("s2", r)
             x = self._input(b, xs[r], "x")
@@ -817,7 +898,13 @@ class MoELayer:
             if "shard_fill" not in b:
                 b["shard_fill"] = torch.zeros(d.E, dtype=torch.int32, device=self.dev)
             rt.run(x, s.gate, d.k, out=b["send"], slot_lo=L.mp_pos(r) * b["q"], fill_fan=[b["shard_fill"].data_ptr()])
-        self.world.exchange(self._fused_msgs("s2", "send", "recv", with_fill=True, fill_key="shard_fill"))
+        b0 = self.st[self.ranks[0]].bufs["s2"]
+        self._emit(rec_split("mp", d.MP, self._unpad(b0["send"].numel()) * d.MP))
+        msgs = self._fused_msgs("s2", "send", "recv", with_fill=True, fill_key="shard_fill")
+        sent = self._sent(msgs)
+        self._emit(rec_dump(d.ESP, sent // d.ESP))
+        self._emit(rec_alltoall("ep_esp", d.P, sent))
+        self.world.exchange(msgs)
         for r in self.ranks:
             self._ffn_fwd(self.st[r], self.st[r].bufs["s2"])
         self._saa("y", "ret", "comb", "gath")
@@ -868,20 +955,27 @@ class MoELayer:
             b["xin"] = x
             b["route"].run(x, s.gate, d.k)                         # routing of the own block (slot pass only)
             ins[r], outs[r] = x, b["xg"]
+        self._emit(rec_allgather("esp", d.ESP, self._unpad(ins[self.ranks[0]].numel())))
         self.world.allgather("esp", ins, outs)                   # ESP-AllGather of raw tokens
         for r in self.ranks:
             s, b = self.st[r], self.st[r].bufs["baseline"]
             for q in range(d.ESP):                               # re-gate every gathered block
                 rt = b["route_blk"][q]
                 rt.run(b["xg"][q], s.gate, d.k, out=b["disp"][q])
-        self.world.exchange(self._ep_dispatch_msgs("disp", "recv", with_fill=True))
+        msgs = self._ep_dispatch_msgs("disp", "recv", with_fill=True)
+        self._emit(rec_alltoall("ep", d.EP, self._sent(msgs)))
+        self.world.exchange(msgs)
         ys = {}
         for r in self.ranks:
             b = self.st[r].bufs["baseline"]
             self._ffn_fwd(self.st[r], b)
             ys[r] = b["y"]
+        self._emit(rec_allreduce("esp", d.ESP, self._unpad(ys[self.ranks[0]].numel())))
         self.world.allreduce("esp", ys)                          # ESP-AllReduce of shard partials
-        self.world.exchange(self._ep_return_msgs("y", "ret"))
+        msgs = self._ep_return_msgs("y", "ret")
+        self._emit(rec_alltoall("ep", d.EP, self._sent(msgs)))
+        self.world.exchange(msgs)
+        self._emit(rec_split("esp", d.ESP, self._unpad(ys[self.ranks[0]].numel())))   # own slot range kept
         for r in self.ranks:
             b = self.st[r].bufs["baseline"]
             rt = b["route"]

@@ -3,9 +3,11 @@
 ``elements`` is the cost-model argument: the gathered length for allgather,
 the per-rank buffer length otherwise.  ``wire_per_rank`` counts elements that
 actually cross links per rank: AG n(G-1), A2A/RS n(G-1)/G, AR 2n(G-1)/G,
-split/dump 0.  The B200 executors emit the same records the reference's
-simulated collectives do, computed from shapes (see ``schedule_trace``), so
-trace-structure tests written against ``moesched`` apply unchanged.
+split/dump 0.  The B200 executors (runtime.MoELayer) append these records as
+they run each exchange, sized from the message plans and buffers actually used
+(``MoELayer.last_trace``, returned by ``api.run_schedule``); ``schedule_trace``
+is the analytic expectation of the same sequence, so trace-structure tests
+written against ``moesched`` apply to both.
 """
 
 from __future__ import annotations

@@ -455,3 +455,30 @@ def test_gate_wgrad_matches_f64(cuda_lib, n, M, E):
     assert torch.equal(out, again)
     K.gate_wgrad(x, dlt, again, ws, accumulate=True)
     torch.testing.assert_close(again, 2 * out, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("world", ["local", "peer"])
+def test_emitted_trace_equals_reference_trace(cuda_lib, golden, world):
+    """The CommTrace records the executors emit while running each exchange (sized from the
+    message plans / buffers actually used) equal the reference's recorded traces, on the copy
+    transport and on the NVLink peer transport, for every golden world."""
+    from paper_2407_00599_b200.config import MoEConfig, ParallelLayout
+    from paper_2407_00599_b200.runtime import MoELayer
+    from paper_2407_00599_b200.world import LocalWorld, PeerLocalWorld
+
+    meta, _ = golden
+    for case in meta["schedules"]:
+        cfg = MoEConfig(*case["cfg"])
+        layout = ParallelLayout(*case["layout"], esp_contiguous=case["esp_contiguous"])
+        if world == "peer" and layout.world_size > 8:
+            continue
+        W = PeerLocalWorld(layout) if world == "peer" else LocalWorld(layout)
+        layer = MoELayer(cfg, layout, W)
+        layer.init_random(0)
+        x = {r: torch.randn(cfg.tokens_per_rank, cfg.embed_dim, device="cuda").to(torch.bfloat16)
+             for r in layer.ranks}
+        for s, rec in case["results"].items():
+            layer.forward(s, x)
+            got = [[r.collective, r.group, r.group_size, r.elements, r.wire_per_rank, r.phases, r.overlapped]
+                   for r in layer.last_trace]
+            assert got == rec["trace"], f"{case['name']} {s} {world}"

@@ -96,6 +96,10 @@ def main() -> int:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--schedule", choices=("s1", "s2", "baseline"), default="s1",
+                    help="MoE-layer schedule (baseline = the DeepSpeed-MoE ordering on NCCL collectives)")
+    ap.add_argument("--transport", choices=("peer", "nccl"), default="peer",
+                    help="multi-GPU S1/S2 exchanges: NVLink peer memory or NCCL collectives")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
@@ -119,15 +123,16 @@ def main() -> int:
     torch.manual_seed(1234 + rank // layout.mp_size)    # MP ranks hold identical dense replicas and tokens
     mk_world = None
     if world > 1:
-        from paper_2407_00599_b200.world import PeerWorld
+        from paper_2407_00599_b200.world import NcclWorld, PeerWorld
 
-        mk_world = PeerWorld(layout, dev)
+        mk_world = PeerWorld(layout, dev) if args.transport == "peer" else NcclWorld(layout, dev)
     blocks = []
     for i in range(args.layers):
         moe = None
         if i % 2 == 1:
             if args.moe == "parm":
-                moe = ParmMoE(cfg, layout, mk_world if world > 1 else LocalWorld(layout, dev), schedule="s1", seed=i)
+                moe = ParmMoE(cfg, layout, mk_world if world > 1 else LocalWorld(layout, dev), schedule=args.schedule,
+                              seed=i)
             else:
                 moe = TorchMoE(M, H, E, k, f, n).to(dev)
         blocks.append(Block(M, heads, H, moe, causal=args.model == "gpt2").to(dev))
@@ -178,7 +183,8 @@ def main() -> int:
     if rank == 0:
         name = {"bert": "BERT-large-MoE", "gpt2": "GPT-2-MoE"}[args.model]
         print(json.dumps({"model": f"{name} ({args.layers} blocks, MoE every other FFN, E={E} top-2 f=1.2)",
-                          "moe_impl": args.moe, "n_gpus": world,
+                          "moe_impl": args.moe, "schedule": args.schedule if args.moe == "parm" else None,
+                          "transport": args.transport if world > 1 else "local", "n_gpus": world,
                           "layout": f"MP={layout.mp_size} EP={layout.ep_size} ESP={layout.esp_size}",
                           "tokens_per_step": toks, "ms_per_step": ms, "tokens_per_s": toks / ms * 1e3,
                           "wall_ms_per_step": (time.perf_counter() - t0) / args.steps * 1e3, "loss": float(loss),
