@@ -169,6 +169,10 @@ int parm_peer_barrier(const parm_peer_signal* sigs, int count, void* stream);
 /* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic two-pass).
  * accumulate != 0 adds into dwg. */
 size_t parm_gate_wgrad_workspace(int n, int M, int E);
+/* out[i] (+)= sum_c src[c * len + i], chunks summed in a fixed order (deterministic): the S1
+ * peer transport's MP gate-gradient partials, fanned out to every MP peer, reduced locally
+ * (replaces the MP all-reduce of the gate gradient). */
+int parm_sum_chunks(const float* src, int chunks, long long len, float* out, int accumulate, void* stream);
 int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, void* workspace,
                     size_t workspace_bytes, float* dwg_t, int accumulate, void* stream);
 

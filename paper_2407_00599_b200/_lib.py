@@ -82,6 +82,7 @@ SIGNATURES = {
     "parm_esp_sum": (_c_int, [ctypes.POINTER(SlotViewC), _c_int, _c_int, _c_int, _vp, _vp]),
     "parm_gate_wgrad_workspace": (_size, [_c_int, _c_int, _c_int]),
     "parm_gate_wgrad": (_c_int, [_vp, _c_ll, _vp, _c_int, _c_int, _c_int, _vp, _size, _vp, _c_int, _vp]),
+    "parm_sum_chunks": (_c_int, [_vp, _c_int, _c_ll, _vp, _c_int, _vp]),
     "parm_gemm": (_c_int, [ctypes.POINTER(GemmDescC), _vp]),
     "parm_combine_fwd_fan": (_c_int, [ctypes.POINTER(SlotViewC), _vp, _vp, _vp, _c_int, _c_int, _c_int,
                                       ctypes.POINTER(RowFanC), _c_ll, _vp]),

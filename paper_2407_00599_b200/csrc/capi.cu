@@ -23,6 +23,7 @@ size_t gate_counts_bytes(int, int);
 int route_dispatch(const void*, long long, const int*, const int*, int, int, int, int, int, int*, int*, int*, int, int,
                    void*, long long, long long, const SlotView*, const IntFan*, cudaStream_t);
 size_t gate_wgrad_workspace(int, int, int);
+int sum_chunks(const float*, int, long long, float*, int, cudaStream_t);
 int gate_wgrad(const void*, long long, const float*, int, int, int, float*, size_t, float*, int, cudaStream_t);
 int combine_fwd(const SlotView&, const int*, const int*, const float*, int, int, int, void*, long long, cudaStream_t);
 int dispatch_bwd(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int, void*,
@@ -131,6 +132,10 @@ int parm_esp_sum(const parm_slot_view* y, int E, int slots, int M, void* out, vo
 }
 
 size_t parm_gate_wgrad_workspace(int n, int M, int E) { return parm::gate_wgrad_workspace(n, M, E); }
+
+int parm_sum_chunks(const float* src, int chunks, long long len, float* out, int accumulate, void* stream) {
+    return parm::sum_chunks(src, chunks, len, out, accumulate, S(stream));
+}
 
 int parm_gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, void* workspace,
                     size_t workspace_bytes, float* dwg, int accumulate, void* stream) {

@@ -707,6 +707,14 @@ size_t gate_wgrad_workspace(int n, int M, int E) {
     return (size_t)gate_wgrad_grid(n) * M * E * sizeof(float);
 }
 
+int sum_chunks(const float* src, int chunks, long long len, float* out, int accumulate, cudaStream_t s) {
+    PARM_CHECK_ARG(src != nullptr && out != nullptr && chunks >= 1 && len >= 0, "sum_chunks: bad arguments");
+    if (len == 0) return 0;
+    launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, src, chunks, len, out, accumulate);
+    PARM_CHECK_LAUNCH("sum_chunks");
+    return 0;
+}
+
 int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, float* ws, size_t ws_bytes,
                float* dwgT, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(E <= 32, "gate_wgrad: at most 32 experts supported");

@@ -243,6 +243,16 @@ def esp_sum(view: SlotView, out: torch.Tensor) -> None:
     _lib.call("parm_esp_sum", ctypes.byref(v), E, S, M, out.data_ptr(), _stream())
 
 
+def sum_chunks(src: torch.Tensor, out: torch.Tensor, accumulate: bool = False) -> None:
+    """out (+)= src.sum(0) for a contiguous f32 (chunks, ...) tensor, in a fixed chunk order."""
+    _need(src, torch.float32, "chunks")
+    _need(out, torch.float32, "out")
+    if not (src.is_contiguous() and out.is_contiguous()) or src[0].numel() != out.numel():
+        raise ValueError("sum_chunks: contiguous (chunks, ...) source and an output of one chunk's size")
+    _lib.call("parm_sum_chunks", src.data_ptr(), src.shape[0], out.numel(), out.data_ptr(), int(accumulate),
+              _stream())
+
+
 def gate_wgrad_workspace(n: int, M: int, E: int) -> int:
     return int(_lib.load().parm_gate_wgrad_workspace(n, M, E))
 

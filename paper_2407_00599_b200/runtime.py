@@ -665,7 +665,7 @@ class MoELayer:
         if d.MP > 1:
             for r in self.ranks:                                         # fixed-order sum: identical on the group
                 s, b = self.st[r], self.st[r].bufs["s1"]
-                torch.sum(b["gsum"], dim=0, out=s.dgate)
+                K.sum_chunks(b["gsum"], s.dgate)
         return {r: self.st[r].bufs["s1"]["dx"][:, :d.M] for r in self.ranks}
 
     # ------------------------------------------------------------ S1
