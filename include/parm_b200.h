@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define PARM_ABI_VERSION 14
+#define PARM_ABI_VERSION 15
 
 /* Addressing of a slot tensor split over expert-parallel blocks, expert-
  * sharding partials (summed in p order) and MP slot shards:
@@ -227,6 +227,26 @@ int parm_gemm(const parm_gemm_desc* desc, void* stream);
  * return AlltoAll (collectives.py:286-295) fused into the GEMM, tile by tile. */
 int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld,
                    void* stream);
+
+/* Several GEMMs (1..4) as ONE persistent launch over a shared work queue of pair tiles: a CTA
+ * pair claims its next tile from a device counter, so one GEMM's partial last wave is filled by
+ * the next GEMM's tiles (the expert FFN's forward pair Y = relu(R W1) W2, or its backward
+ * dH, dW2, dR, dW1 -- dataplane.py:122-128 and the adjoints).  deps (nullable): 2 ints per
+ * problem, (kind, earlier problem):
+ *   PARM_DEP_ROW_PAIR   ROW problem reads rows of the same 256-row pair of the earlier ROW
+ *                       problem's output over all its columns (waits for that pair's tiles);
+ *   PARM_DEP_COL_BLOCK  WGT problem reads columns [256 p, 256 p + 256) of the earlier ROW
+ *                       problem's output for every row of its group (p = its 256-row block).
+ * Dependent and depended-on problems must share groups, segments, seg_len and fill.
+ * ws: parm_gemm_multi_workspace() bytes, zeroed once by the caller; the kernel leaves it zeroed
+ * (launches sharing a workspace must be stream-ordered).  seg_prob (-1: none): that problem's
+ * outputs go to seg_dst as in parm_gemm_peer. */
+#define PARM_DEP_NONE 0
+#define PARM_DEP_ROW_PAIR 1
+#define PARM_DEP_COL_BLOCK 2
+size_t parm_gemm_multi_workspace(const parm_gemm_desc* descs, int count);
+int parm_gemm_multi(const parm_gemm_desc* descs, int count, const int* deps, void* ws, size_t ws_bytes, int seg_prob,
+                    const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld, void* stream);
 
 #ifdef __cplusplus
 }

@@ -92,9 +92,12 @@ SIGNATURES = {
     "parm_push_rows": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, ctypes.POINTER(RowFanC), _vp]),
     "parm_fan_copy": (_c_int, [_vp, _c_ll, ctypes.POINTER(RowFanC), _vp]),
     "parm_gemm_peer": (_c_int, [ctypes.POINTER(GemmDescC), ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
+    "parm_gemm_multi_workspace": (ctypes.c_size_t, [ctypes.POINTER(GemmDescC), _c_int]),
+    "parm_gemm_multi": (_c_int, [ctypes.POINTER(GemmDescC), _c_int, ctypes.POINTER(_c_int), _vp, ctypes.c_size_t,
+                                 _c_int, ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 14
+ABI_VERSION = 15
 
 
 class ParmError(RuntimeError):

@@ -34,6 +34,9 @@ int combine_bwd_dispatch(const void*, long long, const SlotView&, const int*, co
 int esp_sum(const SlotView&, int, int, int, void*, cudaStream_t);
 int moe_gemm(const parm_gemm_desc&, cudaStream_t);
 int moe_gemm_peer(const parm_gemm_desc&, const RowFan*, long long, long long, cudaStream_t);
+size_t moe_gemm_multi_workspace(const parm_gemm_desc*, int);
+int moe_gemm_multi(const parm_gemm_desc*, int, const int*, void*, size_t, int, const RowFan*, long long, long long,
+                   cudaStream_t);
 int combine_fwd_fan(const SlotView&, const int*, const int*, const float*, int, int, int, const RowFan&, long long,
                     cudaStream_t);
 int dispatch_bwd_fan(const SlotView&, const int*, const int*, const float*, const void*, int, int, int, int,
@@ -208,6 +211,29 @@ int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long
     }
     const parm::RowFan fan = parm::abi_cast<parm::RowFan>(seg_dst);
     return parm::moe_gemm_peer(*desc, &fan, dst_g_stride, dst_ld, S(stream));
+}
+
+size_t parm_gemm_multi_workspace(const parm_gemm_desc* descs, int count) {
+    if (!descs || count < 1) return 0;
+    return parm::moe_gemm_multi_workspace(descs, count);
+}
+
+int parm_gemm_multi(const parm_gemm_desc* descs, int count, const int* deps, void* ws, size_t ws_bytes, int seg_prob,
+                    const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld, void* stream) {
+    if (!descs) {
+        parm::set_error("gemm_multi: null descriptors");
+        return 1;
+    }
+    parm::RowFan fan{};
+    if (seg_prob >= 0) {
+        if (!seg_dst) {
+            parm::set_error("gemm_multi: peer-output problem %d without a destination fan", seg_prob);
+            return 1;
+        }
+        fan = parm::abi_cast<parm::RowFan>(seg_dst);
+    }
+    return parm::moe_gemm_multi(descs, count, deps, ws, ws_bytes, seg_prob, seg_prob >= 0 ? &fan : nullptr,
+                                dst_g_stride, dst_ld, S(stream));
 }
 
 }  // extern "C"

@@ -138,100 +138,281 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
     }
 }
 
-// ------------------------------------------------------------------ FP64 tensor-core gate
-// mma.m8n8k4.f64 (DMMA): one instruction = 8 tokens x 8 experts x 4 columns of
-// exact-product f64 FMAs.  Lane (g, q) = (lane / 4, lane % 4) supplies A[g][q] =
-// x[token g][c_q] and B[q][g] = Wg[expert g][c_q]: the k index is the quad lane,
-// mapped to a lane-dependent column (the same mapping for A and B, which is all a
-// dot product needs).  Step u of 32-column group j uses column c_q = 32j + 8q + u,
-// so a lane's 8 consecutive bf16 of x are one 16-byte shared-memory load.
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
+// ------------------------------------------------------------------ tensor-core gate
+// Logits on the tensor cores with a certified error bound (the "fp32 + tie audit" gate):
+//   * mma.sync m16n8k16 bf16 -> f32: A = Wg^T (16 experts x 16 columns, from shared memory),
+//     B = x^T (16 columns x 8 tokens, straight from HBM), D = 16 experts x 8 tokens.  Every
+//     bf16 x bf16 product is exact; the tensor core sums a 32-column chunk (two chained MMAs
+//     from a zero accumulator) in f32, and the chunk sums are added in f64.
+//   * A second MMA pair over |Wg| and |x| gives S = sum_i |x_i w_ie| per (token, expert), so
+//     |logit_gpu - logit_exact| <= kGateEps * S (kGateEps = 2^-17 bounds the f32 rounding of a
+//     32-product chunk, 64x the one-ulp error; tools/probes/gate_err_probe.py measures the
+//     observed ratio on adversarial data).
+//   * Audit: a token whose picks are not separated from each other or from the best unpicked
+//     expert by more than the two bounds is recomputed exactly in f64 (bf16 products exact,
+//     fixed summation order -- the same semantics as the oracle's f64 dot products, so exact
+//     ties still go to the lower expert), then ranked again.  Every other token's ranking is
+//     certified equal to the exact one, hence to the oracle's argsort of f64 scores.
+//   * k-index permutation: lane (g, q) loads 8 consecutive bf16 (one 16-byte load) of
+//     x row g and of Wg^T rows g, g + 8 at column 32j + 8q; the first MMA takes words 0-1
+//     (logical k = 2q, 2q+1, 2q+8, 2q+9), the second words 2-3.  A dot product only needs the
+//     same permutation on both operands.
+// Scores (softmax in f64 of these logits) differ from the oracle's by the logit error, ~1e-7
+// relative for typical inputs.
+constexpr double kGateEps = 1.0 / 131072.0;   // 2^-17
+constexpr int kGmRJ = 16;                     // 32-column groups per load round (16 x 16-B loads in flight / lane)
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Softmax + stable top-k of one token's logits held by a lane quad: lane
-// (g, q) owns experts nt * 8 + 2q + h of token t (the DMMA C-fragment layout).
-// Returns, per owned expert, whether it is one of the token's k picks.
-template <int NT>
-__device__ __forceinline__ void gate_topk_epilogue(double (&lg)[NT][2], int g, int q, int t, bool tok, int E, int k,
-                                                   int* __restrict__ expert_idx, float* __restrict__ combine_w,
-                                                   float* __restrict__ probs, bool (&pick)[NT][2]) {
-    double sc[NT][2];
+// Per-warp epilogue scratch: logits, scores (f64) and bounds (f32) of the warp's 8 tokens.
+template <int NM>
+struct GateScratch {
+    double lg[8][16 * NM];
+    double sc[8][16 * NM];
+    float bd[8][16 * NM];
+};
+
+// Softmax + stable top-k of the 8 tokens in sc: lane (t = lane / 4, r = lane % 4) owns experts
+// r, r + 4, ...  Returns (audit) the mask of tokens whose ranking the bounds do not certify.
+template <int NM>
+__device__ __forceinline__ unsigned gate_rank(GateScratch<NM>& s, int lane, int E, int k, bool audit,
+                                              int (&rank)[4 * NM]) {
+    constexpr int EP = 16 * NM, U = EP / 4;
+    const int t = lane >> 2, r = lane & 3;
+    double ex[U];
     double mx = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            sc[nt][h] = lg[nt][h];
-            if (nt * 8 + 2 * q + h < E) mx = fmax(mx, sc[nt][h]);
-        }
+    for (int u = 0; u < U; ++u)
+        if (r + 4 * u < E) mx = fmax(mx, s.lg[t][r + 4 * u]);
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     double sum = 0.0;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            sc[nt][h] = (nt * 8 + 2 * q + h < E) ? exp(sc[nt][h] - mx) : 0.0;
-            sum += sc[nt][h];
-        }
+    for (int u = 0; u < U; ++u) {
+        ex[u] = (r + 4 * u < E) ? exp(s.lg[t][r + 4 * u] - mx) : 0.0;
+        sum += ex[u];
+    }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    int rank[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int u = 0; u < U; ++u)
+        if (r + 4 * u < E) s.sc[t][r + 4 * u] = ex[u] / sum;
+    __syncwarp();
+    bool unsure = false;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            sc[nt][h] = sc[nt][h] / sum;
-            rank[nt][h] = 0;
+    for (int u = 0; u < U; ++u) {
+        const int e = r + 4 * u;
+        rank[u] = EP;
+        if (e >= E) continue;
+        const double se = s.sc[t][e];
+        int rk = 0;
+        for (int e2 = 0; e2 < E; ++e2) {
+            const double so = s.sc[t][e2];
+            rk += (so > se) || (so == se && e2 < e);
+        }
+        rank[u] = rk;
+        if (audit && rk < k) {   // a pick must be separated from every other expert by the two bounds
+            const double le = s.lg[t][e], be = (double)s.bd[t][e];
+            for (int e2 = 0; e2 < E; ++e2)   // (equal scores: decided by the exact path too)
+                unsure |= e2 != e && (fabs(le - s.lg[t][e2]) <= be + (double)s.bd[t][e2] || s.sc[t][e2] == se);
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, unsure);
+    unsigned tokens = 0;
+#pragma unroll
+    for (int tt = 0; tt < 8; ++tt) tokens |= ((b >> (4 * tt)) & 0xFu) ? (1u << tt) : 0u;
+    return tokens;
+}
+
+template <int NM>
+__global__ void __launch_bounds__(256) gate_fwd_mma_kernel(const bf16* __restrict__ x, long long ldx,
+                                                           const bf16* __restrict__ wg, int n, int M, int E, int k,
+                                                           int* __restrict__ expert_idx, float* __restrict__ combine_w,
+                                                           float* __restrict__ probs, int* __restrict__ counts) {
+    constexpr int EP = 16 * NM, U = EP / 4;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int rowb = 2 * M + 64;   // staged Wg^T row: 64-byte pad spreads the 8 g-rows over all banks
+    const int wpc = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, q = lane & 3;
+    const size_t absoff = (size_t)EP * rowb;   // |Wg^T| rows follow the Wg^T rows
+    GateScratch<NM>& s = reinterpret_cast<GateScratch<NM>*>(smem + 2 * absoff)[warp];
+    const int tiles = (n + 7) / 8;
+    const int nj = M / 32;
+    const int rounds = (nj + kGmRJ - 1) / kGmRJ;
+    int tile = blockIdx.x * wpc + warp;
+    const int stride = gridDim.x * wpc;
+
+    // x loads are unconditional (rows clamped to n - 1, groups to nj - 1; the extra rows and groups
+    // are never used), so no select waits on a load right after it is issued
+    int4 bufA[kGmRJ], bufB[kGmRJ];
+    auto load_round = [&](int4 (&dst)[kGmRJ], int tl, int rd) {
+        const bf16* src = x + (long long)min(tl * 8 + g, n - 1) * ldx + 8 * q;
+#pragma unroll
+        for (int jj = 0; jj < kGmRJ; ++jj)
+            dst[jj] = __ldg(reinterpret_cast<const int4*>(src + 32 * min(rd * kGmRJ + jj, nj - 1)));
+    };
+    if (tile < tiles) load_round(bufA, tile, 0);   // first x loads in flight before the Wg staging barrier
+
+    // Wg^T (E, M) -> shared rows 0..EP-1 (rows >= E zero), and |Wg^T| at absoff (the bound's operand),
+    // eight 16-byte loads in flight per thread
+    constexpr int kU = 8;
+    const int c8n = M / 8;
+    const int units = EP * c8n;
+    for (int u0 = 0; u0 < units; u0 += kU * blockDim.x) {
+        int4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = u0 + u * blockDim.x + threadIdx.x;
+            const int e = i / c8n;
+            v[u] = (i < units && e < E) ? __ldg(reinterpret_cast<const int4*>(wg) + i) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq)
+        for (int u = 0; u < kU; ++u) {
+            const int i = u0 + u * blockDim.x + threadIdx.x;
+            const int e = i / c8n, c8 = i - e * c8n;
+            if (i < units) {
+                unsigned char* dst = smem + (size_t)e * rowb + c8 * 16;
+                *reinterpret_cast<int4*>(dst) = v[u];
+                *reinterpret_cast<int4*>(dst + absoff) =
+                    make_int4(v[u].x & 0x7FFF7FFF, v[u].y & 0x7FFF7FFF, v[u].z & 0x7FFF7FFF, v[u].w & 0x7FFF7FFF);
+            }
+        }
+    }
+    __syncthreads();
+
+    bool first_tile = true;
+    for (; tile < tiles; tile += stride) {
+        // independent accumulator chains (by j parity) so consecutive groups' MMAs and adds overlap
+        double acc[2][NM][4];
+        float dab[2][NM][4];
 #pragma unroll
-        for (int nt2 = 0; nt2 < NT; ++nt2)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                const double other = __shfl_sync(0xffffffffu, sc[nt2][h2], (g << 2) | qq);
-                const int e2 = nt2 * 8 + 2 * qq + h2;
-                if (e2 >= E) continue;
+            for (int m = 0; m < NM; ++m)
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
+                for (int i = 0; i < 4; ++i) {
+                    acc[c][m][i] = 0.0;
+                    dab[c][m][i] = 0.0f;
+                }
+        auto compute = [&](const int4 (&cur)[kGmRJ], int rd) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = nt * 8 + 2 * q + h;
-                        rank[nt][h] += (other > sc[nt][h]) || (other == sc[nt][h] && e2 < e);
+            for (int jj = 0; jj < kGmRJ; ++jj) {
+                const int j = rd * kGmRJ + jj;
+                if (j >= nj) break;
+                const uint32_t xw[4] = {(uint32_t)cur[jj].x, (uint32_t)cur[jj].y, (uint32_t)cur[jj].z,
+                                        (uint32_t)cur[jj].w};
+                uint32_t xa[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) xa[w] = xw[w] & 0x7FFF7FFFu;
+#pragma unroll
+                for (int m = 0; m < NM; ++m) {
+                    const uint4 wa = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g) * rowb + 64 * j + 16 * q);
+                    const uint4 wb =
+                        *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g + 8) * rowb + 64 * j + 16 * q);
+                    float d[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                    mma_bf16_16816(d, wa.x, wb.x, wa.y, wb.y, xw[0], xw[1]);
+                    mma_bf16_16816(d, wa.z, wb.z, wa.w, wb.w, xw[2], xw[3]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[jj & 1][m][i] += (double)d[i];
+                    const uint4 va = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g) * rowb + 64 * j + 16 * q +
+                                                                     absoff);
+                    const uint4 vb = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g + 8) * rowb + 64 * j +
+                                                                     16 * q + absoff);
+                    mma_bf16_16816(dab[jj & 1][m], va.x, vb.x, va.y, vb.y, xa[0], xa[1]);
+                    mma_bf16_16816(dab[jj & 1][m], va.z, vb.z, va.w, vb.w, xa[2], xa[3]);
+                }
+            }
+        };
+        if (!first_tile) load_round(bufA, tile, 0);
+        first_tile = false;
+        for (int rd = 0; rd < rounds; rd += 2) {   // ping-pong: the next round's loads fly during this one
+            if (rd + 1 < rounds) load_round(bufB, tile, rd + 1);
+            compute(bufA, rd);
+            if (rd + 1 < rounds) {
+                if (rd + 2 < rounds) load_round(bufA, tile, rd + 2);
+                compute(bufB, rd + 1);
+            }
+        }
+        // D fragment: (expert 16m + g + 8 (i >> 1), token 2q + (i & 1))
+#pragma unroll
+        for (int m = 0; m < NM; ++m)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int e = 16 * m + g + 8 * (i >> 1), tl = 2 * q + (i & 1);
+                s.lg[tl][e] = acc[0][m][i] + acc[1][m][i];
+                // the f32 sum S of |products| is itself rounded: 2^-10 covers it many times over
+                s.bd[tl][e] = (float)(kGateEps * ((double)dab[0][m][i] + (double)dab[1][m][i]) * (1.0 + 1.0 / 1024.0));
+            }
+        __syncwarp();
+        int rank[U];
+        unsigned redo = gate_rank<NM>(s, lane, E, k, true, rank);
+        const int t0 = tile * 8;
+        redo &= (n - t0 >= 8) ? 0xFFu : ((1u << (n - t0)) - 1u);
+        if (redo) {   // exact f64 logits of the uncertified tokens (rare): fixed order, lane-0 tree sums
+            for (unsigned rm = redo; rm; rm &= rm - 1) {
+                const int tl = __ffs(rm) - 1;
+                const bf16* xr = x + (long long)(t0 + tl) * ldx;
+                for (int e = 0; e < E; ++e) {
+                    double p = 0.0;
+                    for (int c = 8 * lane; c < M; c += 256) {
+                        const int4 xv = __ldg(reinterpret_cast<const int4*>(xr + c));
+                        const int4 wv = *reinterpret_cast<const int4*>(smem + (size_t)e * rowb + 2 * c);
+                        const uint32_t xs[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+                        const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            p = fma((double)__uint_as_float(xs[w] << 16), (double)__uint_as_float(ws[w] << 16), p);
+                            p = fma((double)__uint_as_float(xs[w] & 0xFFFF0000u),
+                                    (double)__uint_as_float(ws[w] & 0xFFFF0000u), p);
+                        }
                     }
-            }
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = nt * 8 + 2 * q + h;
-            pick[nt][h] = tok && e < E && rank[nt][h] < k;
-            if (!tok || e >= E) continue;
-            if (rank[nt][h] < k) {
-                expert_idx[(long long)t * k + rank[nt][h]] = e;
-                combine_w[(long long)t * k + rank[nt][h]] = (float)sc[nt][h];
+                    for (int o = 16; o >= 1; o >>= 1) p += __shfl_down_sync(0xffffffffu, p, o);
+                    if (lane == 0) s.lg[tl][e] = p;
+                }
             }
-            if (probs) probs[(long long)t * E + e] = (float)sc[nt][h];
+            __syncwarp();
+            gate_rank<NM>(s, lane, E, k, false, rank);
         }
+        // outputs: lane (t, r) owns experts r + 4u of token t0 + t
+        const int t = lane >> 2, r = lane & 3;
+        const bool tok = t0 + t < n;
+        bool pick[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = r + 4 * u;
+            pick[u] = tok && e < E && rank[u] < k;
+            if (!tok || e >= E) continue;
+            const long long tt = t0 + t;
+            const float sc = (float)s.sc[t][e];
+            if (rank[u] < k) {
+                expert_idx[tt * k + rank[u]] = e;
+                combine_w[tt * k + rank[u]] = sc;
+            }
+            if (probs) probs[tt * E + e] = sc;
+        }
+        if (counts != nullptr) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {   // expert rr + 4u: the lanes with r == rr
+                    const unsigned b = __ballot_sync(0xffffffffu, pick[u] && r == rr);
+                    const int e = rr + 4 * u;
+                    if (lane == 0 && e < E) counts[(long long)tile * E + e] = __popc(b);
+                }
+        }
+        __syncwarp();   // scratch reused by the next tile
+    }
 }
 
-__device__ __forceinline__ double bf16_to_f64(uint32_t bits16) { return (double)__uint_as_float(bits16 << 16); }
-
-// Exact f32 -> f64 widening of a bf16-valued f32 bit pattern with integer ops (no F2F on the
-// DMMA operand path): sign | (exponent + 896) << 20 | mantissa << 13 in the high word, low word
-// zero.  Zero keeps its sign; subnormals, infinities and NaNs take the conversion instruction.
-__device__ __forceinline__ double bf16_bits_to_f64(uint32_t f) {
-    const uint32_t mag = f & 0x7FFFFFFFu;
-    const uint32_t ex = mag >> 23;
-    uint32_t hi = (f & 0x80000000u) | (mag ? (mag >> 3) + 0x38000000u : 0u);
-    if (__builtin_expect(ex == 0u && mag != 0u, 0) || __builtin_expect(ex == 0xFFu, 0))
-        return (double)__uint_as_float(f);
-    return __hiloint2double((int)hi, 0);
-}
 
 namespace gring {   // bulk-copy helpers (same protocol as permute.cu's rings)
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -257,198 +438,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 }  // namespace gring
 
-// One CTA per SM (persistent), wpc warps, each walking its own 8-token tiles.
-//   * Wg^T (bf16 (E, M) in global) is converted once per CTA to f64 in shared memory,
-//     lane-major: the double2 of lane l for (group j, n-tile nt, u-pair up) sits at
-//     ((j * NT + nt) * 4 + up) * 32 + l, so every B-fragment load is a conflict-free
-//     contiguous 512-byte warp access and carries two steps' operands.
-//   * x arrives by cp.async.bulk into a per-warp ring of S stages (8 token rows x kGateCC
-//     columns each, rows padded to 576 B so the quad lanes' 16-byte loads hit distinct
-//     banks), issued S-1 items ahead: all of a warp's rows are in flight at once instead
-//     of one dependent round trip per chunk.
-//   * Two independent DMMA accumulator chains per warp (steps u even / odd).
-//   * counts (nullable): per 8-token tile, how many of its tokens picked each expert --
-//     the first pass of the exact slot scan, so the slot kernel needs no count pass.
-constexpr int kGateCC = 256;                        // columns per ring stage
-constexpr int kGateRow = kGateCC * 2 + 64;          // bytes per staged row (bank-spreading pad)
-constexpr int kGateStage = 8 * kGateRow;            // one 8-token stage
-
-template <int NT>
-__global__ void __launch_bounds__(256, 1) gate_fwd_tc_kernel(const bf16* __restrict__ x, long long ldx,
-                                                             const bf16* __restrict__ wg, int n, int M, int E, int k,
-                                                             int S, int* __restrict__ expert_idx,
-                                                             float* __restrict__ combine_w, float* __restrict__ probs,
-                                                             int* __restrict__ counts) {
-    extern __shared__ __align__(128) unsigned char smem[];
-#ifdef GATE_V_EMPTY
-    if (threadIdx.x < 1000000) return;
-#endif
-    const int wpc = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, q = lane & 3;
-    const int ngroups = M / 32;
-    double2* sw = reinterpret_cast<double2*>(smem);
-    unsigned char* ring = smem + (size_t)ngroups * NT * 4 * 32 * sizeof(double2) + (size_t)warp * S * kGateStage;
-    const uint32_t bar0 = gring::saddr(smem + (size_t)ngroups * NT * 4 * 32 * sizeof(double2) +
-                                       (size_t)wpc * S * kGateStage) + warp * S * 8;
-    if (lane == 0) {
-        for (int s = 0; s < S; ++s) gring::bar_init(bar0 + 8 * s);
-#ifndef GATE_V_NOFENCE
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#endif
-    }
-    __syncwarp();
-
-    const int tiles = (n + 7) / 8;
-    const int nch = (M + kGateCC - 1) / kGateCC;
-    const int first = blockIdx.x * wpc + warp, stride = gridDim.x * wpc;
-    const int my_tiles = first < tiles ? (tiles - 1 - first) / stride + 1 : 0;
-    const int items = my_tiles * nch;
-    auto issue = [&](int it) {          // lane 0: bulk copies of item it (tile it / nch, chunk it % nch)
-#ifdef GATE_V_NOCOPY
-        return;
-#endif
-        const int ti = it / nch, ch = it - ti * nch;
-        const int t0 = (first + ti * stride) * 8;
-        const int c0 = ch * kGateCC;
-        const int cols = min(kGateCC, M - c0);
-        const int rows = min(8, n - t0);
-        const uint32_t st = (uint32_t)it % S;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        gring::bar_expect(bar0 + 8 * st, (uint32_t)(rows * cols * 2));
-        for (int r = 0; r < rows; ++r)
-            gring::bulk_g2s(gring::saddr(ring + st * kGateStage + r * kGateRow), x + (long long)(t0 + r) * ldx + c0,
-                            cols * 2, bar0 + 8 * st);
-    };
-    // Wg^T -> f64 lane-major shared copy; experts >= E are zero.  Unit = one expert's 8
-    // consecutive columns (one 16-byte load) = lane (e % 8, q)'s four double2 of one column
-    // group.  The gate-weight loads are issued FIRST (every warp waits on them), then the x
-    // copies stream in behind them while the weights are converted.
-#ifndef GATE_V_NOWG
-    const int units = NT * 8 * (M / 8);
-#else
-    const int units = 0;
-#endif
-    constexpr int U = 8;
-    const int rounds = (units + U * blockDim.x - 1) / (U * blockDim.x);
-    for (int rd = 0; rd < rounds; ++rd) {
-        const int u0 = rd * U * blockDim.x;
-        int4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = u0 + u * blockDim.x + threadIdx.x;
-            const int e = i / (M / 8), c8 = i - e * (M / 8);
-            v[u] = (i < units && e < E) ? __ldg(reinterpret_cast<const int4*>(wg + (long long)e * M) + c8)
-                                        : make_int4(0, 0, 0, 0);
-        }
-        if (rd == 0 && lane == 0)
-            for (int it = 0; it < min(items, S - 1); ++it) issue(it);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = u0 + u * blockDim.x + threadIdx.x;
-            if (i >= units) break;
-            const int e = i / (M / 8), c8 = i - e * (M / 8);
-            const int nt = e >> 3, l = ((e & 7) << 2) | (c8 & 3), j = c8 >> 2;
-            const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
-#pragma unroll
-            for (int up = 0; up < 4; ++up)
-                sw[((j * NT + nt) * 4 + up) * 32 + l] = make_double2(bf16_to_f64(w[up] & 0xFFFFu),
-                                                                    bf16_to_f64(w[up] >> 16));
-        }
-    }
-    if (rounds == 0 && lane == 0)
-        for (int it = 0; it < min(items, S - 1); ++it) issue(it);
-    __syncthreads();
-
-    int it = 0;
-    for (int ti = 0; ti < my_tiles; ++ti) {
-        const int tile = first + ti * stride;
-        double acc[4][NT][2];   // four independent DMMA chains (DMMA latency ~28 cycles, issue ~16 per SMSP)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
-        for (int ch = 0; ch < nch; ++ch, ++it) {
-            if (lane == 0 && it + S - 1 < items) issue(it + S - 1);
-            const uint32_t st = (uint32_t)it % S;
-#ifndef GATE_V_NOWAIT
-            gring::bar_wait(bar0 + 8 * st, ((uint32_t)it / S) & 1);
-#endif
-            const unsigned char* xs = ring + st * kGateStage + g * kGateRow;
-            const int cols = min(kGateCC, M - ch * kGateCC);
-            const int j0 = ch * (kGateCC / 32);
-            // software-pipelined: group jj + 1's shared-memory operands load while group jj's DMMAs issue
-            const int ng = cols / 32;
-            int4 xv = *reinterpret_cast<const int4*>(xs + 8 * q * 2);
-            double2 wv[NT][4];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int up = 0; up < 4; ++up) wv[nt][up] = sw[((j0 * NT + nt) * 4 + up) * 32 + lane];
-#pragma unroll 2
-            for (int jj = 0; jj < ng; ++jj) {
-                const int jn = jj + 1 < ng ? jj + 1 : jj;
-                const int4 xn = *reinterpret_cast<const int4*>(xs + (jn * 32 + 8 * q) * 2);
-                double2 wn[NT][4];
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int up = 0; up < 4; ++up) wn[nt][up] = sw[(((j0 + jn) * NT + nt) * 4 + up) * 32 + lane];
-                const uint32_t xw[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
-                double a[8];
-#pragma unroll
-                for (int up = 0; up < 4; ++up) {
-                    a[2 * up] = bf16_bits_to_f64(xw[up] << 16);
-                    a[2 * up + 1] = bf16_bits_to_f64(xw[up] & 0xFFFF0000u);
-                }
-#ifndef GATE_V_NOMMA
-#pragma unroll
-                for (int up = 0; up < 4; ++up)
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        dmma884(acc[(2 * up) & 3][nt][0], acc[(2 * up) & 3][nt][1], a[2 * up], wv[nt][up].x);
-                        dmma884(acc[(2 * up + 1) & 3][nt][0], acc[(2 * up + 1) & 3][nt][1], a[2 * up + 1],
-                                wv[nt][up].y);
-                    }
-#else
-                acc[0][0][0] += a[0] * wv[0][0].x + a[7];
-#endif
-                xv = xn;
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int up = 0; up < 4; ++up) wv[nt][up] = wn[nt][up];
-            }
-            __syncwarp();   // every lane is done with the stage before lane 0 refills it
-        }
-        double lg[NT][2];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            lg[nt][0] = (acc[0][nt][0] + acc[1][nt][0]) + (acc[2][nt][0] + acc[3][nt][0]);
-            lg[nt][1] = (acc[0][nt][1] + acc[1][nt][1]) + (acc[2][nt][1] + acc[3][nt][1]);
-        }
-        const int t = tile * 8 + g;
-        bool pick[NT][2];
-#ifndef GATE_V_NOEPI
-        gate_topk_epilogue<NT>(lg, g, q, t, t < n, E, k, expert_idx, combine_w, probs, pick);
-#else
-        pick[0][0] = lg[0][0] > 0; pick[0][1] = false;
-        if (t < n && q < k) { expert_idx[(long long)t * k + q] = q; combine_w[(long long)t * k + q] = (float)lg[0][0]; }
-#endif
-        if (counts != nullptr) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) {   // expert nt*8 + 2qq + h: the lanes of quad index qq
-                        const unsigned b = __ballot_sync(0xffffffffu, pick[nt][h] && q == qq);
-                        const int e = nt * 8 + 2 * qq + h;
-                        if (lane == 0 && e < E) counts[(long long)tile * E + e] = __popc(b);
-                    }
-        }
-    }
-}
 
 // dWg^T partials: part[c][e][m] = sum_{t in token range c} dlogits[t][e] * x[t][m].
 // One CTA per SM over a contiguous token range (~n/148 tokens): the range's rows stream into
@@ -467,8 +456,12 @@ constexpr int kWgStageBytes = 64 * 1024;
 // their sums through shared memory at the end: 16 warps per SM for latency hiding.
 template <int EMAX, int NB>   // 4 columns x EMAX experts per thread for NB column blocks (M <= NB * 1024)
 __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
-                                                                        const float* __restrict__ dlogits, int n, int M,
+                                                                        const float* __restrict__ dlogits, int n, int Mfull,
                                                                         int E, float* __restrict__ part) {
+    // blockIdx.y: this CTA's column slice [cbase, cbase + M) of the NB * 1024 columns it covers
+    const int cbase = blockIdx.y * NB * kWgBlock;
+    const int M = min(Mfull - cbase, NB * kWgBlock);
+    x += cbase;
     __shared__ float sdl[kWgMaxTok * EMAX];
     __shared__ __align__(8) uint64_t bars[kWgStages];
     extern __shared__ __align__(128) unsigned char sx[];
@@ -484,7 +477,7 @@ __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(cons
         unsigned char* dst = sx + (size_t)st * kWgStageBytes;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         gring::bar_expect(bar0 + 8 * st, (uint32_t)(rows * M * 2));
-        if (ldx == M) {
+        if (ldx == M && gridDim.y == 1) {
             gring::bulk_g2s(gring::saddr(dst), x + (long long)(t0 + r0) * ldx, rows * M * 2, bar0 + 8 * st);
         } else {
             for (int r = 0; r < rows; ++r)
@@ -561,7 +554,7 @@ __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(cons
             for (int e = 0; e < EMAX; ++e) {
                 if (e >= E) break;
                 const float4 o = fold[(b * EMAX + e) * kWgThreads + ht];
-                *reinterpret_cast<float4*>(part + ((long long)blockIdx.x * E + e) * M + c) =
+                *reinterpret_cast<float4*>(part + ((long long)blockIdx.x * E + e) * Mfull + cbase + c) =
                     make_float4(acc[b][e][0] + o.x, acc[b][e][1] + o.y, acc[b][e][2] + o.z, acc[b][e][3] + o.w);
             }
         }
@@ -610,7 +603,6 @@ __global__ void tile_count_kernel(const int* __restrict__ expert_idx, int n, int
         for (int j = 0; j < k; ++j) c += __ldg(expert_idx + (long long)(tile * 8 + i) * k + j) == lane;
     if (lane < E) counts[(long long)tile * E + lane] = c;
 }
-
 // ------------------------------------------------------------------ host
 template <int EMAX>
 static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wgT, int n, int M, int E, int k, int* ei,
@@ -626,15 +618,13 @@ static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wgT, int n
 
 size_t gate_counts_bytes(int n, int E) { return (size_t)((n + 7) / 8) * E * sizeof(int); }
 
-// Tensor-core gate configuration for (n, M, E): warps per CTA and ring depth, or false.
-static bool gate_tc_config(int n, int M, int E, int& wpc, int& stages, size_t& smem) {
-    if (M % 32 != 0 || E > 16) return false;
-    const int NT = E > 8 ? 2 : 1;
-    const size_t wbytes = (size_t)(M / 32) * NT * 4 * 32 * 16;
-    const size_t budget = 227 * 1024;
-    if (wbytes + 2 * 4 * kGateStage + 1024 > budget) return false;
+// Tensor-core gate configuration for (n, M, E): warps per CTA and shared memory, or false.
+static bool gate_mma_config(int n, int M, int E, int& wpc, size_t& smem) {
+    if (M % 32 != 0 || E > 32) return false;
+    const int NM = E > 16 ? 2 : 1;
+    const size_t scratch = (size_t)8 * 16 * NM * (8 + 8 + 4);
     const int tiles = (n + 7) / 8;
-    // warps per CTA (one 8-token tile in flight each): fewest tiles on the busiest SM, most warps on ties
+    // warps per CTA (one 8-token tile each at a time): fewest tiles on the busiest SM, most warps on ties
     wpc = 8;
     long long best = -1;
     for (int w = 8; w >= 4; --w) {
@@ -645,13 +635,8 @@ static bool gate_tc_config(int n, int M, int E, int& wpc, int& stages, size_t& s
             wpc = w;
         }
     }
-    const int nch = (M + kGateCC - 1) / kGateCC;
-    stages = (int)((budget - wbytes - 1024) / ((size_t)wpc * (kGateStage + 8)));
-    const int want = nch * ((tiles + (long long)kNumSMs * wpc - 1) / ((long long)kNumSMs * wpc));   // items per warp
-    stages = std::min(stages, std::max(2, std::min(want, 8)));
-    if (stages < 2) return false;
-    smem = wbytes + (size_t)wpc * stages * (kGateStage + 8) + 128;
-    return true;
+    smem = (size_t)2 * 16 * NM * (2 * M + 64) + (size_t)wpc * scratch;   // Wg^T, |Wg^T|, per-warp scratch
+    return smem <= 227 * 1024;
 }
 
 int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E, int k, int* expert_idx,
@@ -662,23 +647,25 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
     auto W = reinterpret_cast<const bf16*>(wgT);
-    int wpc = 0, stages = 0;
+    int wpc = 0;
     size_t smem = 0;
-    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && gate_tc_config(n, M, E, wpc, stages, smem)) {
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(wgT) & 15) == 0 &&
+        gate_mma_config(n, M, E, wpc, smem)) {
         const int tiles = (n + 7) / 8;
         const int blocks = (int)std::min<long long>((tiles + wpc - 1) / wpc, kNumSMs);
-        if (E <= 8) {
-            cudaFuncSetAttribute(gate_fwd_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            launch_k(gate_fwd_tc_kernel<1>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, stages, expert_idx,
-                     combine_w, probs, counts);
+        if (E <= 16) {
+            cudaFuncSetAttribute(gate_fwd_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_k(gate_fwd_mma_kernel<1>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
+                     probs, counts);
         } else {
-            cudaFuncSetAttribute(gate_fwd_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            launch_k(gate_fwd_tc_kernel<2>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, stages, expert_idx,
-                     combine_w, probs, counts);
+            cudaFuncSetAttribute(gate_fwd_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_k(gate_fwd_mma_kernel<2>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
+                     probs, counts);
         }
         PARM_CHECK_LAUNCH("gate_fwd");
         return 0;
     }
+    // shapes the tensor-core gate does not take (M % 32 != 0, unaligned rows, very wide M): f64 FMA gate
     if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 4)
@@ -718,11 +705,8 @@ int sum_chunks(const float* src, int chunks, long long len, float* out, int accu
 int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M, int E, float* ws, size_t ws_bytes,
                float* dwgT, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(E <= 32, "gate_wgrad: at most 32 experts supported");
-    const int emax = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
-    PARM_CHECK_ARG(M % 8 == 0 && M <= (32 / emax) * kWgBlock && ldx % 8 == 0 &&
-                       (reinterpret_cast<uintptr_t>(x) & 15) == 0,
-                   "gate_wgrad: embed (%d) must be a multiple of 8 and <= %d for %d experts, rows 16-byte aligned", M,
-                   (32 / emax) * kWgBlock, E);
+    PARM_CHECK_ARG(M % 8 == 0 && ldx % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0,
+                   "gate_wgrad: embed (%d) must be a multiple of 8, rows 16-byte aligned", M);
     PARM_CHECK_ARG(ws_bytes >= gate_wgrad_workspace(n, M, E), "gate_wgrad: workspace too small");
     const long long len = (long long)M * E;
     if (n == 0) {
@@ -733,6 +717,8 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     auto X = reinterpret_cast<const bf16*>(x);
     const int smem = kWgStages * kWgStageBytes;
     const int nb = (M + kWgBlock - 1) / kWgBlock;
+    // column slices of NBV * 1024 columns over grid.y (one slice unless M exceeds what a thread's
+    // accumulators cover: 4096 columns for E <= 8, 2048 for E <= 16, 1024 for E <= 32)
 #define PARM_WG_LAUNCH(EM, NBV)                                                                              \
     do {                                                                                                     \
         static bool attr = false;                                                                            \
@@ -741,7 +727,8 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
                                  smem);                                                                      \
             attr = true;                                                                                     \
         }                                                                                                    \
-        launch_k(gate_wgrad_partial_kernel<EM, NBV>, grid, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, ws); \
+        const dim3 gr(grid, (nb + (NBV) - 1) / (NBV));                                                       \
+        launch_k(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, ws); \
     } while (0)
     if (E <= 8 && nb == 1)
         PARM_WG_LAUNCH(8, 1);

@@ -70,6 +70,11 @@ struct Params {
     int pairs;                 // max 256-row pair tiles per group
     int seg_peer;              // ROW: rows of segment (hi, lo) stored through SegMaps.m[hi * nlo + lo] (the
                                //   owners' receive blocks, peer memory) -- the return AlltoAll fused into the epilogue
+    int kind, mb, epi;         // problem kind, B operand major-ness, fused epilogue
+    int dep, dep_on;           // multi-problem launch: dependency kind and the problem depended on
+    int fill_off, prefix_off;  // shared-memory offsets (ints) of the fill table and the ROW live-pair prefix
+    int row_ctr, col_ctr;      // completion counters (ints past ws + 2): (g, pair) and (g, n-block)
+    int signal;                // a later problem depends on this one: publish tile completions
 };
 
 // Per-segment 3-D store maps (N, rows, G) over peer destinations: the TMA-store
@@ -307,14 +312,15 @@ __device__ __forceinline__ bool nth_live_row_tile(const Params& p, const int* sf
 struct PairTile {
     bool live;       // the pair has work (its first tile exists)
     int g, hi, lo, m0, n0;   // this CTA's half: rows [m0, m0+128) of segment (hi, lo); m0 >= L/M -> dummy
+    int pj;                  // pair index within group g (ROW: compacted live pair; WGT: m pair)
 };
 
-__device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfill, int tile, int kind, int bn,
-                                               uint32_t rank, const int* sprefix) {
+__device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfill, int tile, int bn, uint32_t rank,
+                                               const int* sprefix) {
     PairTile t;
     int pj;
     t.hi = t.lo = 0;
-    if (kind == kRow) {   // tile = live pair-tile index: groups' live row pairs, compacted (sprefix)
+    if (p.kind == kRow) {   // tile = live pair-tile index: groups' live row pairs, compacted (sprefix)
         const int pu = tile / p.n_blocks;
         t.n0 = (tile - pu * p.n_blocks) * bn;
         int g = 0;
@@ -328,7 +334,8 @@ __device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfil
         pj = rem / p.n_blocks;
         t.n0 = (rem % p.n_blocks) * bn;
     }
-    if (kind == kRow) {
+    t.pj = pj;
+    if (p.kind == kRow) {
         int h0, l0, m00;
         t.live = nth_live_row_tile(p, sfill, t.g, 2 * pj, h0, l0, m00);
         if (rank == 0) {
@@ -346,6 +353,7 @@ __device__ __forceinline__ PairTile decode_pair(const Params& p, const int* sfil
     }
     return t;
 }
+
 
 // ---------------------------------------------------------------- TMA-store epilogue (pair kernel)
 // Each epilogue warp owns 32 accumulator rows.  Per 128-byte output chunk of
@@ -506,28 +514,211 @@ __device__ __forceinline__ void drain_tile_tma(const Params& p, const CUtensorMa
     }
 }
 
-template <int BN, int KIND, int MB, int EPI>
+constexpr int kBarBytes = 512;   // mbarriers, TMEM slot, tile broadcast ring, queue offsets
+
+template <int BN>
 struct CfgPair {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = (BN / 2) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kEpiBytes = 4 * kEpiBufs * kEpiStageBytes;   // 4 epilogue warps x staging buffers
-    static constexpr int kFixed = kEpiBytes + 1024 + 256 + kMaxFill * 4;
+    static constexpr int kFixed = kEpiBytes + 1024 + kBarBytes + kMaxFill * 4;
     static constexpr int kStages = (PARM_PAIR_SMEM - kFixed) / kStageBytes > 8 ? 8
                                                                                : (PARM_PAIR_SMEM - kFixed) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256 + kMaxFill * 4;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kFixed;
+    static_assert(2 * kStages * 8 + 4 * 8 + 2 * 4 * 8 + 4 + 4 * 4 + 5 * 4 <= kBarBytes, "barrier area");
 };
 
-template <int BN, int KIND, int MB, int EPI>
+// ---------------------------------------------------------------- multi-problem persistent kernel
+// One launch runs up to kMaxProb GEMMs (the expert FFN's forward pair or its four backward
+// GEMMs) as ONE work queue of 256 x BN pair tiles, problem after problem.  Each CTA pair claims
+// its next tile from a global counter (the leader's producer thread) and broadcasts it through a
+// small shared-memory ring to its own MMA / epilogue warps and to the peer CTA, so a pair that
+// finishes early takes more tiles and the partial last wave of one GEMM is filled by the next
+// GEMM's tiles instead of idling (dR / Y have 256 tiles for 74 pairs: 3.46 waves).  A tile of a
+// dependent problem waits, before its first TMA load, for the tiles it reads:
+//   kDepRowPair   ROW tile (g, pair) of problem i reads rows of the same pair of problem j
+//                 over all of j's columns (Y = H W2 after H; dR = dH W1^T after dH);
+//   kDepColBlock  WGT tile (g, m-pair) reads columns [256 m-pair, +256) of problem j's output
+//                 for every row of group g (dW1^T = dH^T R after dH).
+// Completion counters: every epilogue warp of a finished tile (8 per pair) waits for its bulk
+// stores, fences, and adds 1 to the (g, pair) and (g, column block) counters of its problem.
+// Tiles are claimed in queue order and only by running CTAs, so every tile a waiting CTA
+// depends on is held by a running CTA that never waits on a later tile: no deadlock without
+// co-residency.  The last CTA to exit zeroes the queue head and the counters for the next launch.
+constexpr int kMaxProb = 4;
+constexpr int kSched = 4;          // depth of the tile broadcast ring
+enum Dep : int { kDepNone = 0, kDepRowPair = 1, kDepColBlock = 2 };
+
+struct Multi {
+    CUtensorMap ta[kMaxProb], tb[kMaxProb], td[kMaxProb];
+    Params pr[kMaxProb];
+    int nprob;
+    int seg_prob;                  // problem whose ROW outputs go through SegMaps (-1: none)
+    int* ws;                       // [0] queue head, [1] exit count, [2 ...] completion counters
+    int ws_ints;                   // counters to clear at exit (from ws + 2)
+};
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {   // acquire at cluster scope
+    uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) break;
+        if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");
+    }
+}
+
+__device__ __forceinline__ void st_remote_u32(int* local_addr, uint32_t rank, int v) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(local_addr)),
+        "r"(rank), "r"(v)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* bar, uint32_t rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(rank)
+        : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void wait_counter(const int* c, int target) {
+    const long long t0 = clock64();
+    while (ld_acquire(c) < target) {
+        __nanosleep(128);
+        if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // the TMA loads that follow see the data
+}
+
+// (problem, local tile) of queue index `tile` (sbase: prefix of the problems' tile counts)
+__device__ __forceinline__ int find_prob(const int* sbase, int nprob, int tile) {
+    int pi = 0;
+    while (pi + 1 < nprob && sbase[pi + 1] <= tile) ++pi;
+    return pi;
+}
+
+template <int BN>
+__device__ __forceinline__ void drain_any(const Params& p, const CUtensorMap* td, uint32_t taddr, int lane, int row0,
+                                          const PairTile& t, bool row_ok, long long xrow, bool empty, uint8_t* stage,
+                                          int& buf, const CUtensorMap* seg) {
+#define PARM_DRAIN(KD, EP) \
+    drain_tile_tma<BN, KD, EP>(p, td, taddr, lane, row0, t.g, t.lo, t.hi, t.n0, row_ok, xrow, empty, stage, buf, seg)
+    if (p.kind == kRow) {
+        switch (p.epi) {
+            case kEpiReluBF16: PARM_DRAIN(kRow, kEpiReluBF16); break;
+            case kEpiDReluBF16: PARM_DRAIN(kRow, kEpiDReluBF16); break;
+            case kEpiReluMaskBF16: PARM_DRAIN(kRow, kEpiReluMaskBF16); break;
+            case kEpiDMaskBF16: PARM_DRAIN(kRow, kEpiDMaskBF16); break;
+            default: PARM_DRAIN(kRow, kEpiBF16); break;
+        }
+    } else if (p.epi == kEpiF32Acc) {
+        PARM_DRAIN(kWgt, kEpiF32Acc);
+    } else {
+        PARM_DRAIN(kWgt, kEpiF32);
+    }
+#undef PARM_DRAIN
+}
+
+
+// Producer body of one pair tile: its K blocks' A rows and half B tile into the smem ring.
+template <int BN, int KIND, int MB>
+__device__ __forceinline__ void produce_tile(const Params& p, const int* pf, const PairTile& t, uint32_t rank,
+                                             bool leader, const CUtensorMap* tma, const CUtensorMap* tmb,
+                                             uint8_t* smem_a, uint8_t* smem_b, uint64_t* full_bar,
+                                             uint64_t* empty_bar, int& stage, uint32_t& phase) {
+    using C = CfgPair<BN>;
+    constexpr int BNH = BN / 2;
+    const int g = t.g;
+    const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
+    for_each_kblock<KIND>(p, pf, g, [&](int hi, int lo, int r0) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (leader)
+            mbar_expect_tx(&full_bar[stage], 2u * C::kStageBytes);
+        else
+            mbar_arrive_remote(&full_bar[stage], 0);
+        uint8_t* sa = smem_a + stage * C::kABytes;
+        uint8_t* sb = smem_b + stage * C::kBBytes;
+        if (KIND == kRow) {
+            tma2_load_5d(tma, &full_bar[stage], sa, r0, t.m0, g, t.lo, t.hi);
+            if (MB == kKMajor) {
+                tma2_load_3d(tmb, &full_bar[stage], sb, r0, nb0, g);
+            } else {
+#pragma unroll
+                for (int a = 0; a < BNH / 64; ++a)
+                    tma2_load_3d(tmb, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, r0, g);
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < BM / 64; ++a)
+                tma2_load_5d(tma, &full_bar[stage], sa + a * (BK * 128), t.m0 + a * 64, r0, g, lo, hi);
+#pragma unroll
+            for (int a = 0; a < BNH / 64; ++a)
+                tma2_load_5d(tmb, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, r0, g, lo, hi);
+        }
+        if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+        }
+    });
+}
+
+// MMA body of one pair tile (leader, one thread): compile-time instruction / smem descriptors.
+template <int BN, int KIND, int MA, int MBX>
+__device__ __forceinline__ void mma_tile(const Params& p, const int* pf, int g, uint32_t tmem_d, uint8_t* smem_a,
+                                         uint8_t* smem_b, uint64_t* full_bar, uint64_t* empty_bar, int& stage,
+                                         uint32_t& phase) {
+    using C = CfgPair<BN>;
+    constexpr uint32_t idesc = instr_desc_pair<BN, MA, MBX>();
+    constexpr uint32_t a_lbo = (MA == kKMajor) ? 0 : BK * 128;
+    constexpr uint32_t b_lbo = (MBX == kKMajor) ? 0 : BK * 128;
+    constexpr uint32_t a_kstep = (MA == kKMajor) ? 32 : 16 * 128;
+    constexpr uint32_t b_kstep = (MBX == kKMajor) ? 32 : 16 * 128;
+    bool first = true;
+    for_each_kblock<KIND>(p, pf, g, [&](int, int, int) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
+        const uint32_t sb = smem_u32(smem_b + stage * C::kBBytes);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
+            uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
+            tc2_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+        }
+        first = false;
+        tc2_commit_both(&empty_bar[stage]);
+        if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+        }
+    });
+}
+
+template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    moe_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                         const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ Params p,
-                         const __grid_constant__ SegMaps segmaps) {
-    using C = CfgPair<BN, KIND, MB, EPI>;
+    moe_gemm_pair_kernel(const __grid_constant__ Multi mp, const __grid_constant__ SegMaps segmaps) {
+    using C = CfgPair<BN>;
     constexpr int STAGES = C::kStages;
-    constexpr int MA = (KIND == kRow) ? kKMajor : kMNMajor;
-    constexpr int MBX = (KIND == kRow) ? MB : kMNMajor;
     constexpr int BNH = BN / 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -537,22 +728,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* empty_bar = full_bar + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-    int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + 256);
-    uint8_t* smem_epi = smem + STAGES * C::kStageBytes + 256 + kMaxFill * 4;   // 1024-aligned staging
+    uint64_t* sfull_bar = tempty_bar + 2;
+    uint64_t* sempty_bar = sfull_bar + kSched;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty_bar + kSched);
+    int* stile = reinterpret_cast<int*>(tmem_slot + 1);          // kSched broadcast entries
+    int* sbase = stile + kSched;                                  // kMaxProb + 1 queue offsets
+    int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + kBarBytes);
+    uint8_t* smem_epi = smem + STAGES * C::kStageBytes + kBarBytes + kMaxFill * 4;   // 1024-aligned staging
     smem_epi = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_epi) + 1023) & ~uintptr_t(1023));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const int pair_id = blockIdx.x >> 1;
-    const int num_pairs = gridDim.x >> 1;
+    const int nprob = mp.nprob;
 
     if (warp == 0 && lane == 0) {
-        prefetch_tmap(&tmap_a);
-        prefetch_tmap(&tmap_b);
-        prefetch_tmap(&tmap_d);
+        for (int i = 0; i < nprob; ++i) {
+            prefetch_tmap(&mp.ta[i]);
+            prefetch_tmap(&mp.tb[i]);
+            prefetch_tmap(&mp.td[i]);
+        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 2);      // leader expect_tx arrival + peer arrival
             mbar_init(&empty_bar[s], 1);     // leader's multicast commit
@@ -560,6 +756,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull_bar[s], 1);
             mbar_init(&tempty_bar[s], 2 * 128);   // both CTAs' epilogue threads (leader's copy used)
+        }
+        for (int s = 0; s < kSched; ++s) {
+            mbar_init(&sfull_bar[s], 1);          // the leader producer's (local or remote) arrival
+            mbar_init(&sempty_bar[s], 10);        // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -569,93 +769,144 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
-    // everything above is independent of the previous kernel (PDL prologue); fill counts and operands are not
-    if (p.fill)
-        for (int i = threadIdx.x; i < p.G * p.nhi * p.nlo; i += blockDim.x) sfill[i] = __ldg(p.fill + i);
-    // ROW: work list = live 256-row pair tiles only (groups' live row pairs, prefix-summed), so the
-    // static round-robin over the 74 pairs balances the real work instead of an index space with
-    // unfilled capacity holes (max 5 vs the ideal 4 tiles per pair measured on the second GEMM).
-    int* sprefix = sfill + p.G * p.nhi * p.nlo;
-    if (KIND == kRow) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            sprefix[0] = 0;
-            for (int g = 0; g < p.G; ++g) {
-                int lt = 0;
-                for (int seg = 0; seg < p.nhi * p.nlo; ++seg) {
-                    const int h = seg / p.nlo, l = seg - h * p.nlo;
-                    int live = (seg_fill(p, sfill, g, h, l) + BM - 1) / BM;
-                    lt += live > p.m_tiles ? p.m_tiles : live;
+    // fill tables and ROW live-pair prefixes of every problem
+    for (int i = 0; i < nprob; ++i) {
+        const Params& p = mp.pr[i];
+        if (p.fill)
+            for (int j = threadIdx.x; j < p.G * p.nhi * p.nlo; j += blockDim.x) sfill[p.fill_off + j] = __ldg(p.fill + j);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int base = 0;
+        for (int i = 0; i < nprob; ++i) {
+            const Params& p = mp.pr[i];
+            sbase[i] = base;
+            if (p.kind == kRow) {
+                const int* f = sfill + p.fill_off;
+                int* pre = sfill + p.prefix_off;
+                int acc = 0;
+                pre[0] = 0;
+                for (int g = 0; g < p.G; ++g) {
+                    int lt = 0;
+                    for (int seg = 0; seg < p.nhi * p.nlo; ++seg) {
+                        const int h = seg / p.nlo, l = seg - h * p.nlo;
+                        int live = (seg_fill(p, f, g, h, l) + BM - 1) / BM;
+                        lt += live > p.m_tiles ? p.m_tiles : live;
+                    }
+                    acc += (lt + 1) / 2;
+                    pre[g + 1] = acc;
                 }
-                acc += (lt + 1) / 2;
-                sprefix[g + 1] = acc;
+                base += acc * p.n_blocks;
+            } else {
+                base += p.num_tiles;
             }
         }
+        sbase[nprob] = base;
     }
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int ntiles = (KIND == kRow) ? sprefix[p.G] * p.n_blocks : p.num_tiles;
+    const int total = sbase[nprob];
+
+    // Next tile of this pair: the leader producer claims and broadcasts; everyone else receives.
+    // Consumers: one arrival per warp on the leader's sempty after reading the entry.
+    // Static mode (mp.ws == null: one GEMM, no dependencies): pair p takes tiles p, p + pairs, ...
+    const bool dyn = mp.ws != nullptr;
+    const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+    auto receive = [&](int& si, bool whole) -> int {
+        if (!dyn) {
+            const int tile = pair_id + si * num_pairs;
+            ++si;
+            return tile < total ? tile : total;
+        }
+        const int slot = si % kSched;
+        mbar_wait_cluster(&sfull_bar[slot], (si / kSched) & 1);
+        const int tile = *reinterpret_cast<volatile int*>(&stile[slot]);
+        if (whole) __syncwarp();
+        if (lane == 0) {
+            if (leader)
+                mbar_arrive(&sempty_bar[slot]);
+            else
+                mbar_arrive_remote_release(&sempty_bar[slot], 0);
+        }
+        ++si;
+        return tile;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
-                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
+            int si = 0;
+            // claim one tile ahead: the atomic's round trip overlaps the current tile's loads
+            int claimed = (dyn && leader) ? atomicAdd(mp.ws, 1) : 0;
+            while (true) {
+                int tile;
+                if (!dyn) {
+                    tile = receive(si, false);
+                } else if (leader) {
+                    tile = claimed;
+                    if (tile < total) claimed = atomicAdd(mp.ws, 1);
+                    const int slot = si % kSched;
+                    mbar_wait(&sempty_bar[slot], ((si / kSched) & 1) ^ 1);
+                    stile[slot] = tile;
+                    st_remote_u32(&stile[slot], 1, tile);
+                    mbar_arrive(&sfull_bar[slot]);
+                    mbar_arrive_remote_release(&sfull_bar[slot], 1);
+                    ++si;
+                } else {
+                    const int slot = si % kSched;
+                    mbar_wait_cluster(&sfull_bar[slot], (si / kSched) & 1);
+                    tile = *reinterpret_cast<volatile int*>(&stile[slot]);
+                    mbar_arrive_remote_release(&sempty_bar[slot], 0);
+                    ++si;
+                }
+                if (tile >= total) break;
+                const int pi = find_prob(sbase, nprob, tile);
+                const Params p = mp.pr[pi];   // by value: registers, not param-space reloads after every asm clobber
+                const int* pf = sfill + p.fill_off;
+                const PairTile t = decode_pair(p, pf, tile - sbase[pi], BN, rank, sfill + p.prefix_off);
                 if (!t.live) continue;
-                for_each_kblock<KIND>(p, sfill, t.g, [&](int hi, int lo, int r0) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
-                    if (leader)
-                        mbar_expect_tx(&full_bar[stage], 2u * C::kStageBytes);
-                    else
-                        mbar_arrive_remote(&full_bar[stage], 0);
-                    uint8_t* sa = smem_a + stage * C::kABytes;
-                    uint8_t* sb = smem_b + stage * C::kBBytes;
-                    const int nb0 = t.n0 + (int)rank * BNH;   // this CTA's half of the B tile
-                    if (KIND == kRow) {
-                        const int k0 = r0;
-                        tma2_load_5d(&tmap_a, &full_bar[stage], sa, k0, t.m0, t.g, t.lo, t.hi);
-                        if (MB == kKMajor) {
-                            tma2_load_3d(&tmap_b, &full_bar[stage], sb, k0, nb0, t.g);
-                        } else {
-#pragma unroll
-                            for (int a = 0; a < BNH / 64; ++a)
-                                tma2_load_3d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, k0, t.g);
-                        }
-                    } else {
-#pragma unroll
-                        for (int a = 0; a < BM / 64; ++a)
-                            tma2_load_5d(&tmap_a, &full_bar[stage], sa + a * (BK * 128), t.m0 + a * 64, r0, t.g, lo,
-                                         hi);
-#pragma unroll
-                        for (int a = 0; a < BNH / 64; ++a)
-                            tma2_load_5d(&tmap_b, &full_bar[stage], sb + a * (BK * 128), nb0 + a * 64, r0, t.g, lo,
-                                         hi);
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                });
+#ifndef PARM_GEMM_NO_DEPS   // (measurement variant only: dependent tiles do not wait -- wrong results)
+                if (p.dep == kDepRowPair) {
+                    const Params& q = mp.pr[p.dep_on];
+                    wait_counter(mp.ws + 2 + q.row_ctr + t.g * q.pairs + t.pj, 8 * q.n_blocks);
+                } else if (p.dep == kDepColBlock) {
+                    const Params& q = mp.pr[p.dep_on];
+                    const int* qp = sfill + q.prefix_off;
+                    wait_counter(mp.ws + 2 + q.col_ctr + t.g * q.n_blocks + t.pj, 8 * (qp[t.g + 1] - qp[t.g]));
+                }
+#endif
+                const CUtensorMap* tma = &mp.ta[pi];
+                const CUtensorMap* tmb = &mp.tb[pi];
+                // one loop per (kind, B major): compile-time TMA patterns in the per-k-block body
+                if (p.kind == kWgt)
+                    produce_tile<BN, kWgt, kMNMajor>(p, pf, t, rank, leader, tma, tmb, smem_a, smem_b, full_bar,
+                                                     empty_bar, stage, phase);
+                else if (p.mb == kKMajor)
+                    produce_tile<BN, kRow, kKMajor>(p, pf, t, rank, leader, tma, tmb, smem_a, smem_b, full_bar,
+                                                    empty_bar, stage, phase);
+                else
+                    produce_tile<BN, kRow, kMNMajor>(p, pf, t, rank, leader, tma, tmb, smem_a, smem_b, full_bar,
+                                                     empty_bar, stage, phase);
             }
         }
     } else if (warp == 1) {
         if (lane == 0 && leader) {
             // ------------------------------------------------ MMA issuer (leader CTA only)
-            constexpr uint32_t idesc = instr_desc_pair<BN, MA, MBX>();
-            constexpr uint32_t a_lbo = (MA == kKMajor) ? 0 : BK * 128;
-            constexpr uint32_t b_lbo = (MBX == kKMajor) ? 0 : BK * 128;
-            constexpr uint32_t a_kstep = (MA == kKMajor) ? 32 : 16 * 128;
-            constexpr uint32_t b_kstep = (MBX == kKMajor) ? 32 : 16 * 128;
             int stage = 0;
             uint32_t phase = 0;
             int it_tile = 0;
-            for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
-                const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
+            int si = 0;
+            while (true) {
+                const int tile = receive(si, false);
+                if (tile >= total) break;
+                const int pi = find_prob(sbase, nprob, tile);
+                const Params p = mp.pr[pi];   // by value: registers, not param-space reloads after every asm clobber
+                const int* pf = sfill + p.fill_off;
+                const PairTile t = decode_pair(p, pf, tile - sbase[pi], BN, rank, sfill + p.prefix_off);
                 if (!t.live) continue;
                 const int as = it_tile & 1;
                 const uint32_t aphase = (it_tile >> 1) & 1;
@@ -663,25 +914,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_wait(&tempty_bar[as], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + as * BN;
-                bool first = true;
-                for_each_kblock<KIND>(p, sfill, t.g, [&](int, int, int) {
-                    mbar_wait(&full_bar[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem_a + stage * C::kABytes);
-                    const uint32_t sb = smem_u32(smem_b + stage * C::kBBytes);
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        uint64_t ad = smem_desc(sa + k * a_kstep, a_lbo, 1024);
-                        uint64_t bd = smem_desc(sb + k * b_kstep, b_lbo, 1024);
-                        tc2_mma(tmem_d, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
-                    }
-                    first = false;
-                    tc2_commit_both(&empty_bar[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                });
+                if (p.kind == kWgt)
+                    mma_tile<BN, kWgt, kMNMajor, kMNMajor>(p, pf, t.g, tmem_d, smem_a, smem_b, full_bar, empty_bar,
+                                                          stage, phase);
+                else if (p.mb == kKMajor)
+                    mma_tile<BN, kRow, kKMajor, kKMajor>(p, pf, t.g, tmem_d, smem_a, smem_b, full_bar, empty_bar,
+                                                        stage, phase);
+                else
+                    mma_tile<BN, kRow, kKMajor, kMNMajor>(p, pf, t.g, tmem_d, smem_a, smem_b, full_bar, empty_bar,
+                                                         stage, phase);
                 tc2_commit_both(&tfull_bar[as]);
             }
         }
@@ -690,46 +931,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int ew = warp & 3;
         int it_tile = 0;
         int ebuf = 0;
+        int si = 0;
         uint8_t* my_stage = smem_epi + ew * kEpiBufs * kEpiStageBytes;
-        for (int tile = pair_id; tile < ntiles; tile += num_pairs) {
-            const PairTile t = decode_pair(p, sfill, tile, KIND, BN, rank, sprefix);
+        while (true) {
+            const int tile = receive(si, true);
+            if (tile >= total) break;
+            const int pi = find_prob(sbase, nprob, tile);
+            const Params p = mp.pr[pi];   // by value (see the producer)
+            const int* pf = sfill + p.fill_off;
+            const PairTile t = decode_pair(p, pf, tile - sbase[pi], BN, rank, sfill + p.prefix_off);
             if (!t.live) continue;
             const int as = it_tile & 1;
             const uint32_t aphase = (it_tile >> 1) & 1;
             ++it_tile;
             bool empty = false;
-            if (KIND == kWgt && p.fill) {
+            if (p.kind == kWgt && p.fill) {
                 empty = true;
                 for (int seg = 0; seg < p.nhi * p.nlo && empty; ++seg)
-                    empty = seg_fill(p, sfill, t.g, seg / p.nlo, seg % p.nlo) <= 0;
+                    empty = seg_fill(p, pf, t.g, seg / p.nlo, seg % p.nlo) <= 0;
             }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
             const int row = t.m0 + ew * 32 + lane;
-            const bool row_ok = (KIND == kWgt) ? row < p.M : row < p.L;
-            long long drow, xrow = 0;
-            if (KIND == kRow) {
-                drow = (long long)t.g * p.d_g + (long long)t.lo * p.d_lo + (long long)t.hi * p.d_hi +
-                       (long long)row * p.d_ld;
+            const bool row_ok = (p.kind == kWgt) ? row < p.M : row < p.L;
+            long long xrow = 0;
+            if (p.kind == kRow)
                 xrow = (long long)t.g * p.x_g + (long long)t.lo * p.x_lo + (long long)t.hi * p.x_hi +
                        (long long)row * p.x_ld;
-            } else {
-                drow = (long long)t.g * p.d_g + (long long)row * p.d_ld;
-            }
             const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + as * BN;
-            (void)drow;
-            if (KIND == kRow && p.seg_peer) {   // TMA stores straight into the owner's receive block
-                drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
-                                              xrow, empty, my_stage, ebuf, &segmaps.m[t.hi * p.nlo + t.lo]);
-            } else {
-                drain_tile_tma<BN, KIND, EPI>(p, &tmap_d, taddr, lane, t.m0 + ew * 32, t.g, t.lo, t.hi, t.n0, row_ok,
-                                              xrow, empty, my_stage, ebuf);
-            }
+            const CUtensorMap* seg = (p.kind == kRow && p.seg_peer) ? &segmaps.m[t.hi * p.nlo + t.lo] : nullptr;
+            drain_any<BN>(p, &mp.td[pi], taddr, lane, t.m0 + ew * 32, t, row_ok, xrow, empty, my_stage, ebuf, seg);
             tc_fence_before();
             if (leader)
                 mbar_arrive(&tempty_bar[as]);
             else
                 mbar_arrive_remote(&tempty_bar[as], 0);
+#ifdef PARM_GEMM_NO_DEPS
+            if (false) {
+#else
+            if (p.signal && lane == 0) {   // publish this warp's rows of the tile to dependent tiles
+#endif
+                bulk_wait_all();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                atomicAdd(mp.ws + 2 + p.row_ctr + t.g * p.pairs + t.pj, 1);
+                atomicAdd(mp.ws + 2 + p.col_ctr + t.g * p.n_blocks + t.n0 / BN, 1);
+            }
         }
         if (lane == 0) bulk_wait_all();
     }
@@ -741,6 +988,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"((uint32_t)C::kTmemCols)
                      : "memory");
+    }
+    if (dyn && threadIdx.x == 0) {   // the last CTA out resets the queue and the counters for the next launch
+        __threadfence();
+        if (atomicAdd(mp.ws + 1, 1) == (int)gridDim.x - 1) {
+            for (int i = 0; i < mp.ws_ints; ++i) mp.ws[2 + i] = 0;
+            mp.ws[0] = 0;
+            __threadfence();
+            mp.ws[1] = 0;
+        }
     }
 }
 
@@ -786,41 +1042,11 @@ static int make_tmap(CUtensorMap* map, const void* base, int rank, const long lo
     return 0;
 }
 
-static SegMaps g_segmaps;   // per-call store maps of moe_gemm_peer (host calls are stream-ordered, one thread)
+static SegMaps g_segmaps;   // per-call store maps of the peer-output problem (host calls are stream-ordered)
 
-template <int BN, int KIND, int MB, int EPI>
-static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const Params& p,
-                       cudaStream_t stream) {
-    using C = CfgPair<BN, KIND, MB, EPI>;
-    auto kern = moe_gemm_pair_kernel<BN, KIND, MB, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        attr_set = true;
-    }
-    int grid = 2 * (p.num_tiles < kNumSMs / 2 ? p.num_tiles : kNumSMs / 2);   // clusters of 2 CTAs
-    if (grid < 2) grid = 2;
-    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, ta, tb, td, p, g_segmaps);
-    PARM_CHECK_LAUNCH("moe_gemm_pair");
-    return 0;
-}
-
-template <int KIND, int MB, int EPI>
-static int dispatch_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const Params& p,
-                       cudaStream_t s) {
-    if (bn == 256) return launch_pair<256, KIND, MB, EPI>(ta, tb, td, p, s);
-    return launch_pair<128, KIND, MB, EPI>(ta, tb, td, p, s);
-}
-
-}  // namespace gemm
-
-int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g, long long sd_ld, cudaStream_t stream);
-
-int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) { return moe_gemm_peer(q, nullptr, 0, 0, stream); }
-
-int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g, long long sd_ld,
-                  cudaStream_t stream) {
-    using namespace gemm;
+// Parameters and tensor maps of one GEMM descriptor (validates it).  bn: the pair tile's width.
+static int build_problem(const parm_gemm_desc& q, Params& p, CUtensorMap& ta, CUtensorMap& tb, CUtensorMap& td,
+                         int& bn) {
     PARM_CHECK_ARG(q.kind == kRow || q.kind == kWgt, "gemm: bad kind %d", q.kind);
     PARM_CHECK_ARG(q.groups > 0 && q.nhi > 0 && q.nlo > 0 && q.seg_len > 0, "gemm: empty row space");
     PARM_CHECK_ARG(q.N > 0 && q.N % 128 == 0, "gemm: N=%d must be a positive multiple of 128", q.N);
@@ -831,7 +1057,7 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
                        ((reinterpret_cast<uintptr_t>(q.aux.ptr) & 7) == 0 && q.N % 64 == 0 && q.aux.ld % 2 == 0),
                    "gemm: bit-mask aux must be 8-byte aligned with N %% 64 == 0");
     PARM_CHECK_ARG(q.groups * q.nhi * q.nlo + q.groups + 1 <= kMaxFill, "gemm: fill table too large");
-    Params p;
+    memset(&p, 0, sizeof(p));
     p.G = q.groups;
     p.nhi = q.nhi;
     p.nlo = q.nlo;
@@ -841,20 +1067,10 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     p.K = q.K;
     p.alpha = q.alpha;
     p.fill = q.fill;
-    p.seg_peer = 0;
-    if (seg_dst != nullptr) {
-        PARM_CHECK_ARG(q.kind == kRow && (q.epi == kEpiBF16 || q.epi == kEpiReluBF16),
-                       "gemm: peer segment outputs need a ROW GEMM with a bf16 epilogue");
-        PARM_CHECK_ARG(seg_dst->n == q.nhi * q.nlo, "gemm: %d peer outputs for %d segments", seg_dst->n,
-                       q.nhi * q.nlo);
-        PARM_CHECK_ARG(sd_ld % 8 == 0 && sd_g % 8 == 0, "gemm: peer output rows must be 16-byte aligned");
-        p.seg_peer = 1;
-        for (int i = 0; i < seg_dst->n; ++i) {
-            const long long dd[3] = {q.N, q.seg_len, q.groups};
-            const long long ds[2] = {sd_ld, sd_g};
-            if (int rc = make_tmap(&g_segmaps.m[i], seg_dst->ptr[i], 3, dd, ds, 32, 2, 64)) return rc;
-        }
-    }
+    p.kind = q.kind;
+    p.mb = q.kind == kRow ? q.b_major : kMNMajor;
+    p.epi = q.epi;
+    p.dep_on = -1;
     p.D = const_cast<void*>(q.d.ptr);
     p.d_ld = q.d.ld;
     p.d_g = q.d.g_stride;
@@ -865,9 +1081,8 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
     p.x_g = q.aux.g_stride;
     p.x_lo = q.aux.lo_stride;
     p.x_hi = q.aux.hi_stride;
-    const int bn = (q.N % 256 == 0) ? 256 : 128;
+    bn = (q.N % 256 == 0) ? 256 : 128;
     p.n_blocks = q.N / bn;
-    CUtensorMap ta, tb, td;
     int rc;
     if (q.kind == kRow) {   // D: bf16 [hi][lo][g][r][n] -> dims (N, L, G, nlo, nhi), 32-row x 128 B store boxes
         const long long dd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
@@ -899,36 +1114,146 @@ int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g
             const long long bs[2] = {q.b.ld, q.b.g_stride};
             rc = make_tmap(&tb, q.b.ptr, 3, bd, bs, BK);
         }
-        if (rc) return rc;
-        const int combo = q.b_major;
-        if (combo == kKMajor) {
-            if (q.epi == kEpiReluBF16) return dispatch_bn<kRow, kKMajor, kEpiReluBF16>(bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiReluMaskBF16)
-                return dispatch_bn<kRow, kKMajor, kEpiReluMaskBF16>(bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kKMajor, kEpiBF16>(bn, ta, tb, td, p, stream);
-        } else {
-            if (q.epi == kEpiDReluBF16) return dispatch_bn<kRow, kMNMajor, kEpiDReluBF16>(bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiDMaskBF16) return dispatch_bn<kRow, kMNMajor, kEpiDMaskBF16>(bn, ta, tb, td, p, stream);
-            if (q.epi == kEpiBF16) return dispatch_bn<kRow, kMNMajor, kEpiBF16>(bn, ta, tb, td, p, stream);
-        }
-    } else {
-        PARM_CHECK_ARG(q.M > 0 && q.M % BM == 0, "gemm: M=%d must be a positive multiple of %d", q.M, BM);
-        PARM_CHECK_ARG(q.epi == kEpiF32 || q.epi == kEpiF32Acc, "gemm: weight GEMMs produce f32");
-        p.m_tiles = q.M / BM;
-        p.pairs = (p.m_tiles + 1) / 2;
-        p.num_tiles = p.G * p.pairs * p.n_blocks;
-        p.k_iters = p.nhi * p.nlo * ((q.seg_len + BK - 1) / BK);
-        const long long ad[5] = {q.M, q.seg_len, q.groups, q.nlo, q.nhi};
-        const long long as[4] = {q.a.ld, q.a.g_stride, q.a.lo_stride, q.a.hi_stride};
-        if ((rc = make_tmap(&ta, q.a.ptr, 5, ad, as, BK))) return rc;
-        const long long bd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
-        const long long bs[4] = {q.b.ld, q.b.g_stride, q.b.lo_stride, q.b.hi_stride};
-        if ((rc = make_tmap(&tb, q.b.ptr, 5, bd, bs, BK))) return rc;
-        if (q.epi == kEpiF32) return dispatch_bn<kWgt, kMNMajor, kEpiF32>(bn, ta, tb, td, p, stream);
-        return dispatch_bn<kWgt, kMNMajor, kEpiF32Acc>(bn, ta, tb, td, p, stream);
+        return rc;
     }
-    set_error("gemm: unsupported combination kind=%d b_major=%d epi=%d", q.kind, q.b_major, q.epi);
-    return 1;
+    PARM_CHECK_ARG(q.M > 0 && q.M % BM == 0, "gemm: M=%d must be a positive multiple of %d", q.M, BM);
+    PARM_CHECK_ARG(q.epi == kEpiF32 || q.epi == kEpiF32Acc, "gemm: weight GEMMs produce f32");
+    p.m_tiles = q.M / BM;
+    p.pairs = (p.m_tiles + 1) / 2;
+    p.num_tiles = p.G * p.pairs * p.n_blocks;
+    p.k_iters = p.nhi * p.nlo * ((q.seg_len + BK - 1) / BK);
+    const long long ad[5] = {q.M, q.seg_len, q.groups, q.nlo, q.nhi};
+    const long long as[4] = {q.a.ld, q.a.g_stride, q.a.lo_stride, q.a.hi_stride};
+    if ((rc = make_tmap(&ta, q.a.ptr, 5, ad, as, BK))) return rc;
+    const long long bd[5] = {q.N, q.seg_len, q.groups, q.nlo, q.nhi};
+    const long long bs[4] = {q.b.ld, q.b.g_stride, q.b.lo_stride, q.b.hi_stride};
+    return make_tmap(&tb, q.b.ptr, 5, bd, bs, BK);
 }
+
+// Completion counters one problem needs when another depends on it: (g, pair) and (g, n-block).
+static long long counter_ints(const Params& p) { return (long long)p.G * (p.pairs + p.n_blocks); }
+
+static size_t multi_workspace(const parm_gemm_desc* qs, int count) {
+    long long ints = 2;
+    for (int i = 0; i < count; ++i) {
+        const parm_gemm_desc& q = qs[i];
+        const int bn = (q.N % 256 == 0) ? 256 : 128;
+        const long long pairs = q.kind == kRow ? ((long long)q.nhi * q.nlo * ((q.seg_len + BM - 1) / BM) + 1) / 2
+                                               : ((q.M + BM - 1) / BM + 1) / 2;
+        ints += (long long)q.groups * (pairs + q.N / bn);
+    }
+    return (size_t)ints * sizeof(int);
+}
+
+template <int BN>
+static void launch_multi(const Multi& m, int grid, cudaStream_t stream) {
+    using C = CfgPair<BN>;
+    auto kern = moe_gemm_pair_kernel<BN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        attr_set = true;
+    }
+    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, m, g_segmaps);
+}
+
+// count GEMMs as one persistent launch.  deps: 2 ints per problem (kind, problem depended on) or null.
+// ws: null (count == 1, no dependencies: static tile order) or a zero-initialised workspace of
+// multi_workspace() bytes, left zeroed by the kernel.  seg_prob >= 0: that problem's ROW outputs go
+// to seg_dst (the owners' receive blocks) instead of its D.
+static int run_multi(const parm_gemm_desc* qs, int count, const int* deps, int* ws, size_t ws_bytes, int seg_prob,
+                     const RowFan* seg_dst, long long sd_g, long long sd_ld, cudaStream_t stream) {
+    PARM_CHECK_ARG(count >= 1 && count <= kMaxProb, "gemm: %d problems (1..%d per launch)", count, kMaxProb);
+    PARM_CHECK_ARG(ws != nullptr || (count == 1 && (deps == nullptr || deps[0] == kDepNone)),
+                   "gemm: several problems or dependencies need a workspace");
+    PARM_CHECK_ARG(ws == nullptr || ws_bytes >= multi_workspace(qs, count), "gemm: workspace too small");
+    Multi m;
+    memset(&m, 0, sizeof(m));
+    int bn = 0, fill_ints = 0;
+    long long ctr = 0, ub = 0;
+    for (int i = 0; i < count; ++i) {
+        Params& p = m.pr[i];
+        int b;
+        if (int rc = build_problem(qs[i], p, m.ta[i], m.tb[i], m.td[i], b)) return rc;
+        PARM_CHECK_ARG(i == 0 || b == bn, "gemm: problems of one launch need the same tile width (N %% 256)");
+        bn = b;
+        p.fill_off = fill_ints;
+        if (p.fill) fill_ints += p.G * p.nhi * p.nlo;
+        p.prefix_off = fill_ints;
+        if (p.kind == kRow) fill_ints += p.G + 1;
+        ub += p.num_tiles;
+        if (deps != nullptr && deps[2 * i] != kDepNone) {
+            const int kd = deps[2 * i], on = deps[2 * i + 1];
+            PARM_CHECK_ARG(on >= 0 && on < i, "gemm: problem %d depends on %d (must be an earlier problem)", i, on);
+            const Params& q = m.pr[on];
+            PARM_CHECK_ARG(q.kind == kRow && q.G == p.G && q.nhi == p.nhi && q.nlo == p.nlo && q.L == p.L &&
+                               q.fill == p.fill,
+                           "gemm: a dependency must be a ROW problem over the same rows and fill counts");
+            if (kd == kDepRowPair) {
+                PARM_CHECK_ARG(p.kind == kRow, "gemm: row-pair dependency of a non-ROW problem");
+            } else {
+                PARM_CHECK_ARG(kd == kDepColBlock && p.kind == kWgt && bn == 256 && q.N == p.M,
+                               "gemm: column-block dependency needs a WGT problem with M = the ROW problem's N "
+                               "and 256-wide tiles");
+            }
+            p.dep = kd;
+            p.dep_on = on;
+            m.pr[on].signal = 1;
+        }
+    }
+    PARM_CHECK_ARG(fill_ints <= kMaxFill, "gemm: fill tables too large");
+    for (int i = 0; i < count; ++i) {
+        Params& p = m.pr[i];
+        if (!p.signal) continue;
+        p.row_ctr = (int)ctr;
+        p.col_ctr = (int)(ctr + (long long)p.G * p.pairs);
+        ctr += counter_ints(p);
+    }
+    m.seg_prob = seg_prob;
+    if (seg_prob >= 0) {
+        const parm_gemm_desc& q = qs[seg_prob];
+        PARM_CHECK_ARG(seg_prob < count && seg_dst != nullptr, "gemm: bad peer-output problem %d", seg_prob);
+        PARM_CHECK_ARG(q.kind == kRow && (q.epi == kEpiBF16 || q.epi == kEpiReluBF16),
+                       "gemm: peer segment outputs need a ROW GEMM with a bf16 epilogue");
+        PARM_CHECK_ARG(seg_dst->n == q.nhi * q.nlo, "gemm: %d peer outputs for %d segments", seg_dst->n,
+                       q.nhi * q.nlo);
+        PARM_CHECK_ARG(sd_ld % 8 == 0 && sd_g % 8 == 0, "gemm: peer output rows must be 16-byte aligned");
+        PARM_CHECK_ARG(!m.pr[seg_prob].signal, "gemm: a peer-output problem cannot be depended on");
+        m.pr[seg_prob].seg_peer = 1;
+        for (int i = 0; i < seg_dst->n; ++i) {
+            const long long dd[3] = {q.N, q.seg_len, q.groups};
+            const long long ds[2] = {sd_ld, sd_g};
+            if (int rc = make_tmap(&g_segmaps.m[i], seg_dst->ptr[i], 3, dd, ds, 32, 2, 64)) return rc;
+        }
+    }
+    m.nprob = count;
+    m.ws = ws;
+    m.ws_ints = (int)ctr;
+    long long pairs = ub < kNumSMs / 2 ? ub : kNumSMs / 2;   // clusters of 2 CTAs, one per TPC
+    if (pairs < 1) pairs = 1;
+    if (bn == 256)
+        launch_multi<256>(m, (int)(2 * pairs), stream);
+    else
+        launch_multi<128>(m, (int)(2 * pairs), stream);
+    PARM_CHECK_LAUNCH("moe_gemm_pair");
+    return 0;
+}
+
+}  // namespace gemm
+
+size_t moe_gemm_multi_workspace(const parm_gemm_desc* qs, int count) { return gemm::multi_workspace(qs, count); }
+
+int moe_gemm_multi(const parm_gemm_desc* qs, int count, const int* deps, void* ws, size_t ws_bytes, int seg_prob,
+                   const RowFan* seg_dst, long long sd_g, long long sd_ld, cudaStream_t stream) {
+    return gemm::run_multi(qs, count, deps, reinterpret_cast<int*>(ws), ws_bytes, seg_prob, seg_dst, sd_g, sd_ld,
+                           stream);
+}
+
+int moe_gemm_peer(const parm_gemm_desc& q, const RowFan* seg_dst, long long sd_g, long long sd_ld,
+                  cudaStream_t stream) {
+    return gemm::run_multi(&q, 1, nullptr, nullptr, 0, seg_dst ? 0 : -1, seg_dst, sd_g, sd_ld, stream);
+}
+
+int moe_gemm(const parm_gemm_desc& q, cudaStream_t stream) { return moe_gemm_peer(q, nullptr, 0, 0, stream); }
 
 }  // namespace parm

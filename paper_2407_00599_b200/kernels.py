@@ -300,18 +300,12 @@ def _rows(t: torch.Tensor | None) -> _lib.RowsC:
     raise ValueError(f"GEMM operand must be 3-D or 5-D, got {t.dim()}-D")
 
 
-def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill, flops, peer=None) -> None:
-    desc = _lib.GemmDescC(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, float(alpha), 0, _rows(a), _rows(b),
+def _desc(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill):
+    return _lib.GemmDescC(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, float(alpha), 0, _rows(a), _rows(b),
                           _rows(d), _rows(aux), _ptr(fill))
 
-    def launch():
-        if peer is None:
-            _lib.call("parm_gemm", ctypes.byref(desc), _stream())
-        else:
-            ptrs, g_stride, ld = peer
-            f = _fan(ptrs)
-            _lib.call("parm_gemm_peer", ctypes.byref(desc), ctypes.byref(f), g_stride, ld, _stream())
 
+def _timed(launch, flops) -> None:
     if gemm_timer is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -323,12 +317,78 @@ def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fil
     launch()
 
 
-def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, epi: int,
-              aux: torch.Tensor | None = None, fill: torch.Tensor | None = None, alpha: float = 1.0,
-              peer: tuple | None = None) -> None:
-    """ROW GEMM: D[hi][lo][g][r][n] = alpha * A[hi][lo][g][r][:] . B[g][n][:] (5-D A/D, 3-D weights B).
-    ``peer=(addresses, g_stride, ld)``: rows of segment hi*nlo+lo go to addresses[seg] + g*g_stride + r*ld
-    instead of D (the epilogue stores into the owners' receive blocks over NVLink)."""
+def _gemm(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill, flops, peer=None) -> None:
+    desc = _desc(kind, epi, b_major, G, nhi, nlo, L, M, N, Kd, alpha, a, b, d, aux, fill)
+
+    def launch():
+        if peer is None:
+            _lib.call("parm_gemm", ctypes.byref(desc), _stream())
+        else:
+            ptrs, g_stride, ld = peer
+            f = _fan(ptrs)
+            _lib.call("parm_gemm_peer", ctypes.byref(desc), ctypes.byref(f), g_stride, ld, _stream())
+
+    _timed(launch, flops)
+
+
+class Gemm:
+    """One GEMM of a multi-problem launch (``row`` / ``wgrad`` build it with the checks of
+    gemm_rows / gemm_wgrad; ``flops`` counts every row of the row space)."""
+
+    def __init__(self, desc, flops: int, tensors: tuple):
+        self.desc, self.flops, self._keep = desc, flops, tensors
+
+    @staticmethod
+    def row(a, b, b_major, d, epi, aux=None, fill=None, alpha=1.0) -> "Gemm":
+        nhi, nlo, G, L, Kd, N = _check_rows(a, b, b_major, d, epi, aux)
+        return Gemm(_desc(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill),
+                    2 * nhi * nlo * G * L * N * Kd, (a, b, d, aux, fill))
+
+    @staticmethod
+    def wgrad(a, b, d, epi=None, fill=None, alpha=1.0) -> "Gemm":
+        epi = EPI_F32 if epi is None else epi
+        nhi, nlo, G, L, M, N = _check_wgrad(a, b, d)
+        return Gemm(_desc(WGT, epi, MNMAJOR, G, nhi, nlo, L, M, N, 0, alpha, a, b, d, None, fill),
+                    2 * nhi * nlo * G * L * M * N, (a, b, d, fill))
+
+
+DEP_NONE, DEP_ROW_PAIR, DEP_COL_BLOCK = 0, 1, 2
+
+
+def gemm_multi_workspace(gemms: list) -> int:
+    arr = (_lib.GemmDescC * len(gemms))(*[g.desc for g in gemms])
+    return int(_lib.load().parm_gemm_multi_workspace(arr, len(gemms)))
+
+
+def gemm_multi(gemms: list, deps: list | None, ws: torch.Tensor, peer: tuple | None = None,
+               seg_prob: int = -1) -> None:
+    """``gemms`` as one persistent launch over a shared tile queue (parm_gemm_multi).  ``deps``: per
+    problem None or (DEP_ROW_PAIR | DEP_COL_BLOCK, index of an earlier problem).  ``ws``: a zeroed
+    workspace of >= gemm_multi_workspace bytes that stays zeroed between launches.  ``peer``
+    (addresses, g_stride, ld): problem ``seg_prob``'s outputs go to the owners' receive blocks."""
+    n = len(gemms)
+    arr = (_lib.GemmDescC * n)(*[g.desc for g in gemms])
+    dep = (_lib._c_int * (2 * n))()
+    for i, dd in enumerate(deps or [None] * n):
+        if dd is not None:
+            dep[2 * i], dep[2 * i + 1] = dd
+    need = gemm_multi_workspace(gemms)
+    if ws.numel() * ws.element_size() < need:
+        raise ValueError(f"gemm_multi: workspace of {ws.numel() * ws.element_size()} bytes < {need}")
+
+    def launch():
+        if peer is None:
+            _lib.call("parm_gemm_multi", arr, n, dep, ws.data_ptr(), need, -1, None, 0, 0, _stream())
+        else:
+            ptrs, g_stride, ld = peer
+            f = _fan(ptrs)
+            _lib.call("parm_gemm_multi", arr, n, dep, ws.data_ptr(), need, seg_prob, ctypes.byref(f), g_stride, ld,
+                      _stream())
+
+    _timed(launch, sum(g.flops for g in gemms))
+
+
+def _check_rows(a, b, b_major, d, epi, aux):
     _need(a, torch.bfloat16, "A")
     _need(b, torch.bfloat16, "B")
     _need(d, torch.bfloat16, "D")
@@ -341,13 +401,10 @@ def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, e
             raise ValueError("bit-mask epilogues need an int32 aux of shape D[..., N/32]")
     elif aux is not None and tuple(aux.shape) != tuple(d.shape):
         raise ValueError("aux must be shaped like D")
-    _gemm(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill,
-          2 * nhi * nlo * G * L * N * Kd, peer)
+    return nhi, nlo, G, L, Kd, N
 
 
-def gemm_wgrad(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epi: int = EPI_F32,
-               fill: torch.Tensor | None = None, alpha: float = 1.0) -> None:
-    """WGT GEMM: D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n] (f32 D)."""
+def _check_wgrad(a, b, d):
     _need(a, torch.bfloat16, "A")
     _need(b, torch.bfloat16, "B")
     _need(d, torch.float32, "D")
@@ -355,6 +412,24 @@ def gemm_wgrad(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epi: int = EPI
     N = b.shape[4]
     if tuple(b.shape[:4]) != (nhi, nlo, G, L) or tuple(d.shape) != (G, M, N):
         raise ValueError(f"gemm_wgrad shape mismatch: A{tuple(a.shape)} B{tuple(b.shape)} D{tuple(d.shape)}")
+    return nhi, nlo, G, L, M, N
+
+
+def gemm_rows(a: torch.Tensor, b: torch.Tensor, b_major: int, d: torch.Tensor, epi: int,
+              aux: torch.Tensor | None = None, fill: torch.Tensor | None = None, alpha: float = 1.0,
+              peer: tuple | None = None) -> None:
+    """ROW GEMM: D[hi][lo][g][r][n] = alpha * A[hi][lo][g][r][:] . B[g][n][:] (5-D A/D, 3-D weights B).
+    ``peer=(addresses, g_stride, ld)``: rows of segment hi*nlo+lo go to addresses[seg] + g*g_stride + r*ld
+    instead of D (the epilogue stores into the owners' receive blocks over NVLink)."""
+    nhi, nlo, G, L, Kd, N = _check_rows(a, b, b_major, d, epi, aux)
+    _gemm(ROW, epi, b_major, G, nhi, nlo, L, 0, N, Kd, alpha, a, b, d, aux, fill,
+          2 * nhi * nlo * G * L * N * Kd, peer)
+
+
+def gemm_wgrad(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epi: int = EPI_F32,
+               fill: torch.Tensor | None = None, alpha: float = 1.0) -> None:
+    """WGT GEMM: D[g][m][n] = alpha * sum_{hi,lo,r} A[hi][lo][g][r][m] * B[hi][lo][g][r][n] (f32 D)."""
+    nhi, nlo, G, L, M, N = _check_wgrad(a, b, d)
     _gemm(WGT, epi, MNMAJOR, G, nhi, nlo, L, M, N, 0, alpha, a, b, d, None, fill, 2 * nhi * nlo * G * L * M * N)
 
 

@@ -170,7 +170,8 @@ class MoELayer:
                    baseline (DeepSpeed-MoE ordering) always runs on the collectives."""
 
     def __init__(self, cfg: MoEConfig, layout: ParallelLayout, world: World | None = None, device=None, *,
-                 s1_return: str = "epilogue", s2_return: str = "pull", saa: str = "seq", peer: bool | None = None):
+                 s1_return: str = "epilogue", s2_return: str = "pull", saa: str = "seq", peer: bool | None = None,
+                 fused_ffn: bool = True):
         check_compatible(cfg, layout)
         if cfg.top_k > 8 or cfg.num_experts > 32:
             raise ValueError("B200 kernels support top_k <= 8 and num_experts <= 32")
@@ -192,7 +193,10 @@ class MoELayer:
         self.peer_push = s1_return in ("epilogue", "push")
         self.peer_epilogue = s1_return == "epilogue"
         self.peer_push_s2 = s2_return == "push"
-        self.options = {"s1_return": s1_return, "s2_return": s2_return, "saa": saa, "peer": self.peer}
+        # expert FFN GEMMs as one persistent launch per pass (forward 2, backward 4; parm_gemm_multi)
+        self.fused_ffn = fused_ffn and d.Mp % 256 == 0 and d.Hsp % 256 == 0
+        self.options = {"s1_return": s1_return, "s2_return": s2_return, "saa": saa, "peer": self.peer,
+                        "fused_ffn": self.fused_ffn}
         bf, f32 = dict(dtype=torch.bfloat16, device=self.dev), dict(dtype=torch.float32, device=self.dev)
         self.ranks = list(self.world.ranks)
         self.st: dict[int, RankState] = {}
@@ -203,6 +207,7 @@ class MoELayer:
                                    torch.zeros(d.e_local, d.Mp, d.Hsp, **f32))
         self._last: str | None = None
         self._ws_gate = None
+        self._ws_gemm: dict[int, torch.Tensor] = {}   # per rank: tile queue + completion counters (kept zeroed)
         self._trace: CommTrace | None = None
         self.last_trace: CommTrace | None = None      # records of the last forward's exchanges
 
@@ -369,13 +374,38 @@ class MoELayer:
         K.combine_bwd_dispatch(dout, yv, rt.expert_idx, rt.slot_idx, rt.probs, rt.combine_w, dlogits, slot_lo,
                                rt.fill, out=out, dst=dst, slots_out=slots_out)
 
+    def _gemm_ws(self, rank: int, gemms: list) -> torch.Tensor:
+        need = K.gemm_multi_workspace(gemms)
+        ws = self._ws_gemm.get(rank)
+        if ws is None or ws.numel() * 4 < need:
+            ws = self._ws_gemm[rank] = torch.zeros(max(need // 4, 64), dtype=torch.int32, device=self.dev)
+        return ws
+
     def _ffn_fwd(self, s: RankState, b: dict, y_peer: tuple | None = None) -> None:
-        K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=b["fill_in"])
-        K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=b["fill_in"], peer=y_peer)
+        """H = relu(R W1) (+ the H > 0 bit mask), Y = H W2 (dataplane.py:122-128): one persistent
+        launch, each Y row-pair tile starting once its H row pair is stored."""
+        f = b["fill_in"]
+        if self.fused_ffn:
+            gs = [K.Gemm.row(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=f),
+                  K.Gemm.row(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=f)]
+            K.gemm_multi(gs, [None, (K.DEP_ROW_PAIR, 0)], self._gemm_ws(s.rank, gs), peer=y_peer, seg_prob=1)
+            return
+        K.gemm_rows(b["recv"], s.w1t, K.KMAJOR, b["h"], K.EPI_RELU_MASK, aux=b["hmask"], fill=f)
+        K.gemm_rows(b["h"], s.w2t, K.KMAJOR, b["y"], K.EPI_BF16, fill=f, peer=y_peer)
 
     def _ffn_bwd(self, s: RankState, b: dict, wscale: float = 1.0, dr_peer: tuple | None = None) -> None:
+        """dH = (dY W2^T) . [H > 0], dW2^T = dY^T H, dR = dH W1^T, dW1^T = dH^T R: one persistent
+        launch in that queue order (dW2 has no dependency and fills in while dH rows complete)."""
         f = b["fill_in"]
         # ReLU' from the bit mask the forward GEMM wrote (1/16 of re-reading H)
+        if self.fused_ffn:
+            gs = [K.Gemm.row(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DMASK, aux=b["hmask"], fill=f),
+                  K.Gemm.wgrad(b["dyrecv"], b["h"], s.dw2t, K.EPI_F32, fill=f, alpha=wscale),
+                  K.Gemm.row(b["dh"], s.w1t, K.MNMAJOR, b["dr"], K.EPI_BF16, fill=f),
+                  K.Gemm.wgrad(b["dh"], b["recv"], s.dw1t, K.EPI_F32, fill=f, alpha=wscale)]
+            K.gemm_multi(gs, [None, None, (K.DEP_ROW_PAIR, 0), (K.DEP_COL_BLOCK, 0)], self._gemm_ws(s.rank, gs),
+                         peer=dr_peer, seg_prob=2)
+            return
         K.gemm_rows(b["dyrecv"], s.w2t, K.MNMAJOR, b["dh"], K.EPI_DMASK, aux=b["hmask"], fill=f)
         K.gemm_wgrad(b["dyrecv"], b["h"], s.dw2t, K.EPI_F32, fill=f, alpha=wscale)
         K.gemm_wgrad(b["dh"], b["recv"], s.dw1t, K.EPI_F32, fill=f, alpha=wscale)

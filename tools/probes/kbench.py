@@ -68,8 +68,14 @@ def main():
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--f", type=float, default=1.2)
     a = ap.parse_args()
-    if a.lib:
-        _lib._lib = _lib.load(a.lib)
+    if a.lib:   # any build, also of another ABI version: type only the symbols it has
+        import ctypes
+        lib = ctypes.CDLL(a.lib)
+        for name, (res, args) in _lib.SIGNATURES.items():
+            fn = getattr(lib, name, None)
+            if fn is not None:
+                fn.restype, fn.argtypes = res, args
+        _lib._lib = lib
     dev = torch.device("cuda", 0)
     n, M, E, k = a.n, a.M, a.E, a.k
     cap = -(-int(a.f * k * n) // E)
