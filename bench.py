@@ -486,11 +486,16 @@ def gemm_roofline(layer, schedule, xs, ds, steps, dist, dev):
     b = layer.st[r].bufs[schedule if d.P > 1 else "_local"]
     useful_rows = int((b["recv"].abs().amax(dim=-1) > 0).sum().item())   # real (kept) assignment rows
     alg_flops_step = 6 * 2 * useful_rows * d.M * d.Hs                   # 6 GEMMs per step (fwd 2, bwd 4)
-    per_launch_alg = alg_flops_step / 6
+    per_step = launches / steps                                         # 2 when fused (fwd pair, bwd four)
+    per_launch_alg = alg_flops_step / per_step
     avg_ms = ms / launches
-    return {"kernel": "moe_gemm_pair_kernel (tcgen05.mma.cta_group::2 kind::f16, TMA, TMEM)", "avg_launch_ms": avg_ms,
-            "alg_flops_per_launch": per_launch_alg, "capacity_flops_per_launch": padded_flops / launches,
-            "launches": launches, "useful_rows": useful_rows, "gemm_ms_per_step": ms / steps}
+    return {"kernel": "moe_gemm_pair_kernel (tcgen05.mma.cta_group::2 kind::f16, TMA, TMEM; "
+                      + ("forward pair and backward four as one persistent launch each)" if layer.fused_ffn
+                         else "one launch per GEMM)"),
+            "avg_launch_ms": avg_ms, "alg_flops_per_launch": per_launch_alg,
+            "capacity_flops_per_launch": padded_flops / launches, "launches": launches,
+            "launches_per_step": per_step, "useful_rows": useful_rows, "gemm_ms_per_step": ms / steps,
+            "alg_flops_per_step": alg_flops_step}
 
 
 def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
@@ -611,8 +616,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     achieved = roof["alg_flops_per_launch"] / (roof["avg_launch_ms"] / 1e3) / 1e12
     traffic = None
     tfile = ROOT / "profiles" / "gemm_traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+    if tfile.exists():   # ncu dram bytes per launch of the same launch structure (fused or one per GEMM)
+        tj = json.loads(tfile.read_text())
+        traffic = tj.get("dram_bytes_per_launch_fused" if layer.fused_ffn else "dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "frac_burst": achieved / burst, "frac_sustained": achieved / sustained,
                 "traffic": traffic, "peak_source": peak_src, "kernel": roof["kernel"],
@@ -621,7 +627,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
                 "timing": "CUDA events around each GEMM launch on the launching stream, launches queued behind a "
                           "device sleep (no host gaps inside the intervals)",
                 "gemm_share_of_step": roof["gemm_ms_per_step"] / ms,
-                "units": "alg FLOPs = 2 * kept assignment rows * M * (H/N_ESP) per GEMM; 6 GEMMs per step"}
+                "launches_per_step": roof["launches_per_step"],
+                "units": "alg FLOPs = 2 * kept assignment rows * M * (H/N_ESP) per GEMM; 6 GEMMs per step "
+                         "in launches_per_step launches"}
     roofline["layer"] = layer_roofline(cfg, layout, schedule, ms, peak, peaks_hbm())
     cpu = None
     if not args.no_cpu_baseline and world == 1:
