@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kGateThreads) gate_fwd_kernel(const bf16* __re
 // Scores (softmax in f64 of these logits) differ from the oracle's by the logit error, ~1e-7
 // relative for typical inputs.
 constexpr double kGateEps = 1.0 / 131072.0;   // 2^-17
-constexpr int kGmRJ = 16;                     // 32-column groups per load round (16 x 16-B loads in flight / lane)
+constexpr int kGmRJ = 8;                      // 32-column groups per load round (8 x 16-B loads in flight / lane)
+constexpr int kGmMaxPairs = 7;                // warp pairs per CTA (448 threads: <= 146 registers)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
@@ -171,99 +172,169 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Per-warp epilogue scratch: logits, scores (f64) and bounds (f32) of the warp's 8 tokens.
+// Per warp pair (one 8-token tile): the two column halves' partial sums, then the tile's logits,
+// scores, bounds and ranks.
 template <int NM>
-struct GateScratch {
+struct GateTile {
+    double part[2][8][16 * NM];
+    float bpart[2][8][16 * NM];
     double lg[8][16 * NM];
     double sc[8][16 * NM];
     float bd[8][16 * NM];
+    int rk[8][16 * NM];
 };
 
-// Softmax + stable top-k of the 8 tokens in sc: lane (t = lane / 4, r = lane % 4) owns experts
-// r, r + 4, ...  Returns (audit) the mask of tokens whose ranking the bounds do not certify.
+// Softmax + stable top-k of the 4 tokens 4h..4h+3 of the tile: lane (t = lane / 8, r = lane % 8)
+// owns experts r, r + 8, ...  Returns (audit) the mask of those tokens (bit t) whose ranking the
+// bounds do not certify.
 template <int NM>
-__device__ __forceinline__ unsigned gate_rank(GateScratch<NM>& s, int lane, int E, int k, bool audit,
-                                              int (&rank)[4 * NM]) {
-    constexpr int EP = 16 * NM, U = EP / 4;
-    const int t = lane >> 2, r = lane & 3;
+__device__ __forceinline__ unsigned gate_rank4(GateTile<NM>& s, int lane, int h, int E, int k, bool audit,
+                                               int (&rank)[2 * NM]) {
+    constexpr int EP = 16 * NM, U = EP / 8;
+    const int t = 4 * h + (lane >> 3), r = lane & 7;
     double ex[U];
     double mx = -INFINITY;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (r + 4 * u < E) mx = fmax(mx, s.lg[t][r + 4 * u]);
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        if (r + 8 * u < E) mx = fmax(mx, s.lg[t][r + 8 * u]);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     double sum = 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        ex[u] = (r + 4 * u < E) ? exp(s.lg[t][r + 4 * u] - mx) : 0.0;
+        ex[u] = (r + 8 * u < E) ? exp(s.lg[t][r + 8 * u] - mx) : 0.0;
         sum += ex[u];
     }
-    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (r + 4 * u < E) s.sc[t][r + 4 * u] = ex[u] / sum;
+        if (r + 8 * u < E) s.sc[t][r + 8 * u] = ex[u] / sum;
     __syncwarp();
     bool unsure = false;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int e = r + 4 * u;
+        const int e = r + 8 * u;
         rank[u] = EP;
         if (e >= E) continue;
         const double se = s.sc[t][e];
         int rk = 0;
-        for (int e2 = 0; e2 < E; ++e2) {
+#pragma unroll
+        for (int e2 = 0; e2 < EP; ++e2) {   // compile-time trip count: the shared loads pipeline
+            if (e2 >= E) break;
             const double so = s.sc[t][e2];
             rk += (so > se) || (so == se && e2 < e);
         }
         rank[u] = rk;
         if (audit && rk < k) {   // a pick must be separated from every other expert by the two bounds
             const double le = s.lg[t][e], be = (double)s.bd[t][e];
-            for (int e2 = 0; e2 < E; ++e2)   // (equal scores: decided by the exact path too)
+#pragma unroll
+            for (int e2 = 0; e2 < EP; ++e2) {   // (equal scores: decided by the exact path too)
+                if (e2 >= E) break;
                 unsure |= e2 != e && (fabs(le - s.lg[t][e2]) <= be + (double)s.bd[t][e2] || s.sc[t][e2] == se);
+            }
         }
     }
     const unsigned b = __ballot_sync(0xffffffffu, unsure);
     unsigned tokens = 0;
 #pragma unroll
-    for (int tt = 0; tt < 8; ++tt) tokens |= ((b >> (4 * tt)) & 0xFu) ? (1u << tt) : 0u;
+    for (int tt = 0; tt < 4; ++tt) tokens |= ((b >> (8 * tt)) & 0xFFu) ? (1u << tt) : 0u;
     return tokens;
 }
 
+#ifdef PARM_GATE_TRACE   // phase timestamps per CTA (tools/probes/gate_trace.py; variant builds only)
+__device__ unsigned long long g_gate_trace[kNumSMs * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GATE_MARK(i) \
+    if (threadIdx.x == 0 && blockIdx.x < kNumSMs) g_gate_trace[blockIdx.x * 8 + (i)] = gtime()
+#else
+#define GATE_MARK(i)
+#endif
+
+// Exact f64 logits of one token (the audit's recompute; a warp, rare): four experts per pass over
+// the row, every product exact, sums in a fixed order (lane partials in column order, then a lane-0
+// tree) -- the same for every expert, so equal gate columns give equal logits.
+__device__ __forceinline__ void gate_exact_logits(const bf16* __restrict__ xr, const unsigned char* smem, int rowb,
+                                               int lane, int E, int M, double* lg) {
+    for (int e0 = 0; e0 < E; e0 += 4) {   // four experts per pass over the row (x loads shared)
+        double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int c = 8 * lane; c < M; c += 256) {
+            const int4 xv = __ldg(reinterpret_cast<const int4*>(xr + c));
+            const uint32_t xs[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (e0 + u >= E) break;
+                const int4 wv = *reinterpret_cast<const int4*>(smem + (size_t)(e0 + u) * rowb + 2 * c);
+                const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    p[u] = fma((double)__uint_as_float(xs[w] << 16), (double)__uint_as_float(ws[w] << 16), p[u]);
+                    p[u] = fma((double)__uint_as_float(xs[w] & 0xFFFF0000u),
+                               (double)__uint_as_float(ws[w] & 0xFFFF0000u), p[u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[u] += __shfl_down_sync(0xffffffffu, p[u], o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lane == 0 && e0 + u < E) lg[e0 + u] = p[u];
+    }
+}
+
+__device__ __forceinline__ void pair_sync(int pw) { asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory"); }
+
+// One warp PAIR per 8-token tile: warp h of the pair sums column groups [h nj/2, (h+1) nj/2)
+// (more warps in flight per SM than one warp per tile: the kernel is latency-bound), the
+// partials meet in shared memory in a fixed order, and each warp ranks 4 of the tile's tokens.
 template <int NM>
-__global__ void __launch_bounds__(256) gate_fwd_mma_kernel(const bf16* __restrict__ x, long long ldx,
-                                                           const bf16* __restrict__ wg, int n, int M, int E, int k,
-                                                           int* __restrict__ expert_idx, float* __restrict__ combine_w,
-                                                           float* __restrict__ probs, int* __restrict__ counts) {
-    constexpr int EP = 16 * NM, U = EP / 4;
+__global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf16* __restrict__ x, long long ldx,
+                                                                        const bf16* __restrict__ wg, int n, int M,
+                                                                        int E, int k, int* __restrict__ expert_idx,
+                                                                        float* __restrict__ combine_w,
+                                                                        float* __restrict__ probs,
+                                                                        int* __restrict__ counts) {
+    constexpr int EP = 16 * NM, U = EP / 8;
     extern __shared__ __align__(16) unsigned char smem[];
     const int rowb = 2 * M + 64;   // staged Wg^T row: 64-byte pad spreads the 8 g-rows over all banks
-    const int wpc = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, q = lane & 3;
     const size_t absoff = (size_t)EP * rowb;   // |Wg^T| rows follow the Wg^T rows
-    GateScratch<NM>& s = reinterpret_cast<GateScratch<NM>*>(smem + 2 * absoff)[warp];
+    const int npairs = blockDim.x >> 6;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pw = warp >> 1, h = warp & 1;
+    const int g = lane >> 2, q = lane & 3;
+    GateTile<NM>& s = reinterpret_cast<GateTile<NM>*>(smem + 2 * absoff)[pw];
     const int tiles = (n + 7) / 8;
-    const int nj = M / 32;
-    const int rounds = (nj + kGmRJ - 1) / kGmRJ;
-    int tile = blockIdx.x * wpc + warp;
-    const int stride = gridDim.x * wpc;
+    const int nj = M / 32, nj0 = nj / 2;
+    const int jb = h ? nj0 : 0, njh = h ? nj - nj0 : nj0;   // this warp's column groups
+    const int rounds = (njh + kGmRJ - 1) / kGmRJ;
+    int tile = blockIdx.x * npairs + pw;
+    const int stride = gridDim.x * npairs;
+    GATE_MARK(0);
 
-    // x loads are unconditional (rows clamped to n - 1, groups to nj - 1; the extra rows and groups
-    // are never used), so no select waits on a load right after it is issued
+    // x loads are unconditional (rows clamped to n - 1, groups to the half's last; the extra rows
+    // and groups are never used), so no select waits on a load right after it is issued
     int4 bufA[kGmRJ], bufB[kGmRJ];
     auto load_round = [&](int4 (&dst)[kGmRJ], int tl, int rd) {
-        const bf16* src = x + (long long)min(tl * 8 + g, n - 1) * ldx + 8 * q;
+        const bf16* src = x + (long long)min(tl * 8 + g, n - 1) * ldx + 8 * q + 32 * jb;
 #pragma unroll
         for (int jj = 0; jj < kGmRJ; ++jj)
-            dst[jj] = __ldg(reinterpret_cast<const int4*>(src + 32 * min(rd * kGmRJ + jj, nj - 1)));
+            dst[jj] = __ldg(reinterpret_cast<const int4*>(src + 32 * min(rd * kGmRJ + jj, njh - 1)));
     };
-    if (tile < tiles) load_round(bufA, tile, 0);   // first x loads in flight before the Wg staging barrier
+    if (tile < tiles) {   // the first tile's first two rounds in flight before the Wg staging barrier
+        load_round(bufA, tile, 0);
+        if (rounds > 1) load_round(bufB, tile, 1);
+    }
 
     // Wg^T (E, M) -> shared rows 0..EP-1 (rows >= E zero), and |Wg^T| at absoff (the bound's operand),
-    // eight 16-byte loads in flight per thread
-    constexpr int kU = 8;
+    // four 16-byte loads in flight per thread
+    constexpr int kU = 4;   // (the first tile's x rounds are already live in registers)
     const int c8n = M / 8;
     const int units = EP * c8n;
     for (int u0 = 0; u0 < units; u0 += kU * blockDim.x) {
@@ -287,26 +358,25 @@ __global__ void __launch_bounds__(256) gate_fwd_mma_kernel(const bf16* __restric
         }
     }
     __syncthreads();
+    GATE_MARK(1);
 
     bool first_tile = true;
     for (; tile < tiles; tile += stride) {
-        // independent accumulator chains (by j parity) so consecutive groups' MMAs and adds overlap
-        double acc[2][NM][4];
+        // two |.| accumulator chains (by group parity): the HMMA chain is the long dependency
+        double acc[NM][4];
         float dab[2][NM][4];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int m = 0; m < NM; ++m)
 #pragma unroll
-            for (int m = 0; m < NM; ++m)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    acc[c][m][i] = 0.0;
-                    dab[c][m][i] = 0.0f;
-                }
+            for (int i = 0; i < 4; ++i) {
+                acc[m][i] = 0.0;
+                dab[0][m][i] = dab[1][m][i] = 0.0f;
+            }
         auto compute = [&](const int4 (&cur)[kGmRJ], int rd) {
 #pragma unroll
             for (int jj = 0; jj < kGmRJ; ++jj) {
-                const int j = rd * kGmRJ + jj;
-                if (j >= nj) break;
+                if (rd * kGmRJ + jj >= njh) break;
+                const int j = jb + rd * kGmRJ + jj;
                 const uint32_t xw[4] = {(uint32_t)cur[jj].x, (uint32_t)cur[jj].y, (uint32_t)cur[jj].z,
                                         (uint32_t)cur[jj].w};
                 uint32_t xa[4];
@@ -314,105 +384,115 @@ __global__ void __launch_bounds__(256) gate_fwd_mma_kernel(const bf16* __restric
                 for (int w = 0; w < 4; ++w) xa[w] = xw[w] & 0x7FFF7FFFu;
 #pragma unroll
                 for (int m = 0; m < NM; ++m) {
-                    const uint4 wa = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g) * rowb + 64 * j + 16 * q);
-                    const uint4 wb =
-                        *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g + 8) * rowb + 64 * j + 16 * q);
+                    const unsigned char* ra = smem + (size_t)(16 * m + g) * rowb + 64 * j + 16 * q;
+                    const unsigned char* rb = ra + 8 * (size_t)rowb;
+                    const uint4 wa = *reinterpret_cast<const uint4*>(ra);
+                    const uint4 wb = *reinterpret_cast<const uint4*>(rb);
                     float d[4] = {0.0f, 0.0f, 0.0f, 0.0f};
                     mma_bf16_16816(d, wa.x, wb.x, wa.y, wb.y, xw[0], xw[1]);
                     mma_bf16_16816(d, wa.z, wb.z, wa.w, wb.w, xw[2], xw[3]);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[jj & 1][m][i] += (double)d[i];
-                    const uint4 va = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g) * rowb + 64 * j + 16 * q +
-                                                                     absoff);
-                    const uint4 vb = *reinterpret_cast<const uint4*>(smem + (size_t)(16 * m + g + 8) * rowb + 64 * j +
-                                                                     16 * q + absoff);
+                    for (int i = 0; i < 4; ++i) acc[m][i] += (double)d[i];
+                    const uint4 va = *reinterpret_cast<const uint4*>(ra + absoff);
+                    const uint4 vb = *reinterpret_cast<const uint4*>(rb + absoff);
                     mma_bf16_16816(dab[jj & 1][m], va.x, vb.x, va.y, vb.y, xa[0], xa[1]);
                     mma_bf16_16816(dab[jj & 1][m], va.z, vb.z, va.w, vb.w, xa[2], xa[3]);
                 }
             }
         };
-        if (!first_tile) load_round(bufA, tile, 0);
-        first_tile = false;
-        for (int rd = 0; rd < rounds; rd += 2) {   // ping-pong: the next round's loads fly during this one
-            if (rd + 1 < rounds) load_round(bufB, tile, rd + 1);
+        if (!first_tile) {   // (the first tile's two rounds were issued before the staging barrier)
+            load_round(bufA, tile, 0);
+            if (rounds > 1) load_round(bufB, tile, 1);
+        }
+        for (int rd = 0; rd < rounds; rd += 2) {   // bufA holds round rd, bufB round rd + 1: ping-pong
             compute(bufA, rd);
+            if (rd + 2 < rounds) load_round(bufA, tile, rd + 2);
             if (rd + 1 < rounds) {
-                if (rd + 2 < rounds) load_round(bufA, tile, rd + 2);
                 compute(bufB, rd + 1);
+                if (rd + 3 < rounds) load_round(bufB, tile, rd + 3);
             }
         }
+        first_tile = false;
+        GATE_MARK(2);
         // D fragment: (expert 16m + g + 8 (i >> 1), token 2q + (i & 1))
 #pragma unroll
         for (int m = 0; m < NM; ++m)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int e = 16 * m + g + 8 * (i >> 1), tl = 2 * q + (i & 1);
-                s.lg[tl][e] = acc[0][m][i] + acc[1][m][i];
-                // the f32 sum S of |products| is itself rounded: 2^-10 covers it many times over
-                s.bd[tl][e] = (float)(kGateEps * ((double)dab[0][m][i] + (double)dab[1][m][i]) * (1.0 + 1.0 / 1024.0));
+                s.part[h][tl][e] = acc[m][i];
+                s.bpart[h][tl][e] = dab[0][m][i] + dab[1][m][i];
             }
+        pair_sync(pw);
+        {   // this warp's 4 tokens: halves summed in a fixed order (deterministic)
+            const int tl = 4 * h + (lane >> 3), r = lane & 7;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = r + 8 * u;
+                s.lg[tl][e] = s.part[0][tl][e] + s.part[1][tl][e];
+                // the f32 sums of |products| are themselves rounded: 2^-10 covers it many times over
+                s.bd[tl][e] = (float)(kGateEps * ((double)s.bpart[0][tl][e] + (double)s.bpart[1][tl][e]) *
+                                      (1.0 + 1.0 / 1024.0));
+            }
+        }
         __syncwarp();
         int rank[U];
-        unsigned redo = gate_rank<NM>(s, lane, E, k, true, rank);
         const int t0 = tile * 8;
-        redo &= (n - t0 >= 8) ? 0xFFu : ((1u << (n - t0)) - 1u);
+        const int live = min(8, n - t0) - 4 * h;                  // this warp's real tokens (may be <= 0)
+        GATE_MARK(3);
+        unsigned redo = gate_rank4<NM>(s, lane, h, E, k, true, rank);
+        GATE_MARK(4);
+        redo &= live >= 4 ? 0xFu : (live > 0 ? (1u << live) - 1u : 0u);
+#ifdef PARM_GATE_TRACE
+        if (lane == 0 && blockIdx.x < kNumSMs) atomicAdd(&g_gate_trace[blockIdx.x * 8 + 6], (unsigned long long)__popc(redo));
+#endif
+#ifdef PARM_GATE_TRACE
+        const unsigned long long tr0 = gtime();
+#endif
         if (redo) {   // exact f64 logits of the uncertified tokens (rare): fixed order, lane-0 tree sums
             for (unsigned rm = redo; rm; rm &= rm - 1) {
-                const int tl = __ffs(rm) - 1;
+                const int tl = 4 * h + __ffs(rm) - 1;
                 const bf16* xr = x + (long long)(t0 + tl) * ldx;
-                for (int e = 0; e < E; ++e) {
-                    double p = 0.0;
-                    for (int c = 8 * lane; c < M; c += 256) {
-                        const int4 xv = __ldg(reinterpret_cast<const int4*>(xr + c));
-                        const int4 wv = *reinterpret_cast<const int4*>(smem + (size_t)e * rowb + 2 * c);
-                        const uint32_t xs[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
-                        const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
-#pragma unroll
-                        for (int w = 0; w < 4; ++w) {
-                            p = fma((double)__uint_as_float(xs[w] << 16), (double)__uint_as_float(ws[w] << 16), p);
-                            p = fma((double)__uint_as_float(xs[w] & 0xFFFF0000u),
-                                    (double)__uint_as_float(ws[w] & 0xFFFF0000u), p);
-                        }
-                    }
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) p += __shfl_down_sync(0xffffffffu, p, o);
-                    if (lane == 0) s.lg[tl][e] = p;
-                }
+                gate_exact_logits(xr, smem, rowb, lane, E, M, &s.lg[tl][0]);
             }
             __syncwarp();
-            gate_rank<NM>(s, lane, E, k, false, rank);
+            gate_rank4<NM>(s, lane, h, E, k, false, rank);
+#ifdef PARM_GATE_TRACE
+            if (lane == 0 && blockIdx.x < kNumSMs) atomicMax(&g_gate_trace[blockIdx.x * 8 + 7], gtime() - tr0);
+#endif
         }
-        // outputs: lane (t, r) owns experts r + 4u of token t0 + t
-        const int t = lane >> 2, r = lane & 3;
-        const bool tok = t0 + t < n;
-        bool pick[U];
+        // outputs: lane (t, r) owns experts r + 8u of token t0 + 4h + t
+        const int tl = 4 * h + (lane >> 3), r = lane & 7;
+        const bool tok = t0 + tl < n;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int e = r + 4 * u;
-            pick[u] = tok && e < E && rank[u] < k;
+            const int e = r + 8 * u;
+            s.rk[tl][e] = (tok && e < E) ? rank[u] : EP;
             if (!tok || e >= E) continue;
-            const long long tt = t0 + t;
-            const float sc = (float)s.sc[t][e];
+            const long long tt = t0 + tl;
+            const float sc = (float)s.sc[tl][e];
             if (rank[u] < k) {
                 expert_idx[tt * k + rank[u]] = e;
                 combine_w[tt * k + rank[u]] = sc;
             }
             if (probs) probs[tt * E + e] = sc;
         }
-        if (counts != nullptr) {
+        pair_sync(pw);
+        if (counts != nullptr && h == 0 && lane < E) {   // per-tile pick counts of each expert
+            int c = 0;
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int rr = 0; rr < 4; ++rr) {   // expert rr + 4u: the lanes with r == rr
-                    const unsigned b = __ballot_sync(0xffffffffu, pick[u] && r == rr);
-                    const int e = rr + 4 * u;
-                    if (lane == 0 && e < E) counts[(long long)tile * E + e] = __popc(b);
-                }
+            for (int tt = 0; tt < 8; ++tt) c += s.rk[tt][lane] < k;
+            counts[(long long)tile * E + lane] = c;
         }
-        __syncwarp();   // scratch reused by the next tile
+        GATE_MARK(5);
     }
 }
 
+#ifdef PARM_GATE_TRACE
+extern "C" int parm_debug_gate_trace(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_gate_trace, sizeof(g_gate_trace));
+}
+#endif
 
 namespace gring {   // bulk-copy helpers (same protocol as permute.cu's rings)
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -618,24 +698,24 @@ static void launch_gate_fwd(const bf16* x, long long ldx, const bf16* wgT, int n
 
 size_t gate_counts_bytes(int n, int E) { return (size_t)((n + 7) / 8) * E * sizeof(int); }
 
-// Tensor-core gate configuration for (n, M, E): warps per CTA and shared memory, or false.
-static bool gate_mma_config(int n, int M, int E, int& wpc, size_t& smem) {
-    if (M % 32 != 0 || E > 32) return false;
+// Tensor-core gate configuration for (n, M, E): warp pairs per CTA and shared memory, or false.
+static bool gate_mma_config(int n, int M, int E, int& pairs, size_t& smem) {
+    if (M % 64 != 0 || E > 32) return false;
     const int NM = E > 16 ? 2 : 1;
-    const size_t scratch = (size_t)8 * 16 * NM * (8 + 8 + 4);
+    const size_t tile = NM == 1 ? sizeof(GateTile<1>) : sizeof(GateTile<2>);
     const int tiles = (n + 7) / 8;
-    // warps per CTA (one 8-token tile each at a time): fewest tiles on the busiest SM, most warps on ties
-    wpc = 8;
+    // pairs per CTA (one 8-token tile each at a time): fewest tiles on the busiest SM, most pairs on ties
+    pairs = kGmMaxPairs;
     long long best = -1;
-    for (int w = 8; w >= 4; --w) {
+    for (int w = kGmMaxPairs; w >= 2; --w) {
         const long long ctas = (tiles + w - 1) / w;
         const long long load = (ctas + kNumSMs - 1) / kNumSMs * w;
         if (best < 0 || load < best) {
             best = load;
-            wpc = w;
+            pairs = w;
         }
     }
-    smem = (size_t)2 * 16 * NM * (2 * M + 64) + (size_t)wpc * scratch;   // Wg^T, |Wg^T|, per-warp scratch
+    smem = (size_t)2 * 16 * NM * (2 * M + 64) + (size_t)pairs * tile;   // Wg^T, |Wg^T|, per-pair scratch
     return smem <= 227 * 1024;
 }
 
@@ -647,25 +727,25 @@ int gate_fwd(const void* x, long long ldx, const void* wgT, int n, int M, int E,
     if (n == 0) return 0;
     auto X = reinterpret_cast<const bf16*>(x);
     auto W = reinterpret_cast<const bf16*>(wgT);
-    int wpc = 0;
+    int pairs = 0;
     size_t smem = 0;
     if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(wgT) & 15) == 0 &&
-        gate_mma_config(n, M, E, wpc, smem)) {
+        gate_mma_config(n, M, E, pairs, smem)) {
         const int tiles = (n + 7) / 8;
-        const int blocks = (int)std::min<long long>((tiles + wpc - 1) / wpc, kNumSMs);
+        const int blocks = (int)std::min<long long>((tiles + pairs - 1) / pairs, kNumSMs);
         if (E <= 16) {
             cudaFuncSetAttribute(gate_fwd_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            launch_k(gate_fwd_mma_kernel<1>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
-                     probs, counts);
+            launch_k(gate_fwd_mma_kernel<1>, blocks, pairs * 64, smem, s, X, ldx, W, n, M, E, k, expert_idx,
+                     combine_w, probs, counts);
         } else {
             cudaFuncSetAttribute(gate_fwd_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            launch_k(gate_fwd_mma_kernel<2>, blocks, wpc * 32, smem, s, X, ldx, W, n, M, E, k, expert_idx, combine_w,
-                     probs, counts);
+            launch_k(gate_fwd_mma_kernel<2>, blocks, pairs * 64, smem, s, X, ldx, W, n, M, E, k, expert_idx,
+                     combine_w, probs, counts);
         }
         PARM_CHECK_LAUNCH("gate_fwd");
         return 0;
     }
-    // shapes the tensor-core gate does not take (M % 32 != 0, unaligned rows, very wide M): f64 FMA gate
+    // shapes the tensor-core gate does not take (M % 64 != 0, unaligned rows, very wide M): f64 FMA gate
     if (E <= 2)
         launch_gate_fwd<2>(X, ldx, W, n, M, E, k, expert_idx, combine_w, probs, s);
     else if (E <= 4)
