@@ -127,6 +127,13 @@ def measure(args) -> None:
                 for fk, fv in S.step_features(cfg, lay, s, comm).items():
                     row[f"{s}.{fk}"] = fv
             rows.append(row)
+            if rank == 0:   # incremental: a failing point later in the grid keeps the rows measured so far
+                new = not Path(args.out).exists() or len(rows) == 1
+                with open(args.out, "w" if len(rows) == 1 else "a", newline="") as fh:
+                    w = csv.DictWriter(fh, fieldnames=list(rows[0]))
+                    if new:
+                        w.writeheader()
+                    w.writerow(row)
             del layer
             if tr == "peer":
                 worlds[key].release()          # drop this layer's symmetric buffers (keeps the barrier's)
@@ -134,10 +141,6 @@ def measure(args) -> None:
             if rank == 0:
                 print(json.dumps(row), flush=True)
     if rank == 0:
-        with open(args.out, "w", newline="") as fh:
-            w = csv.DictWriter(fh, fieldnames=list(rows[0]))
-            w.writeheader()
-            w.writerows(rows)
         for tr in transports:
             summ = analyze([r for r in rows if r["transport"] == tr])
             print("SUMMARY " + tr + " " + json.dumps(summ), flush=True)
