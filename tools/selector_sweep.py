@@ -151,8 +151,23 @@ def measure(args) -> None:
 
 
 # ---------------------------------------------------------------- analysis (no GPU)
+_PROFILES: dict = {}
+
+
 def _feats(r: dict, s: str) -> dict:
-    return {f: float(r[f"{s}.{f}"]) for f in S.STEP_FEATURES}
+    """Step-model features of schedule s at sweep row r: from the CSV when it carries the current
+    feature set, else recomputed from the row's configuration and the calibrated profiles (so older
+    sweeps can be re-analysed with a newer model)."""
+    if all(f"{s}.{f}" in r for f in S.STEP_FEATURES):
+        return {f: float(r[f"{s}.{f}"]) for f in S.STEP_FEATURES}
+    if not _PROFILES:
+        _PROFILES["nccl"] = S.load_profile(ROOT / "profiles" / "nvlink_profile_p4.csv")
+        _PROFILES["peer"] = json.loads((ROOT / "profiles" / "peer_profile_p4.json").read_text())
+    cfg = MoEConfig(int(r["B"]), int(r["L"]), int(r["M"]), int(r["H"]), int(r["E"]), int(r["k"]), float(r["f"]))
+    lay = ParallelLayout(int(r["MP"]), int(r["EP"]), int(r["ESP"]), int(r["P"]))
+    comm = (S._comm_nccl(cfg, lay, s, _PROFILES["nccl"]) if (s == "baseline" or r["transport"] == "nccl")
+            else S._comm_peer(cfg, lay, s, _PROFILES["peer"]))
+    return S.step_features(cfg, lay, s, comm)
 
 
 def analyze(rows: list[dict], folds: int = 2) -> dict:
