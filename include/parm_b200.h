@@ -228,8 +228,8 @@ int parm_gemm(const parm_gemm_desc* desc, void* stream);
 int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long long dst_g_stride, long long dst_ld,
                    void* stream);
 
-/* Several GEMMs (1..4) as ONE persistent launch over a shared work queue of pair tiles: a CTA
- * pair claims its next tile from a device counter, so one GEMM's partial last wave is filled by
+/* Several GEMMs (1..4) as ONE persistent launch over one queue of pair tiles, problem after
+ * problem, walked round-robin by the resident CTA pairs: one GEMM's partial last wave is filled by
  * the next GEMM's tiles (the expert FFN's forward pair Y = relu(R W1) W2, or its backward
  * dH, dW2, dR, dW1 -- dataplane.py:122-128 and the adjoints).  deps (nullable): 2 ints per
  * problem, (kind, earlier problem):
@@ -237,8 +237,9 @@ int parm_gemm_peer(const parm_gemm_desc* desc, const parm_row_fan* seg_dst, long
  *                       problem's output over all its columns (waits for that pair's tiles);
  *   PARM_DEP_COL_BLOCK  WGT problem reads columns [256 p, 256 p + 256) of the earlier ROW
  *                       problem's output for every row of its group (p = its 256-row block).
- * Dependent and depended-on problems must share groups, segments, seg_len and fill.
- * ws: parm_gemm_multi_workspace() bytes, zeroed once by the caller; the kernel leaves it zeroed
+ * Dependent and depended-on problems must share groups, segments, seg_len and fill.  With
+ * dependencies the launch is cooperative (all CTAs resident) and needs ws:
+ * parm_gemm_multi_workspace() bytes, zeroed once by the caller; the kernel leaves it zeroed
  * (launches sharing a workspace must be stream-ordered).  seg_prob (-1: none): that problem's
  * outputs go to seg_dst as in parm_gemm_peer. */
 #define PARM_DEP_NONE 0

@@ -532,23 +532,26 @@ struct CfgPair {
 
 // ---------------------------------------------------------------- multi-problem persistent kernel
 // One launch runs up to kMaxProb GEMMs (the expert FFN's forward pair or its four backward
-// GEMMs) as ONE work queue of 256 x BN pair tiles, problem after problem.  Each CTA pair claims
-// its next tile from a global counter (the leader's producer thread) and broadcasts it through a
-// small shared-memory ring to its own MMA / epilogue warps and to the peer CTA, so a pair that
-// finishes early takes more tiles and the partial last wave of one GEMM is filled by the next
-// GEMM's tiles instead of idling (dR / Y have 256 tiles for 74 pairs: 3.46 waves).  A tile of a
-// dependent problem waits, before its first TMA load, for the tiles it reads:
+// GEMMs) as ONE queue of 256 x BN pair tiles, problem after problem, walked round-robin by the
+// persistent CTA pairs (pair p takes queue tiles p, p + pairs, ...): the partial last wave of one
+// GEMM is filled by the next GEMM's tiles instead of idling (Y / dR have 256 tiles for 74 pairs:
+// 3.46 waves), and the launch/drain of four kernels becomes one.  A tile of a dependent problem
+// waits, before its first TMA load, for the tiles it reads:
 //   kDepRowPair   ROW tile (g, pair) of problem i reads rows of the same pair of problem j
 //                 over all of j's columns (Y = H W2 after H; dR = dH W1^T after dH);
 //   kDepColBlock  WGT tile (g, m-pair) reads columns [256 m-pair, +256) of problem j's output
 //                 for every row of group g (dW1^T = dH^T R after dH).
 // Completion counters: every epilogue warp of a finished tile (8 per pair) waits for its bulk
-// stores, fences, and adds 1 to the (g, pair) and (g, column block) counters of its problem.
-// Tiles are claimed in queue order and only by running CTAs, so every tile a waiting CTA
-// depends on is held by a running CTA that never waits on a later tile: no deadlock without
-// co-residency.  The last CTA to exit zeroes the queue head and the counters for the next launch.
+// stores, fences, and adds 1 to the (g, pair) and (g, column block) counters of its problem --
+// deferred to the start of its next drain (by then the stores are done) unless that next tile is
+// itself a dependent one.
+// Deadlock freedom: each pair walks its tiles in increasing queue order and a tile only waits
+// on tiles of lower index, so by induction on the index every awaited tile is reached -- given
+// every pair is resident, which the host guarantees with a cooperative launch whenever the
+// launch has dependencies.  (A dynamic queue -- tiles claimed from a device counter and
+// broadcast to the pair through shared memory -- measured ~10% slower per step than this
+// static walk: tools/probes/step_ab.py.)  The last CTA to exit zeroes the counters.
 constexpr int kMaxProb = 4;
-constexpr int kSched = 4;          // depth of the tile broadcast ring
 enum Dep : int { kDepNone = 0, kDepRowPair = 1, kDepColBlock = 2 };
 
 struct Multi {
@@ -556,44 +559,9 @@ struct Multi {
     Params pr[kMaxProb];
     int nprob;
     int seg_prob;                  // problem whose ROW outputs go through SegMaps (-1: none)
-    int* ws;                       // [0] queue head, [1] exit count, [2 ...] completion counters
+    int* ws;                       // [0] unused, [1] exit count, [2 ...] completion counters (null: none)
     int ws_ints;                   // counters to clear at exit (from ws + 2)
 };
-
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {   // acquire at cluster scope
-    uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    const long long t0 = clock64();
-    while (true) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(parity)
-            : "memory");
-        if (done) break;
-        if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");
-    }
-}
-
-__device__ __forceinline__ void st_remote_u32(int* local_addr, uint32_t rank, int v) {
-    asm volatile(
-        "{\n\t.reg .b32 ra;\n\t"
-        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(local_addr)),
-        "r"(rank), "r"(v)
-        : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* bar, uint32_t rank) {
-    asm volatile(
-        "{\n\t.reg .b32 ra;\n\t"
-        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-        "r"(rank)
-        : "memory");
-}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -608,6 +576,29 @@ __device__ __forceinline__ void wait_counter(const int* c, int target) {
         if (clock64() - t0 > (8ll << 30)) asm volatile("trap;");
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");   // the TMA loads that follow see the data
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Completion counter (and its target) a tile of problem p waits on, or null.
+__device__ __forceinline__ int* dep_counter(const Multi& mp, const int* sfill, const Params& p, const PairTile& t,
+                                            int& target) {
+    if (p.dep == kDepRowPair) {
+        const Params& q = mp.pr[p.dep_on];
+        target = 8 * q.n_blocks;
+        return mp.ws + 2 + q.row_ctr + t.g * q.pairs + t.pj;
+    }
+    if (p.dep == kDepColBlock) {
+        const Params& q = mp.pr[p.dep_on];
+        const int* qp = sfill + q.prefix_off;
+        target = 8 * (qp[t.g + 1] - qp[t.g]);
+        return mp.ws + 2 + q.col_ctr + t.g * q.n_blocks + t.pj;
+    }
+    return nullptr;
 }
 
 // (problem, local tile) of queue index `tile` (sbase: prefix of the problems' tile counts)
@@ -728,11 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* empty_bar = full_bar + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint64_t* sfull_bar = tempty_bar + 2;
-    uint64_t* sempty_bar = sfull_bar + kSched;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty_bar + kSched);
-    int* stile = reinterpret_cast<int*>(tmem_slot + 1);          // kSched broadcast entries
-    int* sbase = stile + kSched;                                  // kMaxProb + 1 queue offsets
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    int* sbase = reinterpret_cast<int*>(tmem_slot + 1);          // kMaxProb + 1 queue offsets
     int* sfill = reinterpret_cast<int*>(smem + STAGES * C::kStageBytes + kBarBytes);
     uint8_t* smem_epi = smem + STAGES * C::kStageBytes + kBarBytes + kMaxFill * 4;   // 1024-aligned staging
     smem_epi = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_epi) + 1023) & ~uintptr_t(1023));
@@ -756,10 +744,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull_bar[s], 1);
             mbar_init(&tempty_bar[s], 2 * 128);   // both CTAs' epilogue threads (leader's copy used)
-        }
-        for (int s = 0; s < kSched; ++s) {
-            mbar_init(&sfull_bar[s], 1);          // the leader producer's (local or remote) arrival
-            mbar_init(&sempty_bar[s], 10);        // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -809,29 +793,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     const int total = sbase[nprob];
 
-    // Next tile of this pair: the leader producer claims and broadcasts; everyone else receives.
-    // Consumers: one arrival per warp on the leader's sempty after reading the entry.
-    // Static mode (mp.ws == null: one GEMM, no dependencies): pair p takes tiles p, p + pairs, ...
-    const bool dyn = mp.ws != nullptr;
+    // pair p takes queue tiles p, p + pairs, ... (every role computes the same sequence)
     const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
-    auto receive = [&](int& si, bool whole) -> int {
-        if (!dyn) {
-            const int tile = pair_id + si * num_pairs;
-            ++si;
-            return tile < total ? tile : total;
-        }
-        const int slot = si % kSched;
-        mbar_wait_cluster(&sfull_bar[slot], (si / kSched) & 1);
-        const int tile = *reinterpret_cast<volatile int*>(&stile[slot]);
-        if (whole) __syncwarp();
-        if (lane == 0) {
-            if (leader)
-                mbar_arrive(&sempty_bar[slot]);
-            else
-                mbar_arrive_remote_release(&sempty_bar[slot], 0);
-        }
+    auto next_tile = [&](int& si) -> int {
+        const int tile = pair_id + si * num_pairs;
         ++si;
-        return tile;
+        return tile < total ? tile : total;
     };
 
     if (warp == 0) {
@@ -840,29 +807,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int si = 0;
-            // claim one tile ahead: the atomic's round trip overlaps the current tile's loads
-            int claimed = (dyn && leader) ? atomicAdd(mp.ws, 1) : 0;
+            int pre_tile = -1, pre_val = 0;   // the next dependent tile's counter, read ahead
             while (true) {
-                int tile;
-                if (!dyn) {
-                    tile = receive(si, false);
-                } else if (leader) {
-                    tile = claimed;
-                    if (tile < total) claimed = atomicAdd(mp.ws, 1);
-                    const int slot = si % kSched;
-                    mbar_wait(&sempty_bar[slot], ((si / kSched) & 1) ^ 1);
-                    stile[slot] = tile;
-                    st_remote_u32(&stile[slot], 1, tile);
-                    mbar_arrive(&sfull_bar[slot]);
-                    mbar_arrive_remote_release(&sfull_bar[slot], 1);
-                    ++si;
-                } else {
-                    const int slot = si % kSched;
-                    mbar_wait_cluster(&sfull_bar[slot], (si / kSched) & 1);
-                    tile = *reinterpret_cast<volatile int*>(&stile[slot]);
-                    mbar_arrive_remote_release(&sempty_bar[slot], 0);
-                    ++si;
-                }
+                const int tile = next_tile(si);
                 if (tile >= total) break;
                 const int pi = find_prob(sbase, nprob, tile);
                 const Params p = mp.pr[pi];   // by value: registers, not param-space reloads after every asm clobber
@@ -870,13 +817,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const PairTile t = decode_pair(p, pf, tile - sbase[pi], BN, rank, sfill + p.prefix_off);
                 if (!t.live) continue;
 #ifndef PARM_GEMM_NO_DEPS   // (measurement variant only: dependent tiles do not wait -- wrong results)
-                if (p.dep == kDepRowPair) {
-                    const Params& q = mp.pr[p.dep_on];
-                    wait_counter(mp.ws + 2 + q.row_ctr + t.g * q.pairs + t.pj, 8 * q.n_blocks);
-                } else if (p.dep == kDepColBlock) {
-                    const Params& q = mp.pr[p.dep_on];
-                    const int* qp = sfill + q.prefix_off;
-                    wait_counter(mp.ws + 2 + q.col_ctr + t.g * q.n_blocks + t.pj, 8 * (qp[t.g + 1] - qp[t.g]));
+                int target = 0;
+                if (const int* ctr = dep_counter(mp, sfill, p, t, target)) {
+                    // the counter was read (relaxed) while the previous tile's loads were issued: when it
+                    // already showed the target, a fence makes that read an acquire -- no round trip here
+                    if (pre_tile == tile && pre_val >= target) {
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    } else {
+                        wait_counter(ctr, target);
+                    }
+                }
+                {   // prefetch the next tile's counter
+                    const int nt = pair_id + si * num_pairs;
+                    pre_tile = -1;
+                    if (nt < total) {
+                        const int npi = find_prob(sbase, nprob, nt);
+                        const Params& np = mp.pr[npi];
+                        if (np.dep != kDepNone) {
+                            const PairTile ntt = decode_pair(np, sfill + np.fill_off, nt - sbase[npi], BN, rank,
+                                                             sfill + np.prefix_off);
+                            int nt_target = 0;
+                            if (const int* nctr = dep_counter(mp, sfill, np, ntt, nt_target)) {
+                                pre_val = ld_relaxed(nctr);
+                                pre_tile = nt;
+                            }
+                        }
+                    }
                 }
 #endif
                 const CUtensorMap* tma = &mp.ta[pi];
@@ -901,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int it_tile = 0;
             int si = 0;
             while (true) {
-                const int tile = receive(si, false);
+                const int tile = next_tile(si);
                 if (tile >= total) break;
                 const int pi = find_prob(sbase, nprob, tile);
                 const Params p = mp.pr[pi];   // by value: registers, not param-space reloads after every asm clobber
@@ -933,14 +900,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int ebuf = 0;
         int si = 0;
         uint8_t* my_stage = smem_epi + ew * kEpiBufs * kEpiStageBytes;
+        // Completion of a depended-on tile is published one tile late -- when this warp starts its
+        // next drain its stores have long completed, so the wait is free -- except before a tile
+        // that itself waits on others (this warp's next tile could be waiting on this very
+        // signal) and at the end.
+        int* pend_row = nullptr;
+        int* pend_col = nullptr;
+        auto publish = [&]() {
+            if (pend_row != nullptr && lane == 0) {
+                bulk_wait_all();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                atomicAdd(pend_row, 1);
+                atomicAdd(pend_col, 1);
+            }
+            pend_row = pend_col = nullptr;
+        };
         while (true) {
-            const int tile = receive(si, true);
+            const int tile = next_tile(si);
             if (tile >= total) break;
             const int pi = find_prob(sbase, nprob, tile);
             const Params p = mp.pr[pi];   // by value (see the producer)
             const int* pf = sfill + p.fill_off;
             const PairTile t = decode_pair(p, pf, tile - sbase[pi], BN, rank, sfill + p.prefix_off);
             if (!t.live) continue;
+            if (p.dep != kDepNone) publish();
             const int as = it_tile & 1;
             const uint32_t aphase = (it_tile >> 1) & 1;
             ++it_tile;
@@ -952,6 +936,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
+            publish();
             const int row = t.m0 + ew * 32 + lane;
             const bool row_ok = (p.kind == kWgt) ? row < p.M : row < p.L;
             long long xrow = 0;
@@ -966,18 +951,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_arrive(&tempty_bar[as]);
             else
                 mbar_arrive_remote(&tempty_bar[as], 0);
-#ifdef PARM_GEMM_NO_DEPS
-            if (false) {
-#else
-            if (p.signal && lane == 0) {   // publish this warp's rows of the tile to dependent tiles
-#endif
-                bulk_wait_all();
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                __threadfence();
-                atomicAdd(mp.ws + 2 + p.row_ctr + t.g * p.pairs + t.pj, 1);
-                atomicAdd(mp.ws + 2 + p.col_ctr + t.g * p.n_blocks + t.n0 / BN, 1);
+#ifndef PARM_GEMM_NO_DEPS
+            if (p.signal) {   // this warp's rows of the tile, for dependent tiles (published later)
+                pend_row = mp.ws + 2 + p.row_ctr + t.g * p.pairs + t.pj;
+                pend_col = mp.ws + 2 + p.col_ctr + t.g * p.n_blocks + t.n0 / BN;
             }
+#endif
         }
+        publish();
         if (lane == 0) bulk_wait_all();
     }
 
@@ -989,7 +970,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      "r"((uint32_t)C::kTmemCols)
                      : "memory");
     }
-    if (dyn && threadIdx.x == 0) {   // the last CTA out resets the queue and the counters for the next launch
+    if (mp.ws != nullptr && threadIdx.x == 0) {   // the last CTA out resets the counters for the next launch
         __threadfence();
         if (atomicAdd(mp.ws + 1, 1) == (int)gridDim.x - 1) {
             for (int i = 0; i < mp.ws_ints; ++i) mp.ws[2 + i] = 0;
@@ -1145,8 +1126,9 @@ static size_t multi_workspace(const parm_gemm_desc* qs, int count) {
     return (size_t)ints * sizeof(int);
 }
 
+// coop: a cooperative launch (every CTA resident at once) -- required when tiles wait on others.
 template <int BN>
-static void launch_multi(const Multi& m, int grid, cudaStream_t stream) {
+static void launch_multi(const Multi& m, int grid, bool coop, cudaStream_t stream) {
     using C = CfgPair<BN>;
     auto kern = moe_gemm_pair_kernel<BN>;
     static bool attr_set = false;
@@ -1154,7 +1136,21 @@ static void launch_multi(const Multi& m, int grid, cudaStream_t stream) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
         attr_set = true;
     }
-    launch_k(kern, grid, kThreads, C::kSmemBytes, stream, m, g_segmaps);
+    if (!coop) {
+        launch_k(kern, grid, kThreads, C::kSmemBytes, stream, m, g_segmaps);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, m, g_segmaps);
 }
 
 // count GEMMs as one persistent launch.  deps: 2 ints per problem (kind, problem depended on) or null.
@@ -1164,8 +1160,9 @@ static void launch_multi(const Multi& m, int grid, cudaStream_t stream) {
 static int run_multi(const parm_gemm_desc* qs, int count, const int* deps, int* ws, size_t ws_bytes, int seg_prob,
                      const RowFan* seg_dst, long long sd_g, long long sd_ld, cudaStream_t stream) {
     PARM_CHECK_ARG(count >= 1 && count <= kMaxProb, "gemm: %d problems (1..%d per launch)", count, kMaxProb);
-    PARM_CHECK_ARG(ws != nullptr || (count == 1 && (deps == nullptr || deps[0] == kDepNone)),
-                   "gemm: several problems or dependencies need a workspace");
+    bool any_dep = false;
+    for (int i = 0; deps != nullptr && i < count; ++i) any_dep |= deps[2 * i] != kDepNone;
+    PARM_CHECK_ARG(ws != nullptr || !any_dep, "gemm: dependencies need a workspace (completion counters)");
     PARM_CHECK_ARG(ws == nullptr || ws_bytes >= multi_workspace(qs, count), "gemm: workspace too small");
     Multi m;
     memset(&m, 0, sizeof(m));
@@ -1231,10 +1228,11 @@ static int run_multi(const parm_gemm_desc* qs, int count, const int* deps, int* 
     m.ws_ints = (int)ctr;
     long long pairs = ub < kNumSMs / 2 ? ub : kNumSMs / 2;   // clusters of 2 CTAs, one per TPC
     if (pairs < 1) pairs = 1;
+    if (!any_dep) m.ws = nullptr;
     if (bn == 256)
-        launch_multi<256>(m, (int)(2 * pairs), stream);
+        launch_multi<256>(m, (int)(2 * pairs), any_dep, stream);
     else
-        launch_multi<128>(m, (int)(2 * pairs), stream);
+        launch_multi<128>(m, (int)(2 * pairs), any_dep, stream);
     PARM_CHECK_LAUNCH("moe_gemm_pair");
     return 0;
 }

@@ -362,9 +362,10 @@ def gemm_multi_workspace(gemms: list) -> int:
 
 def gemm_multi(gemms: list, deps: list | None, ws: torch.Tensor, peer: tuple | None = None,
                seg_prob: int = -1) -> None:
-    """``gemms`` as one persistent launch over a shared tile queue (parm_gemm_multi).  ``deps``: per
-    problem None or (DEP_ROW_PAIR | DEP_COL_BLOCK, index of an earlier problem).  ``ws``: a zeroed
-    workspace of >= gemm_multi_workspace bytes that stays zeroed between launches.  ``peer``
+    """``gemms`` as one persistent launch over one tile queue (parm_gemm_multi).  ``deps``: per
+    problem None or (DEP_ROW_PAIR | DEP_COL_BLOCK, index of an earlier problem); with dependencies
+    the launch is cooperative.  ``ws``: a zeroed workspace of >= gemm_multi_workspace bytes that
+    stays zeroed between launches (the dependency counters).  ``peer``
     (addresses, g_stride, ld): problem ``seg_prob``'s outputs go to the owners' receive blocks."""
     n = len(gemms)
     arr = (_lib.GemmDescC * n)(*[g.desc for g in gemms])
