@@ -513,6 +513,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         import torch.distributed as tdist
 
+        # NCCL's own log lines (e.g. "NCCL version ..." when NCCL_DEBUG is set) go to stderr: stdout
+        # carries exactly one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
     cfg = MoEConfig(**C2)
