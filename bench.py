@@ -126,7 +126,7 @@ def run_reference_arm(args, rank: int, world: int) -> None:
                          "reference_anchor": reference_anchor()},
         "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def reference_anchor() -> dict | None:
@@ -513,9 +513,6 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         import torch.distributed as tdist
 
-        # NCCL's own log lines (e.g. "NCCL version ..." when NCCL_DEBUG is set) go to stderr: stdout
-        # carries exactly one JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
     cfg = MoEConfig(**C2)
@@ -662,15 +659,31 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         "launch_mode": "eager" if args.eager else "cuda_graph (one replay per step; NCCL calls captured)",
         "transport": transport,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one stdout line: the JSON result (written to the saved stdout; see main)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
-    # the one stdout line is the JSON result: NCCL's own log lines (e.g. "NCCL version ...",
-    # printed when NCCL_DEBUG is set in the environment) go to stderr
+    # stdout carries exactly one JSON line.  Everything else the process prints -- including
+    # libraries writing straight to file descriptor 1, such as NCCL's "NCCL version ..." when
+    # NCCL_DEBUG is set in the environment -- is sent to stderr: fd 1 is pointed at stderr for the
+    # whole run and the result goes to a saved copy of the original stdout.
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse_args()
     rank = int(os.environ.get("RANK", 0))
