@@ -210,8 +210,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
                                                                  const bf16* __restrict__ wgT, int n, int k, int E,
                                                                  int M, const __grid_constant__ RowFan dx,
                                                                  long long ldx) {
-    constexpr int KT = 2, R = KT * NP, STAGE = R * kCols + 64;   // + 32 f32 of logit gradients (as bf16 units)
-    static_assert(S >= 3, "token pairs need two stages in use plus one in flight");
+        constexpr int KT = 2, R = KT * NP, STAGE = R * kCols + 64;   // + 32 f32 of logit gradients (as bf16 units)
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     bf16* ring = reinterpret_cast<bf16*>(smem) + (size_t)warp * S * STAGE;
@@ -229,11 +228,9 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
             mine.load(base + lane * nw, k, slot_idx, expert_idx, nullptr, dr);
         else
             invalidate(mine);
-        // items in chunk-major order (item q = token q % ntok of chunk q / ntok), so consecutive
-        // items share their columns: token pairs share each gate-weight load of the dlogits . Wg^T term
         const int items = ntok * nch;
         auto issue = [&](int q) {
-            const int i = q % ntok, c0 = (q / ntok) * kCols;
+            const int i = q / nch, c0 = (q - i * nch) * kCols;
             const int cols = min(kCols, M - c0);
             const uint32_t qs = phase_base + q, st = qs % S;
             const PickB<KT> b = bcast(mine, i);
@@ -254,73 +251,53 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
                                      cols * 2, bar0 + 8 * st);
             }
         };
-        int issued = 0;
-        for (int q = 0; q < items;) {
-            const int i = q % ntok, c0 = (q / ntok) * kCols;
+        const int pre = items < S - 1 ? items : S - 1;
+        for (int q = 0; q < pre; ++q) issue(q);
+        for (int q = 0; q < items; ++q) {
+            if (q + S - 1 < items) issue(q + S - 1);
+            const int i = q / nch, c0 = (q - i * nch) * kCols;
             const int cols = min(kCols, M - c0);
-            const int nq = (i + 1 < ntok) ? 2 : 1;       // this token and the next one, same columns
-            // stages of items q .. q+nq-1 are in use; item q+S-1 refills the stage of item q-1
-            for (; issued < items && issued <= q + S - 1; ++issued) issue(issued);
-            float acc[2][2][8];
+            const uint32_t qs = phase_base + q, st = qs % S;
+            const PickB<KT> b = bcast(mine, i);
+            bar_wait(bar0 + 8 * st, (qs / S) & 1);
+            const bf16* sb = ring + st * STAGE;
+            float acc[2][8];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+                for (int u = 0; u < 8; ++u) acc[h][u] = 0.0f;
 #pragma unroll
-                    for (int v = 0; v < 8; ++v) acc[u][h][v] = 0.0f;
-            const bf16* sb0 = ring;
-            const bf16* sb1 = ring;
+            for (int p = 0; p < NP; ++p)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (u >= nq) break;
-                const uint32_t qs = phase_base + q + u, st = qs % S;
-                const PickB<KT> b = bcast(mine, i + u);
-                bar_wait(bar0 + 8 * st, (qs / S) & 1);
-                const bf16* sb = ring + st * STAGE;
-                if (u == 0) sb0 = sb; else sb1 = sb;
-#pragma unroll
-                for (int p = 0; p < NP; ++p)
-#pragma unroll
-                    for (int j = 0; j < KT; ++j) {
-                        if (b.sl[j] < 0) continue;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int c = lane * 8 + h * 256;
-                            if (c < cols) fma_bf16x8(acc[u][h], 1.0f, lds16(sb + (j * NP + p) * kCols + c));
-                        }
-                    }
-            }
-            if (gate) {
-                const float* dl0 = reinterpret_cast<const float*>(sb0 + R * kCols);
-                const float* dl1 = reinterpret_cast<const float*>(sb1 + R * kCols);
-#pragma unroll 4
-                for (int e = 0; e < E; ++e) {
-                    const float d0 = dl0[e], d1 = nq > 1 ? dl1[e] : 0.0f;
+                for (int j = 0; j < KT; ++j) {
+                    if (b.sl[j] < 0) continue;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane * 8 + h * 256;
-                        if (c < cols) {
-                            const int4 wv = ldg16(wgT + (long long)e * M + c0 + c);
-                            fma_bf16x8(acc[0][h], d0, wv);
-                            if (nq > 1) fma_bf16x8(acc[1][h], d1, wv);
-                        }
+                        if (c < cols) fma_bf16x8(acc[h], 1.0f, lds16(sb + (j * NP + p) * kCols + c));
+                    }
+                }
+            if (gate) {
+                const float* dl = reinterpret_cast<const float*>(sb + R * kCols);
+#pragma unroll 4
+                for (int e = 0; e < E; ++e) {
+                    const float d = dl[e];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane * 8 + h * 256;
+                        if (c < cols) fma_bf16x8(acc[h], d, ldg16(wgT + (long long)e * M + c0 + c));
                     }
                 }
             }
+            const long long t = base + i * nw;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (u >= nq) break;
-                const long long t = base + (i + u) * nw;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = lane * 8 + h * 256;
-                    if (c >= cols) continue;
-                    const Vec8 v8 = f32_to_vec8(acc[u][h]);
-                    for (int f = 0; f < dx.n; ++f) st_vec8(dx.ptr[f] + t * ldx + c0 + c, v8);
-                }
+            for (int h = 0; h < 2; ++h) {
+                const int c = lane * 8 + h * 256;
+                if (c >= cols) continue;
+                const Vec8 v8 = f32_to_vec8(acc[h]);
+                for (int f = 0; f < dx.n; ++f) st_vec8(dx.ptr[f] + t * ldx + c0 + c, v8);
             }
             __syncwarp();
-            q += nq;
         }
         phase_base += items;
     }
