@@ -255,40 +255,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define GATE_MARK(i)
 #endif
 
-// Exact f64 logits of one token (the audit's recompute; a warp, rare): four experts per pass over
-// the row, every product exact, sums in a fixed order (lane partials in column order, then a lane-0
-// tree) -- the same for every expert, so equal gate columns give equal logits.
-__device__ __forceinline__ void gate_exact_logits(const bf16* __restrict__ xr, const unsigned char* smem, int rowb,
-                                               int lane, int E, int M, double* lg) {
-    for (int e0 = 0; e0 < E; e0 += 4) {   // four experts per pass over the row (x loads shared)
-        double p[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-        for (int c = 8 * lane; c < M; c += 256) {
-            const int4 xv = __ldg(reinterpret_cast<const int4*>(xr + c));
-            const uint32_t xs[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (e0 + u >= E) break;
-                const int4 wv = *reinterpret_cast<const int4*>(smem + (size_t)(e0 + u) * rowb + 2 * c);
-                const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    p[u] = fma((double)__uint_as_float(xs[w] << 16), (double)__uint_as_float(ws[w] << 16), p[u]);
-                    p[u] = fma((double)__uint_as_float(xs[w] & 0xFFFF0000u),
-                               (double)__uint_as_float(ws[w] & 0xFFFF0000u), p[u]);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p[u] += __shfl_down_sync(0xffffffffu, p[u], o);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (lane == 0 && e0 + u < E) lg[e0 + u] = p[u];
-    }
-}
-
 __device__ __forceinline__ void pair_sync(int pw) { asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory"); }
 
 // One warp PAIR per 8-token tile: warp h of the pair sums column groups [h nj/2, (h+1) nj/2)
@@ -360,8 +326,21 @@ __global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf
     __syncthreads();
     GATE_MARK(1);
 
+    __shared__ int s_nflag[2];          // uncertified tokens of this round (parity double buffer)
+    __shared__ int s_ftok[2 * kGmMaxPairs * 4];
+    __shared__ double s_red[64][8];     // per-warp partial exact logits (<= 14 warps x 8 experts; 64 >= warps)
+    if (threadIdx.x == 0) s_nflag[0] = s_nflag[1] = 0;
+    __syncthreads();
     bool first_tile = true;
-    for (; tile < tiles; tile += stride) {
+    int parity = 0;
+    // CTA-uniform rounds (every pair of the CTA takes part in the exact-path barriers of each round)
+    for (int base = blockIdx.x * npairs; base < tiles; base += stride, parity ^= 1) {
+        tile = base + pw;
+        const bool active = tile < tiles;
+        unsigned redo = 0;
+        int rank[U];
+        const int t0 = tile * 8;
+        if (active) {
         // two |.| accumulator chains (by group parity): the HMMA chain is the long dependency
         double acc[NM][4];
         float dab[2][NM][4];
@@ -436,31 +415,62 @@ __global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf
             }
         }
         __syncwarp();
-        int rank[U];
-        const int t0 = tile * 8;
         const int live = min(8, n - t0) - 4 * h;                  // this warp's real tokens (may be <= 0)
         GATE_MARK(3);
-        unsigned redo = gate_rank4<NM>(s, lane, h, E, k, true, rank);
+        redo = gate_rank4<NM>(s, lane, h, E, k, true, rank);
         GATE_MARK(4);
         redo &= live >= 4 ? 0xFu : (live > 0 ? (1u << live) - 1u : 0u);
-#ifdef PARM_GATE_TRACE
-        if (lane == 0 && blockIdx.x < kNumSMs) atomicAdd(&g_gate_trace[blockIdx.x * 8 + 6], (unsigned long long)__popc(redo));
-#endif
-#ifdef PARM_GATE_TRACE
-        const unsigned long long tr0 = gtime();
-#endif
-        if (redo) {   // exact f64 logits of the uncertified tokens (rare): fixed order, lane-0 tree sums
-            for (unsigned rm = redo; rm; rm &= rm - 1) {
-                const int tl = 4 * h + __ffs(rm) - 1;
-                const bf16* xr = x + (long long)(t0 + tl) * ldx;
-                gate_exact_logits(xr, smem, rowb, lane, E, M, &s.lg[tl][0]);
+        if (lane == 0)
+            for (unsigned rm = redo; rm; rm &= rm - 1) s_ftok[atomicAdd(&s_nflag[parity], 1)] = (pw << 3) | (4 * h + __ffs(rm) - 1);
+        }   // active
+        if (threadIdx.x == 0) s_nflag[parity ^ 1] = 0;            // next round's list (see DESIGN: parity)
+        __syncthreads();
+        const int nflag = s_nflag[parity];
+        // Exact f64 logits of the uncertified tokens (rare), by the whole CTA: thread c handles the
+        // 8-column chunks c, c + blockDim, ... in order, warps reduce by a fixed shuffle tree, then the
+        // warp partials are added in warp order -- the same arithmetic for every expert, so equal gate
+        // columns give equal logits (exact ties, lower expert first).
+        for (int f = 0; f < nflag; ++f) {
+            const int fq = s_ftok[f] >> 3, ftl = s_ftok[f] & 7;
+            GateTile<NM>& fs = reinterpret_cast<GateTile<NM>*>(smem + 2 * absoff)[fq];
+            const bf16* xr = x + (long long)((base + fq) * 8 + ftl) * ldx;
+            for (int e0 = 0; e0 < E; e0 += 8) {
+                double pe[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                for (int c = 8 * threadIdx.x; c < M; c += 8 * blockDim.x) {
+                    const int4 xv = __ldg(reinterpret_cast<const int4*>(xr + c));
+                    const uint32_t xs[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (e0 + u >= E) break;
+                        const int4 wv = *reinterpret_cast<const int4*>(smem + (size_t)(e0 + u) * rowb + 2 * c);
+                        const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            pe[u] = fma((double)__uint_as_float(xs[w] << 16), (double)__uint_as_float(ws[w] << 16),
+                                        pe[u]);
+                            pe[u] = fma((double)__uint_as_float(xs[w] & 0xFFFF0000u),
+                                        (double)__uint_as_float(ws[w] & 0xFFFF0000u), pe[u]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) pe[u] += __shfl_down_sync(0xffffffffu, pe[u], o);
+                if (lane == 0)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) s_red[warp][u] = pe[u];
+                __syncthreads();
+                if (threadIdx.x < 8 && e0 + threadIdx.x < E) {
+                    double v = 0.0;
+                    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += s_red[w][threadIdx.x];
+                    fs.lg[ftl][e0 + threadIdx.x] = v;
+                }
+                __syncthreads();
             }
-            __syncwarp();
-            gate_rank4<NM>(s, lane, h, E, k, false, rank);
-#ifdef PARM_GATE_TRACE
-            if (lane == 0 && blockIdx.x < kNumSMs) atomicMax(&g_gate_trace[blockIdx.x * 8 + 7], gtime() - tr0);
-#endif
         }
+        if (active) {
+        if (redo) gate_rank4<NM>(s, lane, h, E, k, false, rank);   // the recomputed tokens, ranked exactly
         // outputs: lane (t, r) owns experts r + 8u of token t0 + 4h + t
         const int tl = 4 * h + (lane >> 3), r = lane & 7;
         const bool tok = t0 + tl < n;
@@ -485,6 +495,7 @@ __global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf
             counts[(long long)tile * E + lane] = c;
         }
         GATE_MARK(5);
+        }   // active
     }
 }
 
