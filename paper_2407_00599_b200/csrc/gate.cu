@@ -185,31 +185,49 @@ struct GateTile {
 };
 
 // Softmax + stable top-k of the 4 tokens 4h..4h+3 of the tile: lane (t = lane / 8, r = lane % 8)
-// owns experts r, r + 8, ...  Returns (audit) the mask of those tokens (bit t) whose ranking the
-// bounds do not certify.
-template <int NM>
-__device__ __forceinline__ unsigned gate_rank4(GateTile<NM>& s, int lane, int h, int E, int k, bool audit,
-                                               int (&rank)[2 * NM]) {
+// owns experts r, r + 8, ...
+//   EXACT = false (tensor-core logits): rank by the logits (ties -> lower expert) and return the
+//     mask of tokens (bit t) whose picks the bounds do not separate from every other expert --
+//     for the others this ranking is certified to be the exact one; scores in f32 math.
+//   EXACT = true (the recomputed exact logits): f64 softmax and the stable ranking of the f64
+//     scores, exactly the oracle's argsort(-scores, kind="stable").
+template <int NM, bool EXACT>
+__device__ __forceinline__ unsigned gate_rank4(GateTile<NM>& s, int lane, int h, int E, int k, int (&rank)[2 * NM]) {
     constexpr int EP = 16 * NM, U = EP / 8;
     const int t = 4 * h + (lane >> 3), r = lane & 7;
-    double ex[U];
     double mx = -INFINITY;
 #pragma unroll
     for (int u = 0; u < U; ++u)
         if (r + 8 * u < E) mx = fmax(mx, s.lg[t][r + 8 * u]);
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    double sum = 0.0;
+    if (EXACT) {
+        double ex[U];
+        double sum = 0.0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        ex[u] = (r + 8 * u < E) ? exp(s.lg[t][r + 8 * u] - mx) : 0.0;
-        sum += ex[u];
+        for (int u = 0; u < U; ++u) {
+            ex[u] = (r + 8 * u < E) ? exp(s.lg[t][r + 8 * u] - mx) : 0.0;
+            sum += ex[u];
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (r + 8 * u < E) s.sc[t][r + 8 * u] = ex[u] / sum;
+    } else {
+        float ex[U];
+        float sum = 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ex[u] = (r + 8 * u < E) ? expf((float)(s.lg[t][r + 8 * u] - mx)) : 0.0f;
+            sum += ex[u];
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (r + 8 * u < E) s.sc[t][r + 8 * u] = (double)(ex[u] / sum);
     }
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-        if (r + 8 * u < E) s.sc[t][r + 8 * u] = ex[u] / sum;
     __syncwarp();
     bool unsure = false;
 #pragma unroll
@@ -217,21 +235,21 @@ __device__ __forceinline__ unsigned gate_rank4(GateTile<NM>& s, int lane, int h,
         const int e = r + 8 * u;
         rank[u] = EP;
         if (e >= E) continue;
-        const double se = s.sc[t][e];
+        const double ke = EXACT ? s.sc[t][e] : s.lg[t][e];
         int rk = 0;
 #pragma unroll
         for (int e2 = 0; e2 < EP; ++e2) {   // compile-time trip count: the shared loads pipeline
             if (e2 >= E) break;
-            const double so = s.sc[t][e2];
-            rk += (so > se) || (so == se && e2 < e);
+            const double ko = EXACT ? s.sc[t][e2] : s.lg[t][e2];
+            rk += (ko > ke) || (ko == ke && e2 < e);
         }
         rank[u] = rk;
-        if (audit && rk < k) {   // a pick must be separated from every other expert by the two bounds
-            const double le = s.lg[t][e], be = (double)s.bd[t][e];
+        if (!EXACT && rk < k) {   // a pick must be separated from every other expert by the two bounds
+            const double be = (double)s.bd[t][e];
 #pragma unroll
-            for (int e2 = 0; e2 < EP; ++e2) {   // (equal scores: decided by the exact path too)
+            for (int e2 = 0; e2 < EP; ++e2) {   // (equal logits included: |diff| = 0)
                 if (e2 >= E) break;
-                unsure |= e2 != e && (fabs(le - s.lg[t][e2]) <= be + (double)s.bd[t][e2] || s.sc[t][e2] == se);
+                unsure |= e2 != e && fabs(ke - s.lg[t][e2]) <= be + (double)s.bd[t][e2];
             }
         }
     }
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf
         __syncwarp();
         const int live = min(8, n - t0) - 4 * h;                  // this warp's real tokens (may be <= 0)
         GATE_MARK(3);
-        redo = gate_rank4<NM>(s, lane, h, E, k, true, rank);
+        redo = gate_rank4<NM, false>(s, lane, h, E, k, rank);
         GATE_MARK(4);
         redo &= live >= 4 ? 0xFu : (live > 0 ? (1u << live) - 1u : 0u);
         if (lane == 0)
@@ -470,7 +488,13 @@ __global__ void __launch_bounds__(64 * kGmMaxPairs) gate_fwd_mma_kernel(const bf
             }
         }
         if (active) {
-        if (redo) gate_rank4<NM>(s, lane, h, E, k, false, rank);   // the recomputed tokens, ranked exactly
+        if (redo) {   // the recomputed tokens, ranked exactly (the certified ones keep their ranking)
+            int rank2[U];
+            gate_rank4<NM, true>(s, lane, h, E, k, rank2);
+            if ((redo >> (lane >> 3)) & 1u)
+#pragma unroll
+                for (int u = 0; u < U; ++u) rank[u] = rank2[u];
+        }
         // outputs: lane (t, r) owns experts r + 8u of token t0 + 4h + t
         const int tl = 4 * h + (lane >> 3), r = lane & 7;
         const bool tok = t0 + tl < n;
