@@ -1126,6 +1126,28 @@ static size_t multi_workspace(const parm_gemm_desc* qs, int count) {
     return (size_t)ints * sizeof(int);
 }
 
+// CTA pairs of the kernel that can be resident at once on this device (cached per instantiation).
+template <int BN>
+static int resident_pairs() {
+    static int pairs = -1;
+    if (pairs < 0) {
+        using C = CfgPair<BN>;
+        auto kern = moe_gemm_pair_kernel<BN>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(kNumSMs);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = C::kSmemBytes;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            clusters = 0;
+        }
+        pairs = clusters;
+    }
+    return pairs;
+}
+
 // coop: a cooperative launch (every CTA resident at once) -- required when tiles wait on others.
 template <int BN>
 static void launch_multi(const Multi& m, int grid, bool coop, cudaStream_t stream) {
@@ -1229,6 +1251,15 @@ static int run_multi(const parm_gemm_desc* qs, int count, const int* deps, int* 
     long long pairs = ub < kNumSMs / 2 ? ub : kNumSMs / 2;   // clusters of 2 CTAs, one per TPC
     if (pairs < 1) pairs = 1;
     if (!any_dep) m.ws = nullptr;
+    if (any_dep && pairs > (bn == 256 ? resident_pairs<256>() : resident_pairs<128>())) {
+        // the dependency waits need every pair resident; where the device cannot hold the grid at
+        // once, run the problems as stream-ordered single launches instead (same tiles, same results)
+        for (int i = 0; i < count; ++i)
+            if (int rc = run_multi(&qs[i], 1, nullptr, nullptr, 0, seg_prob == i ? 0 : -1, seg_dst, sd_g, sd_ld,
+                                   stream))
+                return rc;
+        return 0;
+    }
     if (bn == 256)
         launch_multi<256>(m, (int)(2 * pairs), any_dep, stream);
     else
