@@ -785,7 +785,11 @@ __global__ void peer_barrier_kernel(const __grid_constant__ PeerSignalSet set) {
     __syncthreads();
     const int j = threadIdx.x;
     if (j < sig.n) {
-        __threadfence_system();
+        // No leading system fence: the data this barrier publishes was written by the kernels before
+        // it on this stream, and a kernel completes only once its stores -- NVLink stores into peer
+        // memory included, and the TMA epilogues wait for their bulk stores -- are performed; the
+        // release store below then orders this rank's arrival after them (measured: 5.9 -> 4.5 us
+        // per barrier at P=2, 6.5 -> 4.9 at P=4, tools/probes/barrier_probe.py).
         unsigned* slot = reinterpret_cast<unsigned*>(sig.pad[j]) + sig.rank;
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
         const unsigned* mine = reinterpret_cast<const unsigned*>(sig.pad[sig.rank]) + j;
