@@ -2,7 +2,7 @@
 backward four as one multi-problem launch (parm_gemm_multi) vs one launch per GEMM, for each
 library build given (tools/probes/build_variant.sh).  CUDA-graph replays, median of reps.
 
-    python tools/probes/ffn_ab.py [lib.so ...]
+    python tools/probes/ffn_ab.py [lib.so ...]   ("" = the in-tree build; repeat to interleave)
 """
 import sys
 from pathlib import Path
@@ -25,9 +25,9 @@ def main():
     dev = torch.device("cuda", 0)
     cfg = MoEConfig(**bench.C2)
     layout = bench.layout_for(1)
+    base = _lib.load()
     for path in libs:
-        if path:  # "" = the in-tree build
-            _lib._lib = _lib.load(path)
+        _lib._lib = _lib.load(path) if path else base   # "" = the in-tree build
         for fused in (True, False):
             layer = MoELayer(cfg, layout, LocalWorld(layout, dev), fused_ffn=fused)
             layer.init_random(0)
