@@ -166,8 +166,11 @@ int parm_fan_copy(const void* src, long long bytes, const parm_row_fan* dst, voi
  * so ranks that wait on one another are co-resident by construction. */
 int parm_peer_barrier(const parm_peer_signal* sigs, int count, void* stream);
 
-/* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic two-pass).
- * accumulate != 0 adds into dwg. */
+/* Gate weight gradient, transposed: dWg^T (E, M) f32 = dlogits^T x (deterministic: per-SM
+ * partials summed in a fixed order, in the same launch behind a grid barrier when every CTA is
+ * resident).  accumulate != 0 adds into dwg.  workspace: parm_gate_wgrad_workspace() bytes,
+ * zeroed once by the caller (it ends with barrier counters the kernel leaves zeroed; launches
+ * sharing a workspace must be stream-ordered). */
 size_t parm_gate_wgrad_workspace(int n, int M, int E);
 /* out[i] (+)= sum_c src[c * len + i], chunks summed in a fixed order (deterministic): the S1
  * peer transport's MP gate-gradient partials, fanned out to every MP peer, reduced locally

@@ -56,6 +56,32 @@ inline void launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem,
     cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
 }
 
+// Cooperative launch (every CTA resident at once): for kernels with a grid-wide barrier.
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_coop(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                               Act&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+
+// Two f32 FMAs in one FFMA2 (sm_100): (a0, a1) += (x0, x1) * w, each rounded as fmaf.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float w) {
+    asm("{\n\t.reg .b64 ra, rx, rw;\n\t"
+        "mov.b64 ra, {%0, %1};\n\tmov.b64 rx, {%2, %3};\n\tmov.b64 rw, {%4, %4};\n\t"
+        "fma.rn.f32x2 ra, rx, rw, ra;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(x0), "f"(x1), "f"(w));
+}
+
 __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 
 // 16-byte vector of 8 bf16 values.

@@ -559,8 +559,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // a shared-memory ring with cp.async.bulk (one copy per stage when rows are contiguous) --
 // every byte of x requested at kernel start, no per-thread load latency on the critical
 // path -- and the range's logit gradients sit in shared memory (broadcast reads).  Thread =
-// 4 consecutive columns of a 1024-column block; f32 accumulation in token order; the
-// partials are summed in a fixed order by sum_partials_kernel (deterministic).
+// 4 consecutive columns of a 1024-column block; f32 accumulation in token order (FFMA2); the
+// partials are summed in a fixed order (deterministic) by the same launch after a grid barrier
+// when every CTA is resident (cooperative launch), else by sum_partials_kernel.
 constexpr int kWgThreads = 256;
 constexpr int kWgBlock = kWgThreads * 4;        // columns per pass
 constexpr int kWgMaxTok = 256;                  // tokens per CTA (host: grid >= n / 256)
@@ -572,7 +573,9 @@ constexpr int kWgStageBytes = 64 * 1024;
 template <int EMAX, int NB>   // 4 columns x EMAX experts per thread for NB column blocks (M <= NB * 1024)
 __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(const bf16* __restrict__ x, long long ldx,
                                                                         const float* __restrict__ dlogits, int n, int Mfull,
-                                                                        int E, float* __restrict__ part) {
+                                                                        int E, float* __restrict__ part,
+                                                                        float* __restrict__ out, int accumulate,
+                                                                        int* __restrict__ sync) {
     // blockIdx.y: this CTA's column slice [cbase, cbase + M) of the NB * 1024 columns it covers
     const int cbase = blockIdx.y * NB * kWgBlock;
     const int M = min(Mfull - cbase, NB * kWgBlock);
@@ -642,10 +645,8 @@ __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(cons
 #pragma unroll
                 for (int e = 0; e < EMAX; ++e) {
                     const float w = d[e];            // experts >= E: never stored below
-                    acc[b][e][0] = fmaf(w, f0, acc[b][e][0]);
-                    acc[b][e][1] = fmaf(w, f1, acc[b][e][1]);
-                    acc[b][e][2] = fmaf(w, f2, acc[b][e][2]);
-                    acc[b][e][3] = fmaf(w, f3, acc[b][e][3]);
+                    ffma2(acc[b][e][0], acc[b][e][1], f0, f1, w);
+                    ffma2(acc[b][e][2], acc[b][e][3], f2, f3, w);
                 }
             }
         }
@@ -674,6 +675,67 @@ __global__ void __launch_bounds__(2 * kWgThreads) gate_wgrad_partial_kernel(cons
             }
         }
         __syncthreads();
+    }
+    if (sync == nullptr) return;   // partials only: the host launches sum_partials_kernel
+    // ---- every CTA's partials stored (grid barrier: cooperative launch), then CTA i sums its
+    //      1/nb slice of the E x M outputs over the gridDim.x partials in a fixed order
+    //      (deterministic): lanes over outputs, warps over chunks w, w + 16, ..., warp sums in order
+    const int nb = gridDim.x * gridDim.y;
+    const int id = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(sync, 1);
+        const long long t_start = clock64();
+        int v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(sync) : "memory");
+            if (v >= nb) break;
+            __nanosleep(64);
+            if (clock64() - t_start > (8ll << 30)) asm volatile("trap;");
+        }
+    }
+    __syncthreads();
+    const long long len = (long long)E * Mfull;
+    const long long lo = len * id / nb, hi = len * (id + 1) / nb;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kRw = 2 * kWgThreads / 32;                   // 16 warps
+    constexpr int kRc = (kNumSMs + kRw - 1) / kRw;             // chunks per warp (gridDim.x <= kNumSMs here)
+    float* red = reinterpret_cast<float*>(sx);                 // [kRw][64]
+    const int chunks = gridDim.x;
+    for (long long i0 = lo; i0 < hi; i0 += 64) {              // 64 outputs per pass, every load in flight
+        float v[2][kRc];
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) {
+            const long long i = i0 + 32 * g2 + lane;
+#pragma unroll
+            for (int r = 0; r < kRc; ++r) {
+                const int c = warp + kRw * r;
+                v[g2][r] = (i < hi && c < chunks) ? __ldcg(part + (long long)c * len + i) : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int r = 0; r < kRc; ++r) sum += v[g2][r];
+            red[warp * 64 + 32 * g2 + lane] = sum;
+        }
+        __syncthreads();
+        if (warp < 2) {
+            const long long i = i0 + 32 * warp + lane;
+            if (i < hi) {
+                float tot = red[32 * warp + lane];
+#pragma unroll
+                for (int w = 1; w < kRw; ++w) tot += red[w * 64 + 32 * warp + lane];
+                out[i] = accumulate ? out[i] + tot : tot;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && atomicAdd(sync + 1, 1) == nb - 1) {   // last CTA out: counters back to zero
+        sync[0] = 0;
+        sync[1] = 0;
+        __threadfence();
     }
 }
 
@@ -805,9 +867,10 @@ static int gate_wgrad_grid(int n) {
     return std::max(g, (n + kWgMaxTok - 1) / kWgMaxTok);          // <= kWgMaxTok tokens per CTA
 }
 
-size_t gate_wgrad_workspace(int n, int M, int E) {
-    return (size_t)gate_wgrad_grid(n) * M * E * sizeof(float);
-}
+// partials, then two barrier counters (zero before first use; the kernel leaves them zero)
+static size_t gate_wgrad_part_bytes(int n, int M, int E) { return (size_t)gate_wgrad_grid(n) * M * E * sizeof(float); }
+
+size_t gate_wgrad_workspace(int n, int M, int E) { return gate_wgrad_part_bytes(n, M, E) + 4 * sizeof(int); }
 
 int sum_chunks(const float* src, int chunks, long long len, float* out, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(src != nullptr && out != nullptr && chunks >= 1 && len >= 0, "sum_chunks: bad arguments");
@@ -832,6 +895,8 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     auto X = reinterpret_cast<const bf16*>(x);
     const int smem = kWgStages * kWgStageBytes;
     const int nb = (M + kWgBlock - 1) / kWgBlock;
+    int* sync = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + gate_wgrad_part_bytes(n, M, E));
+    bool fused = false;   // the sum in the same launch when every CTA fits at once (1 CTA per SM)
     // column slices of NBV * 1024 columns over grid.y (one slice unless M exceeds what a thread's
     // accumulators cover: 4096 columns for E <= 8, 2048 for E <= 16, 1024 for E <= 32)
 #define PARM_WG_LAUNCH(EM, NBV)                                                                              \
@@ -843,7 +908,14 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
             attr = true;                                                                                     \
         }                                                                                                    \
         const dim3 gr(grid, (nb + (NBV) - 1) / (NBV));                                                       \
-        launch_k(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, ws); \
+        if ((long long)gr.x * gr.y <= kNumSMs) {                                                             \
+            fused = launch_coop(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, \
+                                n, M, E, ws, dwgT, accumulate, sync) == cudaSuccess;                         \
+            if (!fused) (void)cudaGetLastError();   /* not co-resident here: the two-launch form */          \
+        }                                                                                                    \
+        if (!fused)                                                                                          \
+            launch_k(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, ws, \
+                     (float*)nullptr, 0, (int*)nullptr);                                                     \
     } while (0)
     if (E <= 8 && nb == 1)
         PARM_WG_LAUNCH(8, 1);
@@ -857,8 +929,10 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
         PARM_WG_LAUNCH(32, 1);
 #undef PARM_WG_LAUNCH
     PARM_CHECK_LAUNCH("gate_wgrad_partial");
-    launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, ws, grid, len, dwgT, accumulate);
-    PARM_CHECK_LAUNCH("gate_wgrad_sum");
+    if (!fused) {
+        launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, ws, grid, len, dwgT, accumulate);
+        PARM_CHECK_LAUNCH("gate_wgrad_sum");
+    }
     return 0;
 }
 

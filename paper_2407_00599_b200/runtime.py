@@ -350,7 +350,7 @@ class MoELayer:
         b["dlogits"] = torch.zeros(nr, d.E, dtype=torch.float32, device=dev)
         need = K.gate_wgrad_workspace(d.n, d.Mp, d.E)
         if self._ws_gate is None or self._ws_gate.numel() * 4 < need:
-            self._ws_gate = torch.empty(max(1, need // 4), dtype=torch.float32, device=dev)
+            self._ws_gate = torch.zeros(max(1, need // 4), dtype=torch.float32, device=dev)   # counters start at zero
         s.bufs[schedule] = b
         return b
 

@@ -521,14 +521,15 @@ def test_input_validation_messages(cuda_lib):
                                    (1024, 8192, 2), (600, 3072, 16), (500, 1536, 32)])   # wide M: column slices
 def test_gate_wgrad_matches_f64(cuda_lib, n, M, E):
     """dWg^T (E, M) = dlogits^T x: one partial per SM over contiguous token ranges, summed in a
-    fixed order -- against the f64 product, and bit-identical run to run (deterministic)."""
+    fixed order (same launch behind a grid barrier, or a second launch for wide M) -- against the
+    f64 product, and bit-identical run to run (deterministic)."""
     from paper_2407_00599_b200 import kernels as K
 
     rng = np.random.default_rng(n + M)
     xh = O.round_bf16(rng.normal(size=(n, M)))
     dl = rng.normal(size=(n, E)).astype(np.float32)
     x, dlt = _t(xh), torch.from_numpy(dl).cuda()
-    ws = torch.empty(K.gate_wgrad_workspace(n, M, E) // 4, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(K.gate_wgrad_workspace(n, M, E) // 4, dtype=torch.float32, device="cuda")
     out = torch.full((E, M), float("nan"), device="cuda")
     K.gate_wgrad(x, dlt, out, ws)
     ref = dl.astype(np.float64).T @ xh
@@ -538,6 +539,7 @@ def test_gate_wgrad_matches_f64(cuda_lib, n, M, E):
     assert torch.equal(out, again)
     K.gate_wgrad(x, dlt, again, ws, accumulate=True)
     torch.testing.assert_close(again, 2 * out, rtol=1e-6, atol=1e-6)
+    assert int(torch.count_nonzero(ws.view(torch.int32)[-4:])) == 0   # grid-barrier counters left zeroed
 
 
 @pytest.mark.parametrize("world", ["local", "peer"])

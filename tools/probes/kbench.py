@@ -97,7 +97,7 @@ def main():
     route()
     dl = torch.randn(n, E, generator=g, device=dev)
     dwg = torch.empty(E, M, device=dev)
-    ws = torch.empty(K.gate_wgrad_workspace(n, M, E) // 4, device=dev)
+    ws = torch.zeros(K.gate_wgrad_workspace(n, M, E) // 4, device=dev)
     wgrad = lambda: K.gate_wgrad(x, dl, dwg, ws)  # noqa: E731
     view = K.SlotView(out, e_local=E, stride_i=cap * M, stride_slo=M)
     y = torch.empty(n, M, dtype=torch.bfloat16, device=dev)
