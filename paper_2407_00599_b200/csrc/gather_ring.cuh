@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) combine_fwd_ring(const __grid_
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane * 8 + h * 256;
-                        if (c < cols) fma_bf16x8(acc[h], b.w[j], lds16(sb + (j * NP + p) * kCols + c));
+                        if (c < cols) fma2_bf16x8(acc[h], b.w[j], lds16(sb + (j * NP + p) * kCols + c));
                     }
                 }
             const long long t = base + i * nw;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane * 8 + h * 256;
-                        if (c < cols) fma_bf16x8(acc[h], 1.0f, lds16(sb + (j * NP + p) * kCols + c));
+                        if (c < cols) add_bf16x8(acc[h], lds16(sb + (j * NP + p) * kCols + c));
                     }
                 }
             if (gate) {
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane * 8 + h * 256;
-                        if (c < cols) fma_bf16x8(acc[h], d, ldg16(wgT + (long long)e * M + c0 + c));
+                        if (c < cols) fma2_bf16x8(acc[h], d, ldg16(wgT + (long long)e * M + c0 + c));
                     }
                 }
             }

@@ -96,6 +96,42 @@ __device__ __forceinline__ void fma_bf16x8(float* acc, float w, const int4& v) {
     for (int u = 0; u < 8; ++u) acc[u] = fmaf(w, f[u], acc[u]);
 }
 
+// acc[u] += v[u] for 8 bf16 values: the sm_100 mixed-precision FMA (f32 += bf16 x bf16, the bf16
+// operand read from its half of the 32-bit register) times 1.0 -- no conversion instructions,
+// and the same single rounding as fmaf(1.0f, float(v[u]), acc[u]).
+__device__ __forceinline__ void add_bf16x8(float* acc, const int4& v) {
+    const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+    const unsigned short one = 0x3F80;   // bf16 1.0
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const unsigned short lo = (unsigned short)(w[i] & 0xFFFFu), hi = (unsigned short)(w[i] >> 16);
+        asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc[2 * i]) : "h"(lo), "h"(one));
+        asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc[2 * i + 1]) : "h"(hi), "h"(one));
+    }
+}
+
+// acc = fmaf(float(a[u]), float(b[u]), acc) for u = 0..7 in order, as eight mixed-precision FMAs
+// on the bf16 halves (no conversions; the bf16 x bf16 product is exact either way).
+__device__ __forceinline__ void dot_bf16x8(float& acc, const int4& a, const int4& b) {
+    const uint32_t x[4] = {(uint32_t)a.x, (uint32_t)a.y, (uint32_t)a.z, (uint32_t)a.w};
+    const uint32_t y[4] = {(uint32_t)b.x, (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        asm("fma.rn.f32.bf16 %0, %1, %2, %0;"
+            : "+f"(acc)
+            : "h"((unsigned short)(x[i] & 0xFFFFu)), "h"((unsigned short)(y[i] & 0xFFFFu)));
+        asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc) : "h"((unsigned short)(x[i] >> 16)), "h"((unsigned short)(y[i] >> 16)));
+    }
+}
+
+// acc[u] = fmaf(w, float(v[u]), acc[u]) for 8 bf16 values, as four FFMA2 (same roundings).
+__device__ __forceinline__ void fma2_bf16x8(float* acc, float w, const int4& v) {
+    const uint32_t x[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        ffma2(acc[2 * i], acc[2 * i + 1], __uint_as_float(x[i] << 16), __uint_as_float(x[i] & 0xFFFF0000u), w);
+}
+
 #include "gather_ring.cuh"
 
 
@@ -128,7 +164,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_fwd_kernel(const __gri
 #pragma unroll
                 for (int j = 0; j < KT; ++j)       // j ascending, like the reference's _combine
 #pragma unroll
-                    for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], pk.w[j], buf[j][i]);
+                    for (int i = 0; i < kChunks; ++i) fma2_bf16x8(acc[i], pk.w[j], buf[j][i]);
             }
 #pragma unroll
             for (int i = 0; i < kChunks; ++i) {
@@ -197,21 +233,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) combine_bwd_kernel(const bf16*
                 int4 buf[KT][kChunks];
                 load_picks<KT>(y, pk, p, g0, lane, M, buf);
 #pragma unroll
-                for (int i = 0; i < kChunks; ++i) {
-                    Vec8 g8;
-                    *reinterpret_cast<int4*>(&g8) = gv[i];
-                    float g[8];
-                    vec8_to_f32(g8, g);
+                for (int i = 0; i < kChunks; ++i)
 #pragma unroll
-                    for (int j = 0; j < KT; ++j) {
-                        Vec8 y8;
-                        *reinterpret_cast<int4*>(&y8) = buf[j][i];
-                        float f[8];
-                        vec8_to_f32(y8, f);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) dw[j] = fmaf(g[u], f[u], dw[j]);
-                    }
-                }
+                    for (int j = 0; j < KT; ++j) dot_bf16x8(dw[j], gv[i], buf[j][i]);
             }
             if (SC) {   // the dy dispatch: w_j * dOut[t] into the pick's slot row
 #pragma unroll
@@ -311,7 +335,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
 #pragma unroll
                 for (int b = 0; b < TB; ++b)
 #pragma unroll
-                    for (int j = 0; j < KT; ++j) fma_bf16x8(acc[b], 1.0f, buf[b][j]);
+                    for (int j = 0; j < KT; ++j) add_bf16x8(acc[b], buf[b][j]);
             }
             if (dlogits != nullptr) {
 #pragma unroll 2
@@ -320,7 +344,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) dispatch_bwd_kernel(const __gr
 #pragma unroll
                     for (int b = 0; b < TB; ++b) {
                         const float d = t0 + b < n ? __ldg(dlogits + (t0 + b) * E + e) : 0.0f;
-                        fma_bf16x8(acc[b], d, wv);
+                        fma2_bf16x8(acc[b], d, wv);
                     }
                 }
             }
@@ -357,7 +381,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) esp_sum_kernel(const __grid_co
                 int4 buf[1][kChunks];
                 load_picks<1>(y, pk, p, g0, lane, M, buf);
 #pragma unroll
-                for (int i = 0; i < kChunks; ++i) fma_bf16x8(acc[i], 1.0f, buf[0][i]);
+                for (int i = 0; i < kChunks; ++i) add_bf16x8(acc[i], buf[0][i]);
             }
 #pragma unroll
             for (int i = 0; i < kChunks; ++i) {
