@@ -589,36 +589,66 @@ __global__ void __launch_bounds__(kRdWarps * 32) route_dispatch_kernel(
     }
     __syncthreads();   // slot_idx of the CTA's tokens visible to every warp (global memory, same CTA)
     // ---- 3. token rows -> slot rows: wait for the rows streamed in since step 0, store each
-    //        to its kept picks' slot rows (bulk stores), refill the ring
-    if (lane == 0 && items > 0) {
+    //        to its kept picks' slot rows (bulk stores), refill the ring.  The picks of the
+    //        warp's next 32 tokens are fetched at once (lane i: token i, every pick's slot row
+    //        as a destination offset, -1 when not stored) and broadcast with shuffles, so the
+    //        issuing lane never waits on a dependent load per token.
+    if (items > 0) {
+        long long dst[8];   // k <= 8
         for (int it = 0; it < items; ++it) {
-            if (it + kRdStages - kRdLag < items) {
-                // the stage being refilled held item it - kRdLag: its stores must have read it
-                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kRdLag - 1) : "memory");
-                rd_load(it + kRdStages - kRdLag);
-            }
-            const int t = tok_of(it), ch = it % nch, c0 = ch * kRdCols;
-            const int cols = min(kRdCols, M - c0);
-            const uint32_t st = (uint32_t)it % kRdStages;
-            ring::bar_wait(bar0 + 8 * st, ((uint32_t)it / kRdStages) & 1);
-            const uint32_t src = ring::saddr(ring + st * kRdCols * 2);
-            for (int j = 0; j < k; ++j) {
-                const int sl = slot_idx[(long long)t * k + j];
-                if (sl < slot_lo || sl >= slot_lo + slots_out) continue;
-                const int e = __ldg(expert_idx + (long long)t * k + j);
-                const int sp = sl - slot_lo;
-                if (peer) {
-                    int ep;
-                    const long long off = slot_inbuf(dstv, e, sp, ep);
-                    for (int pp = 0; pp < dstv.n_p; ++pp)
-                        bulk_s2g(const_cast<bf16*>(slot_base(dstv, ep, pp)) + off + c0, src, cols * 2);
-                } else {
-                    bulk_s2g(out + (long long)e * out_stride_e + (long long)sp * out_stride_s + c0, src, cols * 2);
+            const int ti = it / nch, ch = it - ti * nch;
+            if ((ti & 31) == 0 && ch == 0) {   // fetch picks of tokens ti .. ti + 31 of this warp
+                const int tl = ti + lane;
+                const bool ok = tl < my_tok;
+                const int t = ok ? t_begin + warp + tl * kRdWarps : 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    dst[j] = -1;
+                    if (!ok || j >= k) continue;
+                    const int sl = slot_idx[(long long)t * k + j];
+                    if (sl < slot_lo || sl >= slot_lo + slots_out) continue;
+                    const int e = __ldg(expert_idx + (long long)t * k + j);
+                    const int sp = sl - slot_lo;
+                    if (peer) {
+                        int ep;
+                        const long long off = slot_inbuf(dstv, e, sp, ep);
+                        dst[j] = ((long long)ep << 48) | off;   // (owner, in-buffer offset)
+                    } else {
+                        dst[j] = (long long)e * out_stride_e + (long long)sp * out_stride_s;
+                    }
                 }
             }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            long long d[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d[j] = ring::shfl_ll(dst[j], ti & 31);
+            if (lane == 0) {
+                if (it + kRdStages - kRdLag < items) {
+                    // the stage being refilled held item it - kRdLag: its stores must have read it
+                    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kRdLag - 1) : "memory");
+                    rd_load(it + kRdStages - kRdLag);
+                }
+                const int c0 = ch * kRdCols;
+                const int cols = min(kRdCols, M - c0);
+                const uint32_t st = (uint32_t)it % kRdStages;
+                ring::bar_wait(bar0 + 8 * st, ((uint32_t)it / kRdStages) & 1);
+                const uint32_t src = ring::saddr(ring + st * kRdCols * 2);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (d[j] < 0) continue;
+                    if (peer) {
+                        const int ep = (int)(d[j] >> 48);
+                        const long long off = d[j] & ((1ll << 48) - 1);
+                        for (int pp = 0; pp < dstv.n_p; ++pp)
+                            bulk_s2g(const_cast<bf16*>(slot_base(dstv, ep, pp)) + off + c0, src, cols * 2);
+                    } else {
+                        bulk_s2g(out + d[j] + c0, src, cols * 2);
+                    }
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            __syncwarp();
         }
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     // ---- 4. zero rows up to each expert's last GEMM tile; unfilled slot_src entries
     {
