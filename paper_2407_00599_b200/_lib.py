@@ -133,8 +133,10 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     return lib
 
 
-# Kernel launches each entry point issues on success (bench.py's gpu_launches).
-LAUNCHES_PER_CALL = {"parm_gate_wgrad": 2}
+# Kernel launches each entry point issues on success when not 1 (bench.py's gpu_launches).
+# (parm_gate_wgrad: 1 -- the partial sum runs in the same cooperative launch whenever its CTAs
+# fit on the SMs at once, true up to M = 4096 at E <= 8; wider launches add a second kernel.)
+LAUNCHES_PER_CALL: dict = {}
 launch_count = 0
 
 

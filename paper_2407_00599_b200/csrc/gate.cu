@@ -867,10 +867,13 @@ static int gate_wgrad_grid(int n) {
     return std::max(g, (n + kWgMaxTok - 1) / kWgMaxTok);          // <= kWgMaxTok tokens per CTA
 }
 
-// partials, then two barrier counters (zero before first use; the kernel leaves them zero)
-static size_t gate_wgrad_part_bytes(int n, int M, int E) { return (size_t)gate_wgrad_grid(n) * M * E * sizeof(float); }
+// Workspace: two barrier counters (16 bytes, zero before first use; the kernel leaves them zero)
+// at a fixed offset -- calls with different n share one workspace -- then the partials.
+constexpr size_t kWgSyncBytes = 16;
 
-size_t gate_wgrad_workspace(int n, int M, int E) { return gate_wgrad_part_bytes(n, M, E) + 4 * sizeof(int); }
+size_t gate_wgrad_workspace(int n, int M, int E) {
+    return kWgSyncBytes + (size_t)gate_wgrad_grid(n) * M * E * sizeof(float);
+}
 
 int sum_chunks(const float* src, int chunks, long long len, float* out, int accumulate, cudaStream_t s) {
     PARM_CHECK_ARG(src != nullptr && out != nullptr && chunks >= 1 && len >= 0, "sum_chunks: bad arguments");
@@ -895,7 +898,8 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
     auto X = reinterpret_cast<const bf16*>(x);
     const int smem = kWgStages * kWgStageBytes;
     const int nb = (M + kWgBlock - 1) / kWgBlock;
-    int* sync = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + gate_wgrad_part_bytes(n, M, E));
+    int* sync = reinterpret_cast<int*>(ws);
+    float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kWgSyncBytes);
     bool fused = false;   // the sum in the same launch when every CTA fits at once (1 CTA per SM)
     // column slices of NBV * 1024 columns over grid.y (one slice unless M exceeds what a thread's
     // accumulators cover: 4096 columns for E <= 8, 2048 for E <= 16, 1024 for E <= 32)
@@ -910,11 +914,11 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
         const dim3 gr(grid, (nb + (NBV) - 1) / (NBV));                                                       \
         if ((long long)gr.x * gr.y <= kNumSMs) {                                                             \
             fused = launch_coop(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, \
-                                n, M, E, ws, dwgT, accumulate, sync) == cudaSuccess;                         \
+                                n, M, E, part, dwgT, accumulate, sync) == cudaSuccess;                       \
             if (!fused) (void)cudaGetLastError();   /* not co-resident here: the two-launch form */          \
         }                                                                                                    \
         if (!fused)                                                                                          \
-            launch_k(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, ws, \
+            launch_k(gate_wgrad_partial_kernel<EM, NBV>, gr, 2 * kWgThreads, smem, s, X, ldx, dlogits, n, M, E, part, \
                      (float*)nullptr, 0, (int*)nullptr);                                                     \
     } while (0)
     if (E <= 8 && nb == 1)
@@ -930,7 +934,7 @@ int gate_wgrad(const void* x, long long ldx, const float* dlogits, int n, int M,
 #undef PARM_WG_LAUNCH
     PARM_CHECK_LAUNCH("gate_wgrad_partial");
     if (!fused) {
-        launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, ws, grid, len, dwgT, accumulate);
+        launch_k(sum_partials_kernel, (int)((len + 31) / 32), 256, 0, s, part, grid, len, dwgT, accumulate);
         PARM_CHECK_LAUNCH("gate_wgrad_sum");
     }
     return 0;

@@ -14,8 +14,8 @@
 // several KB in flight without holding them in registers.  The routing of a
 // warp's tokens is fetched once, one token per lane, and broadcast with
 // shuffles.  Arithmetic, order of accumulation and outputs are those of the
-// register kernels; the views must be local (n_peer == 0) with every row
-// 16-byte aligned -- otherwise the host launches the register kernels.
+// register kernels; every row must be 16-byte aligned (local or peer views) --
+// otherwise the host launches the register kernels.
 // (Measured against an 8-token-group variant that issued one bulk copy per
 // (token, pick) lane: bulk-copy operands must be warp-uniform, so per-lane
 // copies serialise in a waterfall loop -- 22 vs 14 us for combine_fwd.)
@@ -304,10 +304,17 @@ __global__ void __launch_bounds__(kRowThreads, 3) dispatch_bwd_ring(const __grid
 }
 
 // ---------------------------------------------------------------- host side
+// Every row 16-byte aligned.  Peer views qualify too: cp.async.bulk reads a peer GPU's
+// NVLink-mapped memory like local HBM (tools/probes/peer_bulk_probe.cu: scattered 1 KB rows from
+// the peer at 705 GB/s, byte-exact), so the pulls of the peer transport stream through the ring.
 inline bool view_aligned(const SlotView& v) {
-    if (v.n_peer != 0) return false;   // bulk copies read local HBM only
-    return v.stride_ep % 8 == 0 && v.stride_i % 8 == 0 && v.stride_p % 8 == 0 && v.stride_shi % 8 == 0 &&
-           v.stride_slo % 8 == 0 && (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
+    if (v.stride_i % 8 != 0 || v.stride_shi % 8 != 0 || v.stride_slo % 8 != 0) return false;
+    if (v.n_peer != 0) {
+        for (int i = 0; i < v.n_peer; ++i)
+            if (reinterpret_cast<uintptr_t>(v.peer[i]) & 15) return false;
+        return true;
+    }
+    return v.stride_ep % 8 == 0 && v.stride_p % 8 == 0 && (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
 }
 
 // Grid of a ring kernel: as many CTAs as fit on the SMs (by shared memory),

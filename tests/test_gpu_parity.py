@@ -539,7 +539,25 @@ def test_gate_wgrad_matches_f64(cuda_lib, n, M, E):
     assert torch.equal(out, again)
     K.gate_wgrad(x, dlt, again, ws, accumulate=True)
     torch.testing.assert_close(again, 2 * out, rtol=1e-6, atol=1e-6)
-    assert int(torch.count_nonzero(ws.view(torch.int32)[-4:])) == 0   # grid-barrier counters left zeroed
+    assert int(torch.count_nonzero(ws.view(torch.int32)[:4])) == 0   # grid-barrier counters left zeroed
+
+
+def test_gate_wgrad_workspace_shared_across_token_counts(cuda_lib):
+    """One workspace serves calls with different token counts (S1 passes the MP token slice, the
+    baseline all tokens): the grid-barrier counters sit at a fixed offset, so no call reads
+    another call's partials as its counters."""
+    from paper_2407_00599_b200 import kernels as K
+
+    M, E = 1024, 8
+    ws = torch.zeros(K.gate_wgrad_workspace(8192, M, E) // 4, dtype=torch.float32, device="cuda")
+    rng = np.random.default_rng(7)
+    for n in (4096, 8192, 300, 8192, 4096, 2048):
+        xh = O.round_bf16(rng.normal(size=(n, M)))
+        dl = rng.normal(size=(n, E)).astype(np.float32)
+        out = torch.full((E, M), float("nan"), device="cuda")
+        K.gate_wgrad(_t(xh), torch.from_numpy(dl).cuda(), out, ws)
+        assert _norm_err(out.cpu().numpy(), dl.astype(np.float64).T @ xh) <= 1e-6, n
+    assert int(torch.count_nonzero(ws.view(torch.int32)[:4])) == 0
 
 
 @pytest.mark.parametrize("world", ["local", "peer"])
