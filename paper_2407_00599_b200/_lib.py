@@ -97,7 +97,7 @@ SIGNATURES = {
                                  _c_int, ctypes.POINTER(RowFanC), _c_ll, _c_ll, _vp]),
 }
 
-ABI_VERSION = 15
+ABI_VERSION = 16
 
 
 class ParmError(RuntimeError):
