@@ -55,11 +55,17 @@ def main():
         tot[e.name[:70]] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
         cnt[e.name[:70]] += 1
     rows = sorted(tot.items(), key=lambda kv: -kv[1])
+    # every kernel of the last profiled step in launch order, with its duration (barriers by position)
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    evs.sort(key=lambda e: e.time_range.start)
+    per_step = len(evs) // steps
+    seq = [(e.name[:40], round(e.time_range.end - e.time_range.start, 2)) for e in evs[-per_step:]]
     if rank == 0:
         out = {"n": n, "schedule": schedule, "steps": steps,
                "kernels_us_per_step": {k: round(v / steps, 2) for k, v in rows},
                "launches_per_step": {k: cnt[k] / steps for k, _ in rows},
-               "sum_us_per_step": round(sum(tot.values()) / steps, 1)}
+               "sum_us_per_step": round(sum(tot.values()) / steps, 1),
+               "last_step_sequence_us": seq}
         print(json.dumps(out, indent=1))
     dist.barrier()
     dist.destroy_process_group()
