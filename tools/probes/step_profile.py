@@ -2,7 +2,7 @@
 replays of the bench layer): where the step goes at N > 1, where ncu (one process) cannot look.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \\
-        tools/probes/step_profile.py N [schedule]
+        tools/probes/step_profile.py N [schedule] [peer|peer-<s1_return>|nccl]
 """
 import collections
 import json
@@ -17,12 +17,13 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2407_00599_b200.config import MoEConfig  # noqa: E402
 from paper_2407_00599_b200.runtime import MoELayer  # noqa: E402
-from paper_2407_00599_b200.world import PeerWorld  # noqa: E402
+from paper_2407_00599_b200.world import NcclWorld, PeerWorld  # noqa: E402
 
 
 def main():
     n = int(sys.argv[1])
     schedule = sys.argv[2] if len(sys.argv) > 2 else "s1"
+    transport = sys.argv[3] if len(sys.argv) > 3 else "peer"
     rank, lrank = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lrank)
     dev = torch.device("cuda", lrank)
@@ -30,7 +31,9 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     cfg = MoEConfig(**bench.C2)
     layout = bench.layout_for(n)
-    layer = MoELayer(cfg, layout, PeerWorld(layout, dev))
+    peer = transport.startswith("peer")
+    opts = {"s1_return": transport.split("-", 1)[1]} if "-" in transport else {}
+    layer = MoELayer(cfg, layout, PeerWorld(layout, dev) if peer else NcclWorld(layout, dev), peer=peer, **opts)
     layer.init_random(0)
     g = torch.Generator(device=dev).manual_seed(1000 + rank // layout.mp_size)
     x = torch.randn(cfg.tokens_per_rank, cfg.embed_dim, generator=g, device=dev).to(torch.bfloat16)
@@ -61,7 +64,7 @@ def main():
     per_step = len(evs) // steps
     seq = [(e.name[:40], round(e.time_range.end - e.time_range.start, 2)) for e in evs[-per_step:]]
     if rank == 0:
-        out = {"n": n, "schedule": schedule, "steps": steps,
+        out = {"n": n, "schedule": schedule, "transport": transport, "steps": steps,
                "kernels_us_per_step": {k: round(v / steps, 2) for k, v in rows},
                "launches_per_step": {k: cnt[k] / steps for k, _ in rows},
                "sum_us_per_step": round(sum(tot.values()) / steps, 1),
